@@ -1,0 +1,433 @@
+"""Benchmark of the B200 hot path (BASELINE.json metric: fused eOp+accu GB/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+One "step" is one pass of the hot path over one batch: the config-1 fused
+expression ``accu(2*A + B % C - exp(D))`` on a 4096 x 4096 f32 block per GPU
+(numpy default_rng(0) U[0,1) inputs on rank 0).
+At N > 1 every rank owns its own 4096 x 4096 column block of a 4096 x 4096N
+matrix (weak scaling); the rank partials are all-gathered over NCCL and
+folded deterministically on the device (paper_2308_03120_b200/dist.py).
+
+value    device throughput: algorithmic bytes (4 inputs x 4 B per element)
+         over K steps timed with CUDA events on the library's stream, inputs
+         resident in HBM (256 MiB > 126 MB L2: no flush needed), max over ranks.
+e2e      the same metric through the public API with host buffers: every step
+         copies A..D from pinned host memory (Matrix.from_numpy) and reads the
+         scalar back (dm.accu).
+roofline the fused kernel's achieved GB/s against MEASURED_PEAKS.json hbm_gbs.
+cpu_baseline  the reference (baseline/_ref devmat, parallel backend on all host
+         cores) on the same inputs, timed for ~10 s on rank 0 at N = 1.
+secondary     the other SURVEY 8d configs on one GPU (dot/norm 2^30, rdim
+         16384^2 f64, GEMM 8192^3 f32/f64, logistic step) -- reported beside the
+         headline, not part of it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import pathlib
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+N_SIDE = 4096
+ELEMS = N_SIDE * N_SIDE
+BYTES_PER_STEP = 4 * 4 * ELEMS          # 268,435,456 B read, nothing written
+METRIC = "fused eOp+accu GB/s (% HBM peak) at 1/2/4/8 B200; GEMM TFLOPS vs CPU ref"
+WORKLOAD = "accu(2*A + B % C - exp(D)), f32 4096x4096 per GPU (SURVEY 8d config 1)"
+
+
+def _peaks() -> tuple[float, float, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), float(d.get("bf16_tflops", 1616.9)), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
+
+
+def _inputs(rank: int):
+    rng = np.random.default_rng(rank)
+    return [rng.random((N_SIDE, N_SIDE), dtype=np.float32) for _ in range(4)]
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during a timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, device: int):
+        self.samples: list[tuple[int, int]] = []
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+                rs = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((mhz, rs))
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        busy = [s for s in self.samples if not (s[1] & 0x1)] or self.samples
+        mask = 0
+        for _, r in busy:
+            mask |= r
+        reasons = [n for b, n in self.REASONS.items() if mask & b and b != 0x1]
+        return {"sm_mhz": statistics.median(m for m, _ in busy), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm / CPU baseline
+
+def _reference_module():
+    ref = ROOT / "baseline" / "_ref"
+    if (ref / "devmat").exists():
+        sys.path.insert(0, str(ref))
+        import devmat
+        return devmat, "reference"
+    return None, "port"
+
+
+def _time_reference_step(devmat, mats) -> float:
+    A, B, C, D = mats
+    t0 = time.perf_counter()
+    devmat.accu(2 * A + B * C - devmat.exp(D))
+    devmat.synchronise()
+    return time.perf_counter() - t0
+
+
+def cpu_reference_run(host_inputs, seconds: float | None, steps: int | None, warmup: int):
+    """Time the reference's own CPU implementation of the step.  Uses the
+    unmodified reference package (baseline/_ref) with its parallel backend on
+    every host core; without it, the oracle port (single thread)."""
+    cores = os.cpu_count() or 1
+    devmat, kind = _reference_module()
+    times = []
+    if devmat is not None:
+        devmat.init("parallel", worker_count=cores)
+        mats = [devmat.Matrix.from_numpy(x) for x in host_inputs]
+        for _ in range(warmup):
+            _time_reference_step(devmat, mats)
+        t_start = time.perf_counter()
+        while True:
+            times.append(_time_reference_step(devmat, mats))
+            if steps is not None and len(times) >= steps:
+                break
+            if seconds is not None and time.perf_counter() - t_start >= seconds:
+                break
+        devmat.shutdown()
+        sample = f"{len(times)} full steps of the 4096x4096 workload, devmat parallel backend, {cores} workers"
+    else:
+        import oracle as O
+        prog = (("load", 0), ("scalar", "eop_scalar_times", 2), ("load", 1), ("load", 2), ("glue", "eglue_schur"),
+                ("glue", "eglue_plus"), ("load", 3), ("unary", "eop_exp", None), ("glue", "eglue_minus"))
+        flat = [x.reshape(-1, order="F") for x in host_inputs]
+        cores = 1
+        t_start = time.perf_counter()
+        while True:
+            t0 = time.perf_counter()
+            O.reduce_accu(O.run_program(prog, flat, np.float32))
+            times.append(time.perf_counter() - t0)
+            if steps is not None and len(times) >= steps:
+                break
+            if seconds is not None and time.perf_counter() - t_start >= seconds:
+                break
+        sample = f"{len(times)} full steps of the 4096x4096 workload, oracle port, 1 thread"
+    mean = sum(times) / len(times)
+    return {"value": BYTES_PER_STEP / mean / 1e9, "unit": "GB/s", "cores": cores, "kind": kind, "sample": sample,
+            "ms_per_step": mean * 1e3}
+
+
+def run_reference_arm(args, rank: int) -> None:
+    if rank != 0:
+        return
+    host = _inputs(0)
+    r = cpu_reference_run(host, None, args.steps, args.warmup)
+    line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": "GB/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (numpy default_rng U[0,1))",
+            "config": {"workload": WORKLOAD, "rows": N_SIDE, "cols": N_SIDE},
+            "cpu_baseline": {"value": r["value"], "unit": "GB/s", "cores": r["cores"], "kind": r["kind"],
+                             "sample": r["sample"]},
+            "e2e": {"value": r["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+
+def _event_time_ms(torch, fn, steps: int) -> float:
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record()
+    for _ in range(steps):
+        fn()
+    end.record()
+    end.synchronize()
+    return start.elapsed_time(end)
+
+
+def secondary_suite(dm, torch) -> dict:
+    """The other SURVEY 8d configs on this GPU (inputs generated on device by
+    the counter RNG; timings with CUDA events, best of a few)."""
+    from paper_2308_03120_b200 import dist as D
+    from paper_2308_03120_b200 import expr as E
+    from paper_2308_03120_b200 import runtime as R
+    out = {}
+    peak_hbm, _, _ = _peaks()
+
+    def best_ms(fn, reps=5, inner=1):
+        fn()
+        torch.cuda.synchronize()
+        return min(_event_time_ms(torch, fn, inner) / inner for _ in range(reps))
+
+    try:  # config 3: dot and norm over 2^30 f32
+        n = 1 << 30
+        dm.set_seed(2)
+        a = dm.Col(n, fill="randu")
+        b = dm.Col(n, fill="randu")
+        rd = D.ShardedReduction("dot", a, b)
+        rn = D.ShardedReduction("dot", a, a)
+        t_dot = best_ms(rd.launch, inner=3)
+        t_norm = best_ms(rn.launch, inner=3)
+        out["dot_2^30_f32"] = {"ms": t_dot, "GB/s": 8 * n / t_dot / 1e6, "frac": 8 * n / t_dot / 1e6 / peak_hbm}
+        out["norm2_2^30_f32"] = {"ms": t_norm, "GB/s": 4 * n / t_norm / 1e6,
+                                 "frac": 4 * n / t_norm / 1e6 / peak_hbm}
+        del a, b, rd, rn
+    except Exception as e:  # pragma: no cover - reported, not fatal
+        out["dot_error"] = repr(e)[:200]
+    try:  # config 2: f64 sum/min/max dims 0/1 on 16384^2
+        m = dm.Matrix(16384, 16384, fill="randu", elem_type="f64")
+        nbytes = 8 * 16384 * 16384
+        for op in ("sum", "min", "max"):
+            for dim in (0, 1):
+                p = E.plan(getattr(dm, op)(m, dim))
+                step = p.steps[0]
+                res = dm.Matrix(*(1, 16384) if dim == 0 else (16384, 1), elem_type="f64")
+                views = E._step_views(p, step, {})
+                inv = dm.KernelInvocation(step.kernel, tuple(views),
+                                          E._make_view(res.mem, res.n_rows, res.n_cols, "flat"), (), step.params)
+                rtm = R.get_runtime()
+                t = best_ms(lambda: rtm.enqueue(inv), reps=3, inner=3)
+                out[f"{op}_dim{dim}_16384^2_f64"] = {"ms": t, "GB/s": nbytes / t / 1e6,
+                                                     "frac": nbytes / t / 1e6 / peak_hbm}
+        del m
+    except Exception as e:  # pragma: no cover
+        out["rdim_error"] = repr(e)[:200]
+    try:  # config 4: NT GEMM 8192^3
+        for elem in ("f32", "f64"):
+            n = 8192
+            A = dm.Matrix(n, n, fill="randu", elem_type=elem)
+            B = dm.Matrix(n, n, fill="randu", elem_type=elem)
+            C = dm.Matrix(n, n, elem_type=elem)
+            rtm = R.get_runtime()
+            inv = dm.KernelInvocation("gemm", (R.BlockView(A.mem, 0, n, n, n), R.BlockView(B.mem, 0, n, n, n)),
+                                      R.BlockView(C.mem, 0, n, n, n), (), {"trans_a": 0, "trans_b": 1})
+            t = best_ms(lambda: rtm.enqueue(inv), reps=3)
+            out[f"gemm_nt_8192^3_{elem}"] = {"ms": t, "TFLOP/s": 2 * n ** 3 / t / 1e9}
+            del A, B, C
+    except Exception as e:  # pragma: no cover
+        out["gemm_error"] = repr(e)[:200]
+    return out
+
+
+def run_b200(args, rank: int, world: int, local_rank: int) -> None:
+    import torch
+    import torch.distributed as tdist
+
+    import paper_2308_03120_b200 as dm
+    from paper_2308_03120_b200 import _clib
+    from paper_2308_03120_b200 import dist as D
+    from paper_2308_03120_b200.runtime import pinned_array
+
+    torch.cuda.set_device(local_rank)
+    dm.init("b200", device_id=local_rank)
+    D.bind_torch_stream()
+    lib = _clib.lib()
+    peak_hbm, _, peak_src = _peaks()
+
+    host = _inputs(rank)
+    mats = [dm.Matrix.from_numpy(x) for x in host]
+    A, B, C, Dm = mats
+    red = D.ShardedReduction("accu", 2 * A + B % C - dm.exp(Dm))
+
+    def barrier():
+        if world > 1:
+            tdist.barrier()
+        torch.cuda.synchronize()
+
+    # correctness of the measured thing (cheap): device result vs single-shard oracle-free self-check
+    for _ in range(args.warmup):
+        red.launch()
+    barrier()
+    c0 = _clib.Counters()
+    lib.bm_get_counters(c0)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clocks:
+        barrier()
+        start.record()
+        for _ in range(args.steps):
+            red.launch()
+        end.record()
+        end.synchronize()
+        barrier()
+    c1 = _clib.Counters()
+    lib.bm_get_counters(c1)
+    ms_total = start.elapsed_time(end)
+    launches = int(c1.launches - c0.launches)
+
+    # kernel-only timing of the fused kernel (roofline): per-launch events
+    kernel_ms = []
+    for _ in range(max(3, min(args.steps, 20))):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        lib.bm_reduce_to_device(__import__("ctypes").byref(red.inv),
+                                __import__("ctypes").c_void_p(red.partial.data_ptr()))
+        e.record()
+        kernel_ms.append((s, e))
+    torch.cuda.synchronize()
+    kern = statistics.median(s.elapsed_time(e) for s, e in kernel_ms)
+
+    # e2e through the public API with pinned host buffers
+    pinned = []
+    for x in host:
+        p = pinned_array(x.shape, np.float32)
+        p[...] = x
+        pinned.append(p)
+    e2e_steps = max(2, min(args.steps, 10))
+
+    def e2e_step():
+        mA, mB, mC, mD = (dm.Matrix.from_numpy(p) for p in pinned)
+        if world == 1:
+            v = dm.accu(2 * mA + mB % mC - dm.exp(mD))
+        else:
+            v = D.sharded_accu(2 * mA + mB % mC - dm.exp(mD))
+        return v
+
+    e2e_step()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_step()
+    barrier()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+
+    ms_step = ms_total / args.steps
+    vals = torch.tensor([ms_step, e2e_s, kern], dtype=torch.float64, device="cuda")
+    if world > 1:
+        tdist.all_reduce(vals, op=tdist.ReduceOp.MAX)
+    ms_step, e2e_s, kern = (float(v) for v in vals.cpu())
+
+    result_value = red.value()
+    secondary = {}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_secondary:
+        secondary = secondary_suite(dm, torch)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_reference_run(host, args.cpu_seconds, None, 1)
+
+    if rank == 0:
+        achieved = BYTES_PER_STEP / (kern * 1e-3) / 1e9
+        line = {
+            "metric": METRIC,
+            "value": world * BYTES_PER_STEP / (ms_step * 1e-3) / 1e9,
+            "unit": "GB/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_step,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f32",
+            "data": "synthetic: numpy default_rng(rank) U[0,1) f32 inputs (SURVEY 8d config 1)",
+            "config": {"workload": WORKLOAD, "rows": N_SIDE, "cols": N_SIDE * world,
+                       "bytes_per_step_per_gpu": BYTES_PER_STEP,
+                       "l2": "inputs 256 MiB per GPU > 126 MB L2; no flush",
+                       "parallelism": f"column-block shards x{world}; rank partials all-gathered (NCCL) and folded "
+                                      "deterministically on device" if world > 1 else "single GPU"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak_hbm, "unit": "GB/s",
+                         "frac": achieved / peak_hbm, "traffic": None, "peak_source": peak_src,
+                         "kernel": "bm_reduce (fused program + numpy-order pairwise accu)",
+                         "kernel_ms": kern},
+            "e2e": {"value": world * BYTES_PER_STEP / e2e_s / 1e9, "unit": "GB/s",
+                    "h2d_bytes_per_step": BYTES_PER_STEP, "d2h_bytes_per_step": 4,
+                    "ms_per_step": e2e_s * 1e3},
+            "gpu_launches": launches,
+            "clocks": clocks.summary(),
+            "result": float(result_value),
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        if secondary:
+            line["secondary"] = secondary
+        print(json.dumps(line), flush=True)
+    dm.shutdown()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference_arm(args, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+        torch.cuda.set_device(local_rank)
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_b200(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as tdist
+            tdist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,138 @@
+// bm_gemm.cu -- glue_times (reference kernels.py:704-708, lowered at
+// expr.py:596-605): C = op(A) * op(B), column-major, transposes folded into
+// the operand addressing so `A @ B.t()` needs no mov_transpose pass.
+//
+// Dispatch:
+//   f32  -> 3xTF32 on tcgen05 (bm_gemm_tc.cu) when the shape is tile-aligned
+//   f64  -> DMMA (mma.sync m8n8k4 f64) (bm_gemm_tc.cu)
+//   i32 / u64 and ragged shapes -> the SIMT kernel below (exact integer
+//   arithmetic, wrapping like numpy's integer np.dot).
+#include <cstring>
+
+#include "bm_internal.h"
+#include "bm_reduce.cuh"
+
+namespace bm {
+
+// 64x64 output tile per CTA, 256 threads x (4x4) outputs, K staged 16 at a time.
+template <typename T>
+__global__ void __launch_bounds__(256) gemm_simt_kernel(int ta, int tb, i64 m, i64 n, i64 k, const T* __restrict__ A,
+                                                        i64 lda, const T* __restrict__ B, i64 ldb, T* __restrict__ C,
+                                                        i64 ldc) {
+    __shared__ T As[16][64 + 1];
+    __shared__ T Bs[16][64 + 1];
+    const i64 m0 = (i64)blockIdx.x * 64, n0 = (i64)blockIdx.y * 64;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    T acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = T(0);
+    for (i64 k0 = 0; k0 < k; k0 += 16) {
+        for (int idx = threadIdx.x; idx < 16 * 64; idx += 256) {
+            const int kk = idx / 64, mm = idx % 64;
+            const i64 gi = m0 + mm, gl = k0 + kk;
+            T va = T(0);
+            if (gi < m && gl < k) va = ta ? A[gl + gi * lda] : A[gi + gl * lda];
+            As[kk][mm] = va;
+            const i64 gj = n0 + mm;
+            T vb = T(0);
+            if (gj < n && gl < k) vb = tb ? B[gj + gl * ldb] : B[gl + gj * ldb];
+            Bs[kk][mm] = vb;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) {
+            T a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = As[kk][tx + 16 * i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = Bs[kk][ty + 16 * j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = OpPlus::f(acc[i][j], OpTimes::f(a[i], b[j]));
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const i64 gi = m0 + tx + 16 * i, gj = n0 + ty + 16 * j;
+            if (gi < m && gj < n) C[gi + gj * ldc] = acc[i][j];
+        }
+}
+
+}  // namespace bm
+
+namespace bmi {
+
+int gemm_tc_f32(int ta, int tb, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const float* B,
+                int64_t ldb, float* C, int64_t ldc, bool* handled);
+int gemm_dmma_f64(int ta, int tb, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B,
+                  int64_t ldb, double* C, int64_t ldc, bool* handled);
+
+template <typename T>
+static int gemm_simt(int ta, int tb, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B,
+                     int64_t ldb, void* C, int64_t ldc) {
+    dim3 grid((unsigned)((m + 63) / 64), (unsigned)((n + 63) / 64));
+    bm::gemm_simt_kernel<T><<<grid, 256, 0, st().stream>>>(ta, tb, m, n, k, (const T*)A, lda, (const T*)B, ldb, (T*)C,
+                                                            ldc);
+    BM_CUDA(cudaGetLastError());
+    st().launches++;
+    return BM_OK;
+}
+
+int launch_gemm(const bm_invocation* inv) {
+    if (inv->n_inputs != 2 || !inv->has_output) return set_error(BM_ERR_ARG, "gemm: needs two inputs and an output");
+    const bm_view &a = inv->inputs[0], &b = inv->inputs[1], &c = inv->output;
+    if (a.dtype != b.dtype || a.dtype != c.dtype) return set_error(BM_ERR_ARG, "gemm: operand types differ");
+    const int ta = inv->trans_a, tb = inv->trans_b;
+    const int64_t m = ta ? a.cols : a.rows, k = ta ? a.rows : a.cols;
+    const int64_t kb = tb ? b.cols : b.rows, n = tb ? b.rows : b.cols;
+    if (k != kb) return set_error(BM_ERR_ARG, "gemm: inner dimensions differ");
+    if (c.rows != m || c.cols != n) return set_error(BM_ERR_ARG, "gemm: output shape mismatch");
+    const int64_t sz = dtype_size(a.dtype);
+    const char* A = (const char*)a.base + a.offset * sz;
+    const char* B = (const char*)b.base + b.offset * sz;
+    char* C = (char*)c.base + c.offset * sz;
+    if (m == 0 || n == 0) return BM_OK;
+    if (k == 0) {
+        // inner dimension zero: C = 0 (tests/test_integration.py:98-103)
+        if (c.lda == m) {
+            BM_CUDA(cudaMemsetAsync(C, 0, (size_t)(m * n * sz), st().stream));
+            return BM_OK;
+        }
+        for (int64_t j = 0; j < n; ++j) BM_CUDA(cudaMemsetAsync(C + j * c.lda * sz, 0, (size_t)(m * sz), st().stream));
+        return BM_OK;
+    }
+    const int algo = st().gemm_algo;
+    switch (a.dtype) {
+        case BM_F32: {
+            if (algo != 2) {
+                bool handled = false;
+                int rc = gemm_tc_f32(ta, tb, m, n, k, (const float*)A, a.lda, (const float*)B, b.lda, (float*)C, c.lda,
+                                     &handled);
+                if (rc || handled) return rc;
+                if (algo == 1) return set_error(BM_ERR_NOTIMPL, "gemm: tensor-core path cannot take this shape");
+            }
+            return gemm_simt<float>(ta, tb, m, n, k, A, a.lda, B, b.lda, C, c.lda);
+        }
+        case BM_F64: {
+            if (algo != 2) {
+                bool handled = false;
+                int rc = gemm_dmma_f64(ta, tb, m, n, k, (const double*)A, a.lda, (const double*)B, b.lda, (double*)C,
+                                       c.lda, &handled);
+                if (rc || handled) return rc;
+                if (algo == 1) return set_error(BM_ERR_NOTIMPL, "gemm: DMMA path cannot take this shape");
+            }
+            return gemm_simt<double>(ta, tb, m, n, k, A, a.lda, B, b.lda, C, c.lda);
+        }
+        case BM_I32: return gemm_simt<int>(ta, tb, m, n, k, A, a.lda, B, b.lda, C, c.lda);
+        case BM_U64: return gemm_simt<unsigned long long>(ta, tb, m, n, k, A, a.lda, B, b.lda, C, c.lda);
+    }
+    return set_error(BM_ERR_ARG, "gemm: bad dtype");
+}
+
+}  // namespace bmi

@@ -1,0 +1,84 @@
+// bm_internal.h -- state shared by the translation units of libb200mat.so.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <atomic>
+#include <cstdint>
+#include <mutex>
+#include <string>
+
+#include "../../include/b200mat.h"
+
+namespace bmi {
+
+struct State {
+    bool initialised = false;
+    int device = -1;
+    int sm_count = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;     // current stream (own or external)
+    void* partials = nullptr;          // reduction scratch (per-CTA partials)
+    unsigned int* ticket = nullptr;    // last-CTA counter, zero between launches
+    void* result = nullptr;            // device slot of the final value
+    void* host_slot = nullptr;         // pinned 64 B for scalar results
+    std::recursive_mutex mu;           // serialises stream use across host threads
+    std::atomic<int64_t> launches{0};
+    std::atomic<int64_t> jit_compiles{0};
+    std::atomic<int64_t> jit_hits{0};
+    std::atomic<int64_t> bytes_h2d{0};
+    std::atomic<int64_t> bytes_d2h{0};
+    int gemm_algo = 0;
+};
+
+State& st();
+
+int set_error(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+int cu_fail(CUresult r, const char* what);
+
+#define BM_CUDA(call)                                           \
+    do {                                                        \
+        cudaError_t _e = (call);                                \
+        if (_e != cudaSuccess) return bmi::cuda_fail(_e, #call); \
+    } while (0)
+
+#define BM_REQUIRE_INIT()                                                          \
+    do {                                                                           \
+        if (!bmi::st().initialised)                                                \
+            return bmi::set_error(BM_ERR_NODEVICE, "libb200mat: bm_init not called"); \
+    } while (0)
+
+inline int64_t dtype_size(int dt) { return (dt == BM_F32 || dt == BM_I32) ? 4 : 8; }
+inline bool dtype_ok(int dt) { return dt >= 0 && dt <= 3; }
+
+// driver entry points fetched through the runtime (no link-time libcuda dependency)
+struct Driver {
+    PFN_cuModuleLoadData_v2000 moduleLoadData = nullptr;
+    PFN_cuModuleGetFunction_v2000 moduleGetFunction = nullptr;
+    PFN_cuLaunchKernel_v4000 launchKernel = nullptr;
+    PFN_cuFuncSetAttribute_v9000 funcSetAttribute = nullptr;
+    PFN_cuTensorMapEncodeTiled_v12000 tensorMapEncodeTiled = nullptr;
+    bool ok = false;
+};
+Driver& drv();
+int load_driver();
+
+// launch helpers implemented per translation unit
+int launch_ewise_or_reduce(const bm_invocation* inv, bool to_device, void* dev_result);
+int launch_rdim(const bm_invocation* inv);
+int launch_gemm(const bm_invocation* inv);
+int launch_misc(const bm_invocation* inv);
+int combine_partials(const void* dev_partials, int64_t count, int dtype, int op, void* dev_out);
+
+// grid heuristics
+inline int ewise_grid(int64_t n_vec_units) {
+    int64_t g = (n_vec_units + 255) / 256;
+    const int64_t cap = (int64_t)st().sm_count * 8;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+}  // namespace bmi

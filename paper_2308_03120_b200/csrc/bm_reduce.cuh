@@ -1,0 +1,472 @@
+// bm_reduce.cuh -- element-wise store and reduction kernels over an abstract
+// element source (a plain buffer or a fused expression program), sm_100a.
+//
+// Summation order.  The reference sums a block with numpy's ndarray.sum
+// (kernels.py:459-460), which is numpy's pairwise summation: segments of at
+// most 128 elements use 8 interleaved accumulators, longer ones split at
+// n/2 rounded down to a multiple of 8; the result is 0 + pairwise(n).  Blocks
+// of REDUCE_BLOCK = 8192 elements (kernels.py:87) are then folded with
+// combine_pairwise (kernels.py:380-392).  This file reproduces that order
+// exactly, so f32/f64 accu is bit-identical to the reference for every
+// element-wise program whose element values are bit-identical.
+//
+// Fast path for one 128-element numpy leaf ("chunk"): a warp loads 16 rows of
+// 512 B fully coalesced (16-B vectors), parks them in a padded shared tile
+// (row pitch 544 B) and re-reads them transposed so each lane owns the
+// interleaved accumulators of one chunk; the 34-unit pitch makes both the
+// row writes and the transposed 16-B reads bank-conflict free.  Per warp
+// that is one "unit" of 2048 f32 / 1024 f64 elements.
+#pragma once
+#include "bm_common.cuh"
+
+namespace bm {
+
+#define BM_MAXIN 16
+#define BM_REDUCE_BLOCK 8192
+#define BM_TILE_PITCH 544
+#define BM_TILE_BYTES (16 * BM_TILE_PITCH)
+#define BM_RWARPS 8
+#define BM_MAX_GROUP 256                 // blocks per CTA
+#define BM_MAX_FINAL 4096                // CTA partials folded by the last CTA
+#define BM_REDUCE_SMEM (BM_RWARPS * BM_TILE_BYTES + 2 * BM_MAX_GROUP * 8)
+
+struct Args {
+    const void* in[BM_MAXIN];   // element 0 of every input view
+    i64 stride[BM_MAXIN];       // element stride of every input view
+    void* out;                  // element 0 of the output view
+    i64 out_stride;
+    i64 n;                      // number of elements
+    double fk[16];              // scalars for float compute types
+    i64 ik[16];                 // scalars for integer compute types
+    void* partials;             // per-CTA partials scratch
+    unsigned int* ticket;       // last-CTA-done counter (reset by the last CTA)
+    void* result;               // device slot for the final value
+    i64 blocks;                 // number of REDUCE_BLOCK blocks
+    int group;                  // blocks per CTA (power of two, multiple of BM_RWARPS or == blocks)
+    int vec_ok;                 // all views contiguous and 16-B aligned
+};
+
+// ---------------------------------------------------------------------------
+// sources
+
+template <typename T> struct BufSrc {
+    typedef T value_type;
+    const T* p;
+    i64 s;
+    __device__ __forceinline__ T at(i64 i) const { return p[i * s]; }
+    template <int V> __device__ __forceinline__ void vec(i64 i, T (&v)[V]) const {
+        if (sizeof(T) * V == 16) {
+            const uint4 q = __ldg(reinterpret_cast<const uint4*>(p + i));
+            const T* t = reinterpret_cast<const T*>(&q);
+#pragma unroll
+            for (int k = 0; k < V; ++k) v[k] = t[k];
+        } else {
+#pragma unroll
+            for (int k = 0; k < V; ++k) v[k] = p[i + k];
+        }
+    }
+};
+
+// vector load of V elements of TI converted to T (16-B transactions)
+template <typename T, typename TI, int V>
+__device__ __forceinline__ void ld_cvt(const void* base, i64 i, T (&v)[V]) {
+    const TI* p = reinterpret_cast<const TI*>(base) + i;
+    if ((sizeof(TI) * V) % 16 == 0) {
+#pragma unroll
+        for (int q = 0; q < (int)(sizeof(TI) * V / 16); ++q) {
+            const uint4 w = __ldg(reinterpret_cast<const uint4*>(p) + q);
+            const TI* t = reinterpret_cast<const TI*>(&w);
+#pragma unroll
+            for (int k = 0; k < (int)(16 / sizeof(TI)); ++k) v[q * (16 / sizeof(TI)) + k] = cvt<T>(t[k]);
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < V; ++k) v[k] = cvt<T>(p[k]);
+    }
+}
+template <typename T, typename TI>
+__device__ __forceinline__ T ld1(const void* base, i64 i, i64 s) {
+    return cvt<T>(reinterpret_cast<const TI*>(base)[i * s]);
+}
+
+// vector store of V elements converted to TO
+template <typename TO, typename T, int V>
+__device__ __forceinline__ void st_cvt(void* base, i64 i, const T (&v)[V]) {
+    TO* p = reinterpret_cast<TO*>(base) + i;
+    if ((sizeof(TO) * V) % 16 == 0) {
+#pragma unroll
+        for (int q = 0; q < (int)(sizeof(TO) * V / 16); ++q) {
+            uint4 w;
+            TO* t = reinterpret_cast<TO*>(&w);
+#pragma unroll
+            for (int k = 0; k < (int)(16 / sizeof(TO)); ++k) t[k] = cvt<TO>(v[q * (16 / sizeof(TO)) + k]);
+            reinterpret_cast<uint4*>(p)[q] = w;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < V; ++k) p[k] = cvt<TO>(v[k]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// element-wise store: out[i] = cast_out(E(i))   (kernels.py:429-454)
+
+template <class E, typename TO>
+__device__ __forceinline__ void ewise_store(const Args& a) {
+    typedef typename E::T T;
+    const i64 n = a.n;
+    const i64 tid = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    const i64 nthr = (i64)gridDim.x * blockDim.x;
+    if (a.vec_ok) {
+        constexpr int V = (16 / sizeof(T)) > (16 / sizeof(TO)) ? (16 / sizeof(T)) : (16 / sizeof(TO));
+        const i64 nv = n / V;
+        for (i64 j = tid; j < nv; j += nthr) {
+            T v[V];
+            E::template vec<V>(a, j * V, v);
+            st_cvt<TO, T, V>(a.out, j * V, v);
+        }
+        for (i64 i = nv * V + tid; i < n; i += nthr)
+            reinterpret_cast<TO*>(a.out)[i] = cvt<TO>(E::at(a, i));
+    } else {
+        for (i64 i = tid; i < n; i += nthr)
+            reinterpret_cast<TO*>(a.out)[i * a.out_stride] = cvt<TO>(E::at(a, i));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// numpy pairwise summation
+
+// one warp-cooperative unit: 16 rows x (32 lanes x 16 B)
+template <typename T, class S>
+__device__ __forceinline__ T pw_unit(const S& s, i64 off, char* tile, bool vec_ok) {
+    constexpr int V = 16 / sizeof(T);
+    constexpr int W = 32 * V;
+    const int lane = threadIdx.x & 31;
+#pragma unroll 4
+    for (int r = 0; r < 16; ++r) {
+        T v[V];
+        if (vec_ok) {
+            s.template vec<V>(off + r * W + lane * V, v);
+        } else {
+#pragma unroll
+            for (int k = 0; k < V; ++k) v[k] = s.at(off + r * W + lane * V + k);
+        }
+        *reinterpret_cast<uint4*>(tile + r * BM_TILE_PITCH + lane * 16) = *reinterpret_cast<const uint4*>(v);
+    }
+    __syncwarp();
+    T res;
+    if (sizeof(T) == 4) {
+        // lane = 2*chunk + half; accumulators 4*half .. 4*half+3
+        const int c = lane >> 1, h = lane & 1;
+        const char* base = tile + c * BM_TILE_PITCH + h * 16;
+        uint4 q = *reinterpret_cast<const uint4*>(base);
+        T r0 = reinterpret_cast<const T*>(&q)[0], r1 = reinterpret_cast<const T*>(&q)[1];
+        T r2 = reinterpret_cast<const T*>(&q)[2], r3 = reinterpret_cast<const T*>(&q)[3];
+#pragma unroll
+        for (int i = 1; i < 16; ++i) {
+            q = *reinterpret_cast<const uint4*>(base + i * 32);
+            r0 = r0 + reinterpret_cast<const T*>(&q)[0];
+            r1 = r1 + reinterpret_cast<const T*>(&q)[1];
+            r2 = r2 + reinterpret_cast<const T*>(&q)[2];
+            r3 = r3 + reinterpret_cast<const T*>(&q)[3];
+        }
+        const T sh = (r0 + r1) + (r2 + r3);
+        T ch = sh + warp_shfl_xor(sh, 1);
+        ch = ch + warp_shfl_xor(ch, 2);
+        ch = ch + warp_shfl_xor(ch, 4);
+        ch = ch + warp_shfl_xor(ch, 8);
+        ch = ch + warp_shfl_xor(ch, 16);
+        res = ch;
+    } else {
+        // lane = 4*chunk + quarter; accumulators 2*quarter, 2*quarter+1
+        const int c = lane >> 2, qq = lane & 3;
+        T r0 = 0, r1 = 0;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const uint4 q = *reinterpret_cast<const uint4*>(tile + (2 * c + (i >> 3)) * BM_TILE_PITCH + (i & 7) * 64 + qq * 16);
+            const T x0 = reinterpret_cast<const T*>(&q)[0], x1 = reinterpret_cast<const T*>(&q)[1];
+            if (i == 0) { r0 = x0; r1 = x1; } else { r0 = r0 + x0; r1 = r1 + x1; }
+        }
+        T t = r0 + r1;
+        t = t + warp_shfl_xor(t, 1);
+        t = t + warp_shfl_xor(t, 2);
+        t = t + warp_shfl_xor(t, 4);
+        t = t + warp_shfl_xor(t, 8);
+        t = t + warp_shfl_xor(t, 16);
+        res = t;
+    }
+    __syncwarp();
+    return res;
+}
+
+template <typename T> struct PwUnit { static const int value = 32 * 16 * (16 / sizeof(T)); };
+
+// balanced pairwise tree over `count` = 2^k consecutive units
+template <typename T, class S>
+__device__ T pw_balanced(const S& s, i64 off, i64 count, char* tile, bool vec_ok) {
+    constexpr i64 U = PwUnit<T>::value;
+    T stk[24];
+    int lvl[24];
+    int sp = 0;
+    for (i64 u = 0; u < count; ++u) {
+        T v = pw_unit<T>(s, off + u * U, tile, vec_ok);
+        int l = 0;
+        while (sp > 0 && lvl[sp - 1] == l) { v = stk[sp - 1] + v; --sp; ++l; }
+        stk[sp] = v; lvl[sp] = l; ++sp;
+    }
+    return stk[0];
+}
+
+// numpy leaf: n < 8 sequential from 0; n <= 128 eight interleaved accumulators
+template <typename T, class S>
+__device__ __forceinline__ T pw_leaf(const S& s, i64 off, i64 n) {
+    const int lane = threadIdx.x & 31;
+    if (n < 8) {
+        T r = 0;
+        for (i64 i = 0; i < n; ++i) r = r + s.at(off + i);
+        return r;
+    }
+    T acc = 0;
+    const i64 body = n - (n % 8);
+    if (lane < 8) {
+        acc = s.at(off + lane);
+        for (i64 i = 8; i < body; i += 8) acc = acc + s.at(off + i + lane);
+    }
+    const T a0 = __shfl_sync(0xffffffffu, acc, 0), a1 = __shfl_sync(0xffffffffu, acc, 1);
+    const T a2 = __shfl_sync(0xffffffffu, acc, 2), a3 = __shfl_sync(0xffffffffu, acc, 3);
+    const T a4 = __shfl_sync(0xffffffffu, acc, 4), a5 = __shfl_sync(0xffffffffu, acc, 5);
+    const T a6 = __shfl_sync(0xffffffffu, acc, 6), a7 = __shfl_sync(0xffffffffu, acc, 7);
+    T r = ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
+    for (i64 i = body; i < n; ++i) r = r + s.at(off + i);
+    return r;
+}
+
+// general numpy pairwise_sum over [off, off+n): explicit post-order walk of
+// the split tree (no device recursion); balanced sub-trees of whole units
+// take the coalesced fast path.  Warp-uniform control flow.
+template <typename T, class S>
+__device__ __noinline__ T pw_generic(const S& s, i64 off, i64 n, char* tile, bool vec_ok) {
+    constexpr i64 U = PwUnit<T>::value;
+    if (n <= 128) return pw_leaf<T>(s, off, n);
+    i64 f_off[48], f_n[48];
+    int f_state[48];  // 0 = unvisited, 1 = left pending, 2 = right pending
+    T f_left[48];
+    int sp = 0;
+    f_off[0] = off; f_n[0] = n; f_state[0] = 0; sp = 1;
+    T ret = 0;
+    bool have = false;  // `ret` holds a finished child value for the top frame
+    while (sp > 0) {
+        const int t = sp - 1;
+        if (have) {
+            if (f_state[t] == 1) {
+                f_left[t] = ret;
+                f_state[t] = 2;
+                i64 n2 = f_n[t] / 2;
+                n2 -= n2 % 8;
+                f_off[sp] = f_off[t] + n2; f_n[sp] = f_n[t] - n2; f_state[sp] = 0; ++sp;
+                have = false;
+            } else {
+                ret = f_left[t] + ret;
+                --sp;
+            }
+            continue;
+        }
+        const i64 nn = f_n[t];
+        bool direct = nn <= 128;
+        bool balanced = false;
+        if (!direct && nn % U == 0) {
+            const i64 c = nn / U;
+            balanced = (c & (c - 1)) == 0;
+        }
+        if (direct || balanced) {
+            ret = direct ? pw_leaf<T>(s, f_off[t], nn) : pw_balanced<T>(s, f_off[t], nn / U, tile, vec_ok);
+            have = true;
+            --sp;
+            continue;
+        }
+        i64 n2 = nn / 2;
+        n2 -= n2 % 8;
+        f_state[t] = 1;
+        f_off[sp] = f_off[t]; f_n[sp] = n2; f_state[sp] = 0; ++sp;
+    }
+    return ret;
+}
+
+// ---------------------------------------------------------------------------
+// block partials for the flat reductions (one warp per REDUCE_BLOCK block)
+
+template <typename T, class S>
+__device__ __forceinline__ T block_accu(const S& s, i64 off, i64 len, char* tile, bool vec_ok) {
+    if constexpr (is_float_t<T>::value) {
+        if (len == BM_REDUCE_BLOCK) return pw_balanced<T>(s, off, BM_REDUCE_BLOCK / PwUnit<T>::value, tile, vec_ok);
+        return pw_generic<T>(s, off, len, tile, vec_ok);
+    } else {
+        // integers wrap: any summation order gives the same bits
+        const int lane = threadIdx.x & 31;
+        T acc = 0;
+        for (i64 i = lane; i < len; i += 32) acc = OpPlus::f(acc, s.at(off + i));
+#pragma unroll
+        for (int m = 16; m >= 1; m >>= 1) acc = OpPlus::f(acc, warp_shfl_xor(acc, m));
+        return acc;
+    }
+}
+
+template <typename T, bool IS_MAX, class S>
+__device__ __forceinline__ T block_minmax(const S& s, i64 off, i64 len, bool vec_ok) {
+    constexpr int V = 16 / sizeof(T);
+    const int lane = threadIdx.x & 31;
+    T acc = s.at(off);  // len >= 1
+    if (vec_ok && len == BM_REDUCE_BLOCK) {
+        for (i64 i = lane * V; i < len; i += 32 * V) {
+            T v[V];
+            s.template vec<V>(off + i, v);
+#pragma unroll
+            for (int k = 0; k < V; ++k) acc = IS_MAX ? np_max(acc, v[k]) : np_min(acc, v[k]);
+        }
+    } else {
+        for (i64 i = lane; i < len; i += 32) {
+            const T x = s.at(off + i);
+            acc = IS_MAX ? np_max(acc, x) : np_min(acc, x);
+        }
+    }
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+        const T o = warp_shfl_xor(acc, m);
+        acc = IS_MAX ? np_max(acc, o) : np_min(acc, o);
+    }
+    return acc;
+}
+
+// dot partials accumulate in double for float inputs (the reference block
+// partial is OpenBLAS sdot/ddot, kernels.py:471-472; parity is by tolerance)
+template <typename T> struct DotAcc { typedef double type; };
+template <> struct DotAcc<int> { typedef int type; };
+template <> struct DotAcc<u64> { typedef u64 type; };
+
+template <typename T, class S2>
+__device__ __forceinline__ typename DotAcc<T>::type block_dot(const S2& s, i64 off, i64 len, bool vec_ok) {
+    typedef typename DotAcc<T>::type A;
+    constexpr int V = 16 / sizeof(T);
+    const int lane = threadIdx.x & 31;
+    A acc = 0;
+    if (vec_ok && len == BM_REDUCE_BLOCK) {
+        for (i64 i = lane * V; i < len; i += 32 * V) {
+            T x[V], y[V];
+            s.template vec2<V>(off + i, x, y);
+#pragma unroll
+            for (int k = 0; k < V; ++k) acc = OpPlus::f(acc, OpTimes::f((A)x[k], (A)y[k]));
+        }
+    } else {
+        for (i64 i = lane; i < len; i += 32) {
+            T x, y;
+            s.at2(off + i, x, y);
+            acc = OpPlus::f(acc, OpTimes::f((A)x, (A)y));
+        }
+    }
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) acc = OpPlus::f(acc, warp_shfl_xor(acc, m));
+    return acc;
+}
+
+// ---------------------------------------------------------------------------
+// combine_pairwise (kernels.py:380-392) over `cnt` values in shared memory,
+// executed by the whole CTA.  Adjacent pairs, odd element carried.
+template <typename A, int OP>
+__device__ __forceinline__ A combine_op(A a, A b) {
+    if (OP == 2) return py_min(a, b);
+    if (OP == 3) return py_max(a, b);
+    return OpPlus::f(a, b);
+}
+template <typename A, int OP>
+__device__ A cta_combine_pairwise(A* v, A* w, int cnt) {
+    // ping-pong between v and w; returns the folded value (valid in every thread)
+    while (cnt > 1) {
+        const int half = cnt >> 1;
+        for (int i = threadIdx.x; i < half; i += blockDim.x) w[i] = combine_op<A, OP>(v[2 * i], v[2 * i + 1]);
+        if ((cnt & 1) && threadIdx.x == 0) w[half] = v[cnt - 1];
+        __syncthreads();
+        A* t = v; v = w; w = t;
+        cnt = half + (cnt & 1);
+    }
+    const A r = v[0];
+    __syncthreads();
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// flat reduction kernel body.  CTA c owns blocks [c*group, (c+1)*group); its
+// warps take blocks round-robin; block partials are folded inside the CTA
+// with combine_pairwise, CTA partials by the last CTA to finish.  Because a
+// CTA's range is an aligned power-of-two run of blocks, this equals one
+// combine_pairwise over all blocks ("reduction order").
+template <typename T, int OP, class S>
+__device__ void reduce_flat(const Args& a, const S& s) {
+    typedef typename DotAcc<T>::type DA;
+    extern __shared__ __align__(16) char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    char* tile = smem + warp * BM_TILE_BYTES;
+    // partial slots (room for double)
+    double* slots_d = reinterpret_cast<double*>(smem + BM_RWARPS * BM_TILE_BYTES);
+    const i64 b0 = (i64)blockIdx.x * a.group;
+    i64 b1 = b0 + a.group;
+    if (b1 > a.blocks) b1 = a.blocks;
+    const int cnt = (int)(b1 - b0);
+    const bool vec_ok = a.vec_ok != 0;
+    for (i64 b = b0 + warp; b < b1; b += BM_RWARPS) {
+        const i64 off = b * BM_REDUCE_BLOCK;
+        i64 len = a.n - off;
+        if (len > BM_REDUCE_BLOCK) len = BM_REDUCE_BLOCK;
+        if constexpr (OP == 1) {
+            const T v = block_accu<T>(s, off, len, tile, vec_ok);
+            if (lane == 0) reinterpret_cast<T*>(slots_d)[b - b0] = v;
+        } else if constexpr (OP == 2 || OP == 3) {
+            const T v = block_minmax<T, OP == 3>(s, off, len, vec_ok);
+            if (lane == 0) reinterpret_cast<T*>(slots_d)[b - b0] = v;
+        } else {
+            const DA v = block_dot<T>(s, off, len, vec_ok);
+            if (lane == 0) reinterpret_cast<DA*>(slots_d)[b - b0] = v;
+        }
+    }
+    __syncthreads();
+    __shared__ bool am_last;
+    if constexpr (OP == 4) {
+        const DA v = cta_combine_pairwise<DA, 1>(reinterpret_cast<DA*>(slots_d), reinterpret_cast<DA*>(slots_d) + BM_MAX_GROUP, cnt);
+        if (threadIdx.x == 0) reinterpret_cast<DA*>(a.partials)[blockIdx.x] = v;
+    } else {
+        const T v = cta_combine_pairwise<T, OP>(reinterpret_cast<T*>(slots_d), reinterpret_cast<T*>(slots_d) + BM_MAX_GROUP, cnt);
+        if (threadIdx.x == 0) reinterpret_cast<T*>(a.partials)[blockIdx.x] = v;
+    }
+    __threadfence();
+    if (threadIdx.x == 0) {
+        const unsigned int t = atomicAdd(a.ticket, 1u);
+        am_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!am_last) return;
+    __threadfence();
+    const int nparts = gridDim.x;
+    // reuse the tile region for the final fold (gridDim.x <= BM_MAX_FINAL)
+    if constexpr (OP == 4) {
+        DA* v = reinterpret_cast<DA*>(smem);
+        for (int i = threadIdx.x; i < nparts; i += blockDim.x) v[i] = reinterpret_cast<volatile DA*>(a.partials)[i];
+        __syncthreads();
+        const DA r = cta_combine_pairwise<DA, 1>(v, v + BM_MAX_FINAL, nparts);
+        if (threadIdx.x == 0) {
+            reinterpret_cast<DA*>(a.result)[0] = r;
+            *a.ticket = 0u;
+        }
+    } else {
+        T* v = reinterpret_cast<T*>(smem);
+        for (int i = threadIdx.x; i < nparts; i += blockDim.x) v[i] = reinterpret_cast<volatile T*>(a.partials)[i];
+        __syncthreads();
+        const T r = cta_combine_pairwise<T, OP>(v, v + BM_MAX_FINAL, nparts);
+        if (threadIdx.x == 0) {
+            T fin = r;
+            if constexpr (OP == 1 && is_float_t<T>::value) fin = r + T(0);  // numpy: 0 + pairwise(...) (-0 -> +0)
+            reinterpret_cast<T*>(a.result)[0] = fin;
+            *a.ticket = 0u;
+        }
+    }
+}
+
+}  // namespace bm

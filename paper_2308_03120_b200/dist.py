@@ -1,0 +1,111 @@
+"""Column-block sharding over the GPUs of one box.
+
+One process per GPU (torchrun); torch.distributed over NCCL is plumbing
+only: it carries one partial per rank.  Element-wise work on a column block
+needs no communication.  A scalar reduction is computed per shard to one
+partial (the fused kernel writes it straight into a device slot), the
+partials are all-gathered in rank order and folded on the device with the
+reference's combine_pairwise (kernels.py:380-392).  When every shard is an
+aligned power-of-two run of REDUCE_BLOCK-element blocks (e.g. 4096x4096 f32
+per GPU), the result is bit-identical to the single-device reduction of the
+concatenated matrix; otherwise it is still deterministic for a given world
+size.  No float atomics, no NCCL sum whose order NCCL chooses.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _clib, kernels
+from . import expr as _expr
+from . import runtime as _rt
+
+_TORCH_DTYPE = {"f32": "float32", "f64": "float64", "i32": "int32", "u64": "uint64"}
+
+
+def column_block(total_cols: int, rank: int, world: int) -> tuple[int, int]:
+    """[start, start+count) of the columns rank `rank` owns: contiguous,
+    balanced, in rank order (column-major => each block is contiguous)."""
+    base, extra = divmod(total_cols, world)
+    start = rank * base + min(rank, extra)
+    return start, base + (1 if rank < extra else 0)
+
+
+def bind_torch_stream() -> None:
+    """Run the device library on torch's current CUDA stream so NCCL
+    collectives issued by torch.distributed are stream-ordered with it."""
+    import torch
+    rt = _rt.get_runtime()
+    _clib.check(rt._lib.bm_set_stream(ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)), "bind stream")
+
+
+def partial_dtype(op: str, elem: str) -> str:
+    """Element type of one rank's partial (dot partials of floats are f64)."""
+    return "f64" if op == "dot" and elem in ("f32", "f64") else elem
+
+
+class ShardedReduction:
+    """A scalar reduction over column-block shards, reusable across steps.
+
+    ``prepare`` plans the fused kernel once; ``launch`` enqueues this rank's
+    partial, the all-gather and the device-side fold without any host
+    synchronisation; ``value`` reads the folded result back.
+    """
+
+    def __init__(self, op: str, *local_exprs, group=None):
+        import torch
+        import torch.distributed as dist
+        self.op = op
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.plan = _expr.plan_reduce(op, *local_exprs)
+        if self.plan.steps:
+            raise ValueError("sharded reduction expects a purely element-wise local program")
+        node = _expr.as_expr(local_exprs[0])
+        self.elem = node.elem_type
+        self.pdt = partial_dtype(op, self.elem)
+        tdt = getattr(torch, _TORCH_DTYPE[self.pdt])
+        self.partial = torch.zeros(1, dtype=tdt, device="cuda")
+        self.gathered = torch.zeros(self.world, dtype=tdt, device="cuda")
+        self.result = torch.zeros(1, dtype=tdt, device="cuda")
+        views = _expr._step_views(self.plan, self.plan.reduce, {})
+        self.inv = _rt.build_invocation(_rt.KernelInvocation("fused_reduce", tuple(views), None, (),
+                                                             dict(self.plan.reduce.params)))
+        self._lib = _clib.lib()
+        self._op_code = {"accu": _clib.BM_R_ACCU, "min": _clib.BM_R_MIN, "max": _clib.BM_R_MAX,
+                         "dot": _clib.BM_R_DOT}[op]
+
+    def launch(self) -> None:
+        _clib.check(self._lib.bm_reduce_to_device(ctypes.byref(self.inv), ctypes.c_void_p(self.partial.data_ptr())),
+                    "sharded reduce")
+        if self.world == 1:
+            return
+        self.dist.all_gather_into_tensor(self.gathered, self.partial, group=self.group)
+        _clib.check(self._lib.bm_combine_partials_to_device(
+            ctypes.c_void_p(self.gathered.data_ptr()), self.world, _clib.DTYPE_CODE[self.elem], self._op_code,
+            ctypes.c_void_p(self.result.data_ptr())), "combine partials")
+
+    def value(self):
+        import torch
+        torch.cuda.synchronize()
+        src = self.partial if self.world == 1 else self.result
+        v = src.cpu().numpy()[0]
+        dt = kernels.NP_DTYPE[self.elem]
+        if self.op == "dot" and dt.kind == "f":
+            return dt.type(v)
+        return np.asarray(v).astype(dt)[()]
+
+
+def sharded_accu(local_expr, group=None):
+    """accu over a column-block-sharded expression (all ranks call)."""
+    r = ShardedReduction("accu", local_expr, group=group)
+    r.launch()
+    return r.value().item()
+
+
+def sharded_dot(a_local, b_local, group=None):
+    r = ShardedReduction("dot", a_local, b_local, group=group)
+    r.launch()
+    return r.value().item()

@@ -1,0 +1,757 @@
+"""Delayed evaluation: immutable expression trees, shape inference,
+construction-time rewrites, and the planner that lowers a tree onto device
+invocations.
+
+Semantics (node kinds, shape rules, error types and messages, the three
+rewrites, plan/evaluate behaviour) are the reference's
+(reference/pkg/src/devmat/expr.py).  The lowering is B200-first:
+
+* an element-wise subtree becomes ONE fused kernel of any depth (the
+  reference splits after 8 stages, expr.py:615-626; splitting never changes
+  bits because every stage rounds, so the planner only splits when the device
+  limits of 16 inputs / 64 program slots are reached);
+* a type conversion of a materialised matrix inside a chain is folded into the
+  chain's load (the reference emits a separate mov_copy, expr.py:512-518);
+* ``op_htrans`` operands of ``glue_times`` become GEMM transpose flags, so
+  ``A @ B.t()`` is one NT GEMM with no mov_transpose (expr.py:543-547);
+* scalar reductions over an expression (``accu``, ``dot``, ``norm``) run the
+  element-wise program and the reduction in the same kernel
+  (:func:`plan_reduce`) instead of materialising the tree first
+  (ops.py:153-177).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import NamedTuple
+
+import numpy as np
+
+from . import kernels, runtime
+from .errors import DimensionError, ElemTypeError
+from .kernels import NP_DTYPE
+from .runtime import BlockView, FlatView, KernelInvocation
+
+
+class Shape(NamedTuple):
+    rows: int
+    cols: int
+
+    @property
+    def n_elem(self) -> int:
+        return self.rows * self.cols
+
+
+EOP_UNARY_KINDS = frozenset(kernels.EOP_UNARY)
+EOP_SCALAR_KINDS = frozenset(kernels.EOP_SCALAR)
+EGLUE_KINDS = frozenset(kernels.EGLUE)
+ELEMENTWISE_KINDS = EOP_UNARY_KINDS | EOP_SCALAR_KINDS | EGLUE_KINDS
+GEN_KINDS = frozenset({"gen_zeros", "gen_ones", "gen_fill", "gen_eye", "gen_linspace", "gen_randu", "gen_randn"})
+UNARY_OP_KINDS = frozenset({"op_htrans", "op_diagmat", "op_diagvec", "op_vectorise", "op_resize", "op_reshape",
+                            "op_repmat"})
+REDUCE_DIM_KINDS = frozenset({"op_sum_dim", "op_min_dim", "op_max_dim", "op_mean_dim", "op_var_dim",
+                              "op_stddev_dim"})
+GLUE_KINDS = frozenset({"glue_times", "glue_join_rows", "glue_join_cols"})
+# conv_to folds into the producing kernel for these (two-way kernels)
+CONV_FUSABLE_KINDS = ELEMENTWISE_KINDS | GEN_KINDS | UNARY_OP_KINDS | frozenset({"subview"})
+
+
+# ---------------------------------------------------------------------------
+# nodes
+
+def _is_scalar(x) -> bool:
+    return isinstance(x, (int, float, np.integer, np.floating)) and not isinstance(x, bool)
+
+
+def as_expr(x) -> "ExprNode":
+    if isinstance(x, ExprNode):
+        return x
+    hook = getattr(x, "_as_expr_node", None)
+    if hook is None:
+        raise TypeError(f"not an expression or matrix: {x!r}")
+    return hook()
+
+
+def _binary(kind_scalar: str, kind_glue: str):
+    def op(a, b):
+        if _is_scalar(b):
+            return build_node(kind_scalar, (as_expr(a),), (b,))
+        return build_node(kind_glue, (as_expr(a), as_expr(b)))
+    return op
+
+
+_plus = _binary("eop_scalar_plus", "eglue_plus")
+_minus = _binary("eop_scalar_minus_post", "eglue_minus")
+_divide = _binary("eop_scalar_div_post", "eglue_div")
+
+
+def _times(a, b):
+    if _is_scalar(b):
+        return scalar_times(as_expr(a), b)
+    return build_node("eglue_schur", (as_expr(a), as_expr(b)))
+
+
+def _schur(a, b):
+    return build_node("eglue_schur", (as_expr(a), as_expr(b)))
+
+
+class ExpressionOps:
+    """Operator surface shared by expression nodes and containers.
+
+    ``*`` is the element-wise (Schur) product or a scalar multiply and ``@``
+    is the matrix product -- the reference's operator assignment
+    (expr.py:93-106), which its own tests depend on.  ``%`` is provided as
+    an explicit Schur-product alias (Armadillo spelling).
+    """
+
+    __slots__ = ()
+    __array_ufunc__ = None
+
+    def __add__(self, other):
+        return _plus(self, other)
+
+    def __radd__(self, other):
+        return _plus(self, other)
+
+    def __sub__(self, other):
+        return _minus(self, other)
+
+    def __rsub__(self, other):
+        return build_node("eop_scalar_minus_pre", (as_expr(self),), (other,))
+
+    def __mul__(self, other):
+        return _times(self, other)
+
+    def __rmul__(self, other):
+        return _times(self, other)
+
+    def __mod__(self, other):
+        return _schur(self, other)
+
+    def __truediv__(self, other):
+        return _divide(self, other)
+
+    def __rtruediv__(self, other):
+        return build_node("eop_scalar_div_pre", (as_expr(self),), (other,))
+
+    def __matmul__(self, other):
+        return build_node("glue_times", (as_expr(self), as_expr(other)))
+
+    def __neg__(self):
+        return build_node("eop_scalar_minus_pre", (as_expr(self),), (0,))
+
+    def __pos__(self):
+        return as_expr(self)
+
+    def __abs__(self):
+        return build_node("eop_abs", (as_expr(self),))
+
+    def __gt__(self, k):
+        return Relational(">", self, k)
+
+    def __lt__(self, k):
+        return Relational("<", self, k)
+
+    def __ge__(self, k):
+        return Relational(">=", self, k)
+
+    def __le__(self, k):
+        return Relational("<=", self, k)
+
+
+@dataclass(frozen=True, eq=False)
+class ExprNode(ExpressionOps):
+    """Immutable DAG node; leaves (kind "leaf") hold a device matrix."""
+    kind: str
+    operands: tuple = ()
+    aux: tuple = ()
+    elem_type: str = "f32"
+
+    __array_ufunc__ = None
+
+    def t(self) -> "ExprNode":
+        return rewrite_trans(self)
+
+    def eval(self, elem_type: str | None = None):
+        return evaluate(self if elem_type is None else conv_node(self, elem_type))
+
+    def __repr__(self):
+        s = shape_of(self)
+        return f"ExprNode({self.kind}, {s.rows}x{s.cols}, {self.elem_type})"
+
+    __hash__ = object.__hash__
+
+
+@dataclass(frozen=True)
+class Relational:
+    """Element-versus-scalar comparison (consumed by find/all/any)."""
+    op: str
+    operand: object
+    threshold: float
+
+
+# ---------------------------------------------------------------------------
+# shape inference (no device work)
+
+def _diag_length(rows: int, cols: int, k: int) -> int:
+    return max(0, min(rows, cols - k)) if k >= 0 else max(0, min(rows + k, cols))
+
+
+def _region_shape(parent: Shape, region: tuple) -> Shape:
+    tag = region[0]
+    if tag == "diag":
+        return Shape(_diag_length(parent.rows, parent.cols, region[1]), 1)
+    if tag == "row":
+        return Shape(1, parent.cols)
+    if tag == "col":
+        return Shape(parent.rows, 1)
+    if tag == "rows":
+        return Shape(region[2] - region[1] + 1, parent.cols)
+    if tag == "cols":
+        return Shape(parent.rows, region[2] - region[1] + 1)
+    if tag == "submat":
+        p, q, r, s = region[1:]
+        return Shape(r - p + 1, s - q + 1)
+    raise ValueError(f"unknown region kind {tag!r}")
+
+
+def shape_of(node: ExprNode) -> Shape:
+    """Result shape of an expression (expr.py:253-297)."""
+    k = node.kind
+    if k == "leaf":
+        m = node.operands[0]
+        return Shape(m.n_rows, m.n_cols)
+    if k == "subview":
+        return _region_shape(shape_of(node.operands[0]), node.aux[0])
+    if k in GEN_KINDS or k in ("op_resize", "op_reshape"):
+        return Shape(node.aux[0], node.aux[1])
+    if k in ELEMENTWISE_KINDS or k == "mtop_conv_to":
+        return shape_of(node.operands[0])
+    a = shape_of(node.operands[0])
+    if k == "op_htrans":
+        return Shape(a.cols, a.rows)
+    if k == "op_diagmat":
+        return Shape(a.n_elem, a.n_elem)
+    if k == "op_diagvec":
+        return Shape(_diag_length(a.rows, a.cols, node.aux[0]), 1)
+    if k == "op_vectorise":
+        return Shape(a.n_elem, 1)
+    if k == "op_repmat":
+        return Shape(a.rows * node.aux[0], a.cols * node.aux[1])
+    if k in REDUCE_DIM_KINDS:
+        return Shape(1, a.cols) if node.aux[0] == 0 else Shape(a.rows, 1)
+    if k in GLUE_KINDS:
+        b = shape_of(node.operands[1])
+        if k == "glue_times":
+            return Shape(a.rows, b.cols)
+        if k == "glue_join_rows":
+            return Shape(a.rows, a.cols + b.cols)
+        return Shape(a.rows + b.rows, a.cols)
+    raise ValueError(f"unknown node kind {k!r}")
+
+
+# ---------------------------------------------------------------------------
+# construction
+
+def _same_type(kind: str, a: ExprNode, b: ExprNode) -> None:
+    if a.elem_type != b.elem_type:
+        raise ElemTypeError(f"{kind}: element types differ ({a.elem_type} vs {b.elem_type}); "
+                            "insert an explicit conversion")
+
+
+def build_node(kind: str, operands: tuple = (), aux: tuple = (), elem_type: str | None = None) -> ExprNode:
+    """Validating constructor: shape/type checks, no rewrites, no device work."""
+    operands = tuple(operands)
+    if elem_type is None:
+        elem_type = operands[0].elem_type if operands else "f32"
+    if kind in EGLUE_KINDS or kind in GLUE_KINDS:
+        a, b = operands
+        sa, sb = shape_of(a), shape_of(b)
+        bad = {
+            "glue_times": sa.cols != sb.rows,
+            "glue_join_rows": sa.rows != sb.rows,
+            "glue_join_cols": sa.cols != sb.cols,
+        }.get(kind, sa != sb)
+        if bad:
+            raise DimensionError(kind, sa, sb)
+        _same_type(kind, a, b)
+    elif kind == "op_diagmat":
+        s = shape_of(operands[0])
+        if s.rows != 1 and s.cols != 1:
+            raise DimensionError(kind, s)
+    elif kind in ("op_resize", "op_reshape") or kind in GEN_KINDS:
+        if aux[0] < 0 or aux[1] < 0:
+            raise DimensionError(kind, (aux[0], aux[1]))
+    elif kind in REDUCE_DIM_KINDS:
+        if aux[0] not in (0, 1):
+            raise ValueError(f"{kind}: dim must be 0 or 1")
+    return ExprNode(kind, operands, tuple(aux), elem_type)
+
+
+def conv_node(x, elem_type: str) -> ExprNode:
+    node = as_expr(x)
+    if elem_type not in NP_DTYPE:
+        raise ElemTypeError(f"unknown element type {elem_type!r}")
+    if node.elem_type == elem_type:
+        return node
+    return build_node("mtop_conv_to", (node,), (), elem_type)
+
+
+def rewrite_trans(x) -> ExprNode:
+    """trans(diagmat(v)) -> diagmat(v); trans(trans(X)) -> X (expr.py:368-380)."""
+    node = as_expr(x)
+    if node.kind == "op_diagmat":
+        return node
+    if node.kind == "op_htrans":
+        return node.operands[0]
+    return build_node("op_htrans", (node,))
+
+
+def scalar_times(x, k) -> ExprNode:
+    """k1*(k2*A) -> (k1*k2)*A (expr.py:383-388)."""
+    node = as_expr(x)
+    if node.kind == "eop_scalar_times":
+        return build_node("eop_scalar_times", node.operands, (node.aux[0] * k,))
+    return build_node("eop_scalar_times", (node,), (k,))
+
+
+def census(x) -> dict[str, int]:
+    """Node-kind histogram, shared nodes counted once."""
+    out: dict[str, int] = {}
+    seen: set[int] = set()
+    stack = [as_expr(x)]
+    while stack:
+        n = stack.pop()
+        if id(n) in seen:
+            continue
+        seen.add(id(n))
+        out[n.kind] = out.get(n.kind, 0) + 1
+        if n.kind != "leaf":
+            stack.extend(n.operands)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# planning
+
+@dataclass(frozen=True)
+class PlanStep:
+    kernel: str
+    inputs: tuple            # ("slot", i) | ("leaf", Matrix)
+    in_modes: tuple          # "flat" | "2d" | ("flat-region" | "block-region", ...)
+    out_slot: int
+    out_mode: str
+    scalars: tuple = ()
+    params: dict = field(default_factory=dict)
+
+
+@dataclass(frozen=True)
+class SlotInfo:
+    rows: int
+    cols: int
+    elem_type: str
+
+
+@dataclass
+class EvalPlan:
+    """Ordered device schedule for one evaluation."""
+    steps: list
+    slots: list
+    result: tuple
+    absorbed: list
+    reduce: PlanStep | None = None   # trailing fused reduction (plan_reduce)
+
+    @property
+    def n_invocations(self) -> int:
+        return len(self.steps) + (1 if self.reduce is not None else 0)
+
+    @property
+    def temp_schedule(self) -> dict:
+        """slot -> (producing step, last consuming step); the result slot has none."""
+        final = self.result[1] if self.result and self.result[0] == "slot" else None
+        span = {s.out_slot: [i, None] for i, s in enumerate(self.steps)}
+        consumers = list(self.steps) + ([self.reduce] if self.reduce is not None else [])
+        for i, s in enumerate(consumers):
+            for ref in s.inputs:
+                if ref[0] == "slot" and ref[1] != final:
+                    span[ref[1]][1] = i
+        return {k: tuple(v) for k, v in span.items()}
+
+    def leaf_buffer_ids(self) -> set[int]:
+        ids = {ref[1].mem.buffer_id for s in self.steps for ref in s.inputs if ref[0] == "leaf"}
+        if self.result and self.result[0] == "leaf":
+            ids.add(self.result[1].mem.buffer_id)
+        return ids
+
+
+_GEN_KERNEL = {"gen_zeros": "gen_fill_const", "gen_ones": "gen_fill_const", "gen_fill": "gen_fill_const",
+               "gen_eye": "gen_eye", "gen_linspace": "gen_linspace", "gen_randu": "gen_randu",
+               "gen_randn": "gen_randn"}
+_RDIM_KERNEL = {"op_sum_dim": "rdim_sum", "op_min_dim": "rdim_min", "op_max_dim": "rdim_max",
+                "op_mean_dim": "rdim_mean", "op_var_dim": "rdim_var", "op_stddev_dim": "rdim_var"}
+
+
+class _Program:
+    """Post-order stage program being assembled for one fused kernel."""
+
+    def __init__(self):
+        self.stages: list[tuple] = []
+        self.inputs: list[tuple] = []
+
+    def load(self, ref: tuple) -> None:
+        key = (ref[0], id(ref[1]) if ref[0] == "leaf" else ref[1])
+        for i, r in enumerate(self.inputs):
+            if (r[0], id(r[1]) if r[0] == "leaf" else r[1]) == key:
+                self.stages.append(("load", i))
+                return
+        self.inputs.append(ref)
+        self.stages.append(("load", len(self.inputs) - 1))
+
+    @property
+    def n_stages(self) -> int:
+        return sum(1 for s in self.stages if s[0] != "load")
+
+
+class _Lowerer:
+    def __init__(self, fuse: bool, chain_max: int | None = None):
+        self.fuse = fuse
+        self.chain_max = kernels.FUSED_CHAIN_MAX if chain_max is None else chain_max
+        self.steps: list[PlanStep] = []
+        self.slots: list[SlotInfo] = []
+        self.absorbed: list[tuple] = []
+
+    def emit(self, kernel, inputs, in_modes, shape, out_type, out_mode, scalars=(), params=None,
+             absorbed_from=None) -> tuple:
+        self.slots.append(SlotInfo(shape.rows, shape.cols, out_type))
+        slot = len(self.slots) - 1
+        self.steps.append(PlanStep(kernel, tuple(inputs), tuple(in_modes), slot, out_mode, tuple(scalars),
+                                   params or {}))
+        if absorbed_from is not None and absorbed_from != out_type:
+            self.absorbed.append((len(self.steps) - 1, absorbed_from, out_type))
+        return ("slot", slot)
+
+    # -- recursion ------------------------------------------------------------------------
+    def lower(self, node: ExprNode, want: str):
+        k = node.kind
+        if k == "leaf":
+            m = node.operands[0]
+            if want == m.elem_type:
+                return ("leaf", m)
+            return self.emit("mov_copy", [("leaf", m)], ["flat"], shape_of(node), want, "flat")
+        if k == "mtop_conv_to":
+            child = node.operands[0]
+            if self.fuse and child.kind in CONV_FUSABLE_KINDS:
+                return self.lower(child, want)
+            src = self.lower(child, child.elem_type)
+            return self.emit("mov_copy", [src], ["flat"], shape_of(node), want, "flat")
+        if k in ELEMENTWISE_KINDS:
+            return self._chain(node, want)
+        if k in GEN_KINDS:
+            return self._generator(node, want)
+        if k == "subview":
+            parent = node.operands[0].operands[0]
+            mode = _region_view_mode(parent, node.aux[0])
+            return self.emit("mov_extract_strided", [("leaf", parent)], [mode], shape_of(node), want, "flat",
+                             absorbed_from=node.elem_type)
+        if k in UNARY_OP_KINDS:
+            child = node.operands[0]
+            src = self.lower(child, child.elem_type)
+            shape = shape_of(node)
+            if k == "op_htrans":
+                return self.emit("mov_transpose", [src], ["2d"], shape, want, "2d", absorbed_from=node.elem_type)
+            if k == "op_diagmat":
+                return self.emit("mov_diagmat_build", [src], ["flat"], shape, want, "2d",
+                                 absorbed_from=node.elem_type)
+            if k == "op_diagvec":
+                return self.emit("mov_diagvec_extract", [src], ["2d"], shape, want, "flat",
+                                 params={"k": node.aux[0]}, absorbed_from=node.elem_type)
+            if k in ("op_vectorise", "op_reshape"):
+                return self.emit("mov_reshape_copy", [src], ["flat"], shape, want, "flat",
+                                 absorbed_from=node.elem_type)
+            if k == "op_resize":
+                return self.emit("mov_resize", [src], ["2d"], shape, want, "2d", absorbed_from=node.elem_type)
+            return self.emit("gen_repmat", [src], ["2d"], shape, want, "flat", params={"rows_out": shape.rows},
+                             absorbed_from=node.elem_type)
+        if k in ("glue_join_rows", "glue_join_cols"):
+            a = self.lower(node.operands[0], node.operands[0].elem_type)
+            b = self.lower(node.operands[1], node.operands[1].elem_type)
+            kern = "mov_join_rows" if k == "glue_join_rows" else "mov_join_cols"
+            return self.emit(kern, [a, b], ["2d", "2d"], shape_of(node), want, "2d", absorbed_from=node.elem_type)
+        if k in REDUCE_DIM_KINDS:
+            child = node.operands[0]
+            src = self.lower(child, child.elem_type)
+            ref = self.emit(_RDIM_KERNEL[k], [src], ["2d"], shape_of(node), child.elem_type, "flat",
+                            params={"dim": node.aux[0]})
+            if k == "op_stddev_dim":
+                ref = self.emit("eop_sqrt", [ref], ["flat"], shape_of(node), child.elem_type, "flat")
+            if want != child.elem_type:
+                ref = self.emit("mov_copy", [ref], ["flat"], shape_of(node), want, "flat")
+            return ref
+        if k == "glue_times":
+            a, b = node.operands
+            ta = tb = 0
+            if a.kind == "op_htrans":     # fold the transpose into the GEMM
+                a, ta = a.operands[0], 1
+            if b.kind == "op_htrans":
+                b, tb = b.operands[0], 1
+            ra = self.lower(a, a.elem_type)
+            rb = self.lower(b, b.elem_type)
+            ref = self.emit("gemm", [ra, rb], ["2d", "2d"], shape_of(node), node.operands[0].elem_type, "2d",
+                            params={"trans_a": ta, "trans_b": tb})
+            if want != node.operands[0].elem_type:
+                ref = self.emit("mov_copy", [ref], ["flat"], shape_of(node), want, "flat")
+            return ref
+        raise ValueError(f"cannot lower node kind {k!r}")
+
+    # -- element-wise programs -----------------------------------------------------------------
+    def program(self, root: ExprNode, elem: str, budget: int) -> _Program:
+        """Collect the fusable element-wise subtree under ``root`` into a stage
+        program; everything else is lowered into slots and loaded."""
+        prog = _Program()
+        left = [budget if self.fuse else 1]
+
+        def load(node: ExprNode) -> None:
+            # a converted materialised matrix is read with a load-time cast
+            if (self.fuse and node.kind == "mtop_conv_to" and node.elem_type == elem
+                    and node.operands[0].kind == "leaf"):
+                prog.load(("leaf", node.operands[0].operands[0]))
+                return
+            prog.load(self.lower(node, elem))
+
+        def walk(node: ExprNode) -> None:
+            if node.kind not in ELEMENTWISE_KINDS or left[0] <= 0:
+                load(node)
+                return
+            left[0] -= 1
+            if node.kind in EGLUE_KINDS:
+                walk(node.operands[0])
+                walk(node.operands[1])
+                prog.stages.append(("glue", node.kind))
+            elif node.kind in EOP_SCALAR_KINDS:
+                walk(node.operands[0])
+                prog.stages.append(("scalar", node.kind, node.aux[0]))
+            else:
+                walk(node.operands[0])
+                prog.stages.append(("unary", node.kind, node.aux[0] if node.aux else None))
+
+        walk(root)
+        return prog
+
+    def _fit_program(self, root: ExprNode, elem: str, extra_slots: int = 0) -> _Program:
+        budget = self.chain_max
+        while True:
+            mark = (len(self.steps), len(self.slots), len(self.absorbed))
+            prog = self.program(root, elem, budget)
+            fits = (len(prog.inputs) <= kernels.FUSED_INPUTS_MAX
+                    and len(prog.stages) + extra_slots <= 64)
+            if fits or budget <= 1:
+                return prog
+            # roll back and retry with a shallower fusion
+            del self.steps[mark[0]:]
+            del self.slots[mark[1]:]
+            del self.absorbed[mark[2]:]
+            budget = max(1, budget // 2)
+
+    def _chain(self, root: ExprNode, want: str):
+        elem = root.elem_type
+        prog = self._fit_program(root, elem)
+        shape = shape_of(root)
+        if prog.n_stages == 1 and len(prog.stages) == len(prog.inputs) + 1 and \
+                all(prog.stages[i] == ("load", i) for i in range(len(prog.inputs))):
+            # one stage over distinct inputs: the reference's dedicated kernel name
+            st = prog.stages[-1]
+            scal = (st[2],) if len(st) > 2 and st[2] is not None else ()
+            return self.emit(st[1], prog.inputs, ["flat"] * len(prog.inputs), shape, want, "flat",
+                             scalars=scal, absorbed_from=elem)
+        return self.emit("fused_chain", prog.inputs, ["flat"] * len(prog.inputs), shape, want, "flat",
+                         params={"program": tuple(prog.stages), "compute_dtype": NP_DTYPE[elem].str},
+                         absorbed_from=elem)
+
+    def _generator(self, node: ExprNode, want: str):
+        shape = shape_of(node)
+        params: dict = {"gen_type": node.elem_type}
+        scalars: tuple = ()
+        k = node.kind
+        if k == "gen_zeros":
+            scalars = (0,)
+        elif k == "gen_ones":
+            scalars = (1,)
+        elif k == "gen_fill":
+            scalars = (node.aux[2],)
+        elif k == "gen_eye":
+            params["rows"] = shape.rows
+        elif k == "gen_linspace":
+            scalars = (node.aux[2], node.aux[3])
+            params["n"] = shape.n_elem
+        else:
+            params["rng"] = True
+        return self.emit(_GEN_KERNEL[k], [], [], shape, want, "flat", scalars=scalars, params=params,
+                         absorbed_from=node.elem_type)
+
+
+def _region_view_mode(parent, region: tuple):
+    """A subview region as a concrete strided view descriptor (expr.py:682-703)."""
+    n, tag = parent.n_rows, region[0]
+    if tag == "diag":
+        k = region[1]
+        length = _diag_length(parent.n_rows, parent.n_cols, k)
+        return ("flat-region", k * n if k >= 0 else -k, length, n + 1)
+    if tag == "row":
+        return ("flat-region", region[1], parent.n_cols, n)
+    if tag == "col":
+        return ("flat-region", region[1] * n, parent.n_rows, 1)
+    if tag == "rows":
+        a, b = region[1], region[2]
+        return ("block-region", a, b - a + 1, parent.n_cols, n)
+    if tag == "cols":
+        c, d = region[1], region[2]
+        return ("block-region", c * n, parent.n_rows, d - c + 1, n)
+    if tag == "submat":
+        p, q, r, s = region[1:]
+        return ("block-region", p + q * n, r - p + 1, s - q + 1, n)
+    raise ValueError(f"unknown region kind {tag!r}")
+
+
+def plan(x, out_elem_type: str | None = None, fuse: bool = True, chain_max: int | None = None) -> EvalPlan:
+    """Lower an expression to an ordered device schedule.  ``chain_max=8``
+    reproduces the reference's chain splitting (kernels.py:91-92)."""
+    node = as_expr(x)
+    low = _Lowerer(fuse, chain_max)
+    result = low.lower(node, out_elem_type or node.elem_type)
+    return EvalPlan(low.steps, low.slots, result, low.absorbed)
+
+
+def plan_reduce(op: str, *xs, fuse: bool = True) -> EvalPlan:
+    """Plan a scalar reduction (``accu``/``min``/``max`` over one expression,
+    ``dot`` over two) whose element-wise part runs inside the reduction kernel.
+    The result is ``plan.reduce``, a ``fused_reduce`` step executed with
+    Runtime.execute_reduce."""
+    nodes = [as_expr(x) for x in xs]
+    elem = nodes[0].elem_type
+    low = _Lowerer(fuse)
+    prog = _Program()
+    for node in nodes:
+        sub = low._fit_program(node, elem, extra_slots=len(prog.stages))
+        remap = []
+        for ref in sub.inputs:
+            before = len(prog.inputs)
+            prog.load(ref)
+            remap.append(prog.stages.pop()[1])
+            del before
+        for st in sub.stages:
+            prog.stages.append(("load", remap[st[1]]) if st[0] == "load" else st)
+    red = PlanStep("fused_reduce", tuple(prog.inputs), ("flat",) * len(prog.inputs), -1, "none", (),
+                   {"program": tuple(prog.stages), "compute_dtype": NP_DTYPE[elem].str, "op": op})
+    return EvalPlan(low.steps, low.slots, None, low.absorbed, reduce=red)
+
+
+# ---------------------------------------------------------------------------
+# execution
+
+def _make_view(buf, rows: int, cols: int, mode):
+    if mode == "flat":
+        return FlatView(buf, 0, rows * cols)
+    if mode == "2d":
+        return BlockView(buf, 0, rows, cols, rows)
+    if mode[0] == "flat-region":
+        return FlatView(buf, mode[1], mode[2], mode[3])
+    if mode[0] == "block-region":
+        return BlockView(buf, mode[1], mode[2], mode[3], mode[4])
+    raise ValueError(f"unknown view mode {mode!r}")
+
+
+def _step_views(plan_obj: EvalPlan, step: PlanStep, slot_bufs: dict) -> list:
+    views = []
+    for ref, mode in zip(step.inputs, step.in_modes):
+        if ref[0] == "leaf":
+            m = ref[1]
+            views.append(_make_view(m.mem, m.n_rows, m.n_cols, mode))
+        else:
+            info = plan_obj.slots[ref[1]]
+            views.append(_make_view(slot_bufs[ref[1]], info.rows, info.cols, mode))
+    return views
+
+
+def execute_plan(plan_obj: EvalPlan, target_buf=None):
+    """Run the plan's steps; returns the result buffer (or the leaf matrix for
+    an empty plan).  When the plan carries a fused reduction it is executed
+    last and its value is returned instead."""
+    rt = runtime.get_runtime()
+    if plan_obj.result is not None and plan_obj.result[0] == "leaf" and plan_obj.reduce is None:
+        return plan_obj.result[1]
+    final_slot = plan_obj.result[1] if plan_obj.result is not None else None
+    release_after = {s: span[1] for s, span in plan_obj.temp_schedule.items()}
+    slot_bufs: dict[int, object] = {}
+
+    def release_inputs(step: PlanStep, i: int) -> None:
+        done = set()
+        for ref in step.inputs:
+            s = ref[1]
+            if ref[0] == "slot" and s != final_slot and release_after.get(s) == i and s not in done:
+                done.add(s)
+                rt.release_deferred(slot_bufs.pop(s))
+
+    for i, step in enumerate(plan_obj.steps):
+        views = _step_views(plan_obj, step, slot_bufs)
+        info = plan_obj.slots[step.out_slot]
+        if step.out_slot == final_slot and target_buf is not None:
+            out_buf = target_buf
+        else:
+            out_buf = rt.acquire_memory(info.rows * info.cols, info.elem_type)
+        slot_bufs[step.out_slot] = out_buf
+        params = dict(step.params)
+        if params.pop("rng", None):
+            params["seed"] = rt.seed
+            params["stream"] = rt.next_stream_id()
+        rt.enqueue(KernelInvocation(step.kernel, tuple(views), _make_view(out_buf, info.rows, info.cols,
+                                                                          step.out_mode),
+                                    step.scalars, params))
+        release_inputs(step, i)
+    if plan_obj.reduce is not None:
+        step = plan_obj.reduce
+        views = _step_views(plan_obj, step, slot_bufs)
+        try:
+            value = rt.execute_reduce(KernelInvocation("fused_reduce", tuple(views), None, (), dict(step.params)))
+        finally:
+            release_inputs(step, len(plan_obj.steps))
+        return value
+    return slot_bufs[final_slot]
+
+
+def evaluate(x, out=None, fuse: bool = True):
+    """Evaluate into ``out`` (or a fresh matrix); expr.py:792-835 semantics:
+    a bare leaf is a device-to-device copy, an output that aliases an operand
+    adopts a fresh result buffer."""
+    from .matrix import Matrix
+
+    node = as_expr(x)
+    rt = runtime.get_runtime()
+    shape = shape_of(node)
+    if out is not None and out.elem_type != node.elem_type:
+        raise ElemTypeError(f"cannot assign {node.elem_type} expression to {out.elem_type} matrix; "
+                            "convert explicitly")
+    p = plan(node, node.elem_type, fuse=fuse)
+    if p.result[0] == "leaf":
+        src = p.result[1]
+        if out is None:
+            out = Matrix._uninitialised(shape.rows, shape.cols, node.elem_type)
+        elif out is src:
+            return out
+        else:
+            out._reshape_storage(shape.rows, shape.cols)
+        rt.copy_d2d(src.mem, out.mem, shape.n_elem)
+        return out
+    aliased = out is not None and out.mem.buffer_id in p.leaf_buffer_ids()
+    if out is None or aliased:
+        buf = execute_plan(p)
+        if out is None:
+            return Matrix._adopt(buf, shape.rows, shape.cols, node.elem_type)
+        out._adopt_buffer(buf, shape.rows, shape.cols)
+        return out
+    out._reshape_storage(shape.rows, shape.cols)
+    execute_plan(p, target_buf=out.mem)
+    return out
+
+
+def reduce_value(op: str, *xs):
+    """Run a fused scalar reduction and return the numpy scalar."""
+    return execute_plan(plan_reduce(op, *xs))

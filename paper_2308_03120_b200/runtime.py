@@ -1,0 +1,724 @@
+"""Process-wide runtime: the firewall between the expression layer and the
+B200 device library.
+
+Public surface and semantics follow the reference's runtime module
+(reference/pkg/src/devmat/runtime.py:366-703): memory acquisition and
+(stream-ordered) release, a FIFO queue of kernel invocations, scalar
+reductions that return one value to the host, synchronous bulk transfers,
+instrumentation counters, a process singleton with automatic selection.
+What lives *under* the surface is different: the queue is a CUDA stream,
+buffers come from the stream-ordered CUDA memory pool, and every invocation
+is translated into a ``bm_invocation`` C struct and handed to
+libb200mat.so (include/b200mat.h).  Nothing is computed in Python.
+"""
+from __future__ import annotations
+
+import ctypes
+import hashlib
+import os
+import threading
+import time
+from dataclasses import dataclass, field, fields, replace
+
+import numpy as np
+
+from . import _clib
+from . import kernels
+from .errors import BackendError, BufferError_, ElemTypeError
+
+__version__ = "0.1.0"
+
+# "b200" is the device; the reference's backend names are accepted as aliases
+# so `dm.init("parallel")` in existing code lands on the GPU unchanged.
+BACKENDS = ("b200", "reference", "parallel")
+CACHE_DIR_ENV = "KERNEL_CACHE_DIR"
+BACKEND_ENV = "DEFAULT_BACKEND"
+SEED_ENV = "RNG_SEED"
+
+
+# ---------------------------------------------------------------------------
+# domain types (runtime.py:59-144)
+
+@dataclass(frozen=True)
+class DeviceDescriptor:
+    backend_name: str
+    device_id: int
+    worker_count: int
+    supports_f64: bool
+    gpu_name: str = ""
+    sm_count: int = 0
+
+    @property
+    def descriptor_hash(self) -> str:
+        text = (f"backend={self.backend_name};device={self.device_id};gpu={self.gpu_name};"
+                f"sm={self.sm_count};arch=sm_100a;version={__version__}")
+        return hashlib.sha256(text.encode()).hexdigest()[:16]
+
+
+@dataclass(frozen=True)
+class DeviceBuffer:
+    device_id: int
+    buffer_id: int
+    length: int
+    elem_type: str
+    ptr: int = 0          # device address (opaque to the expression layer)
+
+
+@dataclass(frozen=True)
+class FlatView:
+    """1-D strided window into a buffer (elements)."""
+    buf: DeviceBuffer
+    offset: int = 0
+    count: int = -1
+    stride: int = 1
+
+
+@dataclass(frozen=True)
+class BlockView:
+    """2-D column-major window: element (r, c) at offset + r + c * lda."""
+    buf: DeviceBuffer
+    offset: int
+    rows: int
+    cols: int
+    lda: int
+
+
+@dataclass(frozen=True)
+class KernelInvocation:
+    kind: str
+    inputs: tuple = ()
+    output: object = None
+    scalars: tuple = ()
+    params: dict = field(default_factory=dict)
+
+
+@dataclass
+class Counters:
+    launches: int = 0
+    compiles: int = 0
+    cache_hits: int = 0
+    transfers_h2d: int = 0
+    transfers_d2h: int = 0
+    bytes_h2d: int = 0
+    bytes_d2h: int = 0
+    buffers_acquired: int = 0
+    buffers_released: int = 0
+
+    def __sub__(self, other: "Counters") -> "Counters":
+        return Counters(**{f.name: getattr(self, f.name) - getattr(other, f.name) for f in fields(Counters)})
+
+    def copy(self) -> "Counters":
+        return replace(self)
+
+
+# ---------------------------------------------------------------------------
+# translation of KernelInvocation -> bm_invocation
+
+_REDUCE_OP = {"reduce_accu": _clib.BM_R_ACCU, "reduce_min": _clib.BM_R_MIN, "reduce_max": _clib.BM_R_MAX,
+              "reduce_dot": _clib.BM_R_DOT, "accu": _clib.BM_R_ACCU, "min": _clib.BM_R_MIN,
+              "max": _clib.BM_R_MAX, "dot": _clib.BM_R_DOT}
+_RDIM_OP = {"rdim_sum": _clib.BM_R_ACCU, "rdim_min": _clib.BM_R_MIN, "rdim_max": _clib.BM_R_MAX,
+            "rdim_mean": _clib.BM_R_MEAN, "rdim_var": _clib.BM_R_VAR}
+_MOVE_SUB = {"mov_extract_strided": _clib.BM_MOV_EXTRACT, "mov_insert_strided": _clib.BM_MOV_INSERT,
+             "mov_resize": _clib.BM_MOV_RESIZE, "mov_reshape_copy": _clib.BM_MOV_RESHAPE,
+             "mov_join_rows": _clib.BM_MOV_JOIN_ROWS, "mov_join_cols": _clib.BM_MOV_JOIN_COLS,
+             "mov_diagmat_build": _clib.BM_MOV_DIAGMAT, "mov_diagvec_extract": _clib.BM_MOV_DIAGVEC,
+             "gen_repmat": _clib.BM_MOV_REPMAT}
+_NPSTR_TO_ELEM = {np.dtype(v).str: k for k, v in kernels.NP_DTYPE.items()}
+
+
+def scalar_for(k, elem_type: str):
+    """The scalar constant as the device sees it: np.float32(k) / np.float64(k)
+    for floats, dtype(int(k)) for integers with numpy's overflow checks
+    (kernels.py:280-283)."""
+    dt = kernels.NP_DTYPE[elem_type]
+    if dt.kind in "iu":
+        return dt.type(int(k))
+    return dt.type(k)
+
+
+def _fill_view(cv: _clib.View, view) -> None:
+    buf = view.buf
+    cv.base = buf.ptr
+    cv.dtype = _clib.DTYPE_CODE[buf.elem_type]
+    if isinstance(view, FlatView):
+        count = view.count if view.count >= 0 else buf.length
+        cv.offset, cv.count, cv.stride = view.offset, count, view.stride
+        cv.rows, cv.cols, cv.lda = 1, count, view.stride
+        cv.is_block = 0
+    else:
+        cv.offset, cv.count, cv.stride = view.offset, view.rows * view.cols, 1
+        cv.rows, cv.cols, cv.lda = view.rows, view.cols, view.lda
+        cv.is_block = 1
+
+
+def _view_bounds_ok(view) -> bool:
+    buf = view.buf
+    if isinstance(view, FlatView):
+        count = view.count if view.count >= 0 else buf.length
+        if count == 0:
+            return True
+        last = view.offset + view.stride * (count - 1)
+        return view.offset >= 0 and 0 <= last < buf.length
+    if view.rows == 0 or view.cols == 0:
+        return True
+    last = view.offset + (view.cols - 1) * view.lda + (view.rows - 1)
+    return view.offset >= 0 and last < buf.length
+
+
+class _ProgramBuilder:
+    """Encodes a post-order stage program (expr.py:611-657) into opcode triples
+    and a scalar table for one compute dtype."""
+
+    def __init__(self, inv: _clib.Invocation, elem_type: str):
+        self.inv = inv
+        self.elem = elem_type
+        self.n = 0
+        self.ns = 0
+
+    def _push(self, tag: int, op: int, arg: int) -> None:
+        if self.n >= _clib.BM_MAX_PROG:
+            raise BufferError_("fused program longer than the device limit")
+        self.inv.prog[3 * self.n] = tag
+        self.inv.prog[3 * self.n + 1] = op
+        self.inv.prog[3 * self.n + 2] = arg
+        self.n += 1
+
+    def _scalar(self, k) -> int:
+        if self.ns >= _clib.BM_MAX_SCALARS:
+            raise BufferError_("fused program has too many scalars")
+        v = scalar_for(k, self.elem)
+        if kernels.NP_DTYPE[self.elem].kind in "iu":
+            iv = int(v)
+            self.inv.iscalars[self.ns] = iv - (1 << 64) if iv >= (1 << 63) else iv
+            self.inv.fscalars[self.ns] = 0.0
+        else:
+            self.inv.fscalars[self.ns] = float(k)
+            self.inv.iscalars[self.ns] = 0
+        self.ns += 1
+        return self.ns - 1
+
+    def stage(self, st: tuple) -> None:
+        tag = st[0]
+        if tag == "load":
+            self._push(_clib.BM_P_LOAD, 0, int(st[1]))
+        elif tag == "unary":
+            op = st[1]
+            if op == "eop_pow":
+                k = st[2]
+                if kernels.NP_DTYPE[self.elem].kind in "iu" and int(k) < 0:
+                    raise ValueError("Integers to negative integer powers are not allowed.")
+                self._push(_clib.BM_P_UNARY, _clib.UNARY_CODE[op], self._scalar(k))
+            else:
+                self._push(_clib.BM_P_UNARY, _clib.UNARY_CODE[op], -1)
+        elif tag == "scalar":
+            self._push(_clib.BM_P_SCALAR, _clib.SCALAR_CODE[st[1]], self._scalar(st[2]))
+        elif tag == "glue":
+            self._push(_clib.BM_P_GLUE, _clib.GLUE_CODE[st[1]], 0)
+        else:
+            raise KeyError(tag)
+
+    def finish(self) -> None:
+        self.inv.n_prog = self.n
+        self.inv.n_scalars = self.ns
+
+
+def _single_stage_program(kind: str, scalars: tuple, n_in: int) -> tuple:
+    if kind in kernels.EGLUE:
+        return (("load", 0), ("load", 1), ("glue", kind))
+    if kind in kernels.EOP_SCALAR:
+        return (("load", 0), ("scalar", kind, scalars[0]))
+    if kind in kernels.EOP_UNARY:
+        return (("load", 0), ("unary", kind, scalars[0] if scalars else None))
+    raise KeyError(kind)
+
+
+def build_invocation(inv: KernelInvocation) -> _clib.Invocation:
+    """KernelInvocation (runtime.py:103-109) -> bm_invocation (b200mat.h)."""
+    c = _clib.Invocation()
+    kind = inv.kind
+    ins = list(inv.inputs)
+    if len(ins) > _clib.BM_MAX_INPUTS:
+        raise BufferError_("too many inputs for one device invocation")
+    c.n_inputs = len(ins)
+    for i, v in enumerate(ins):
+        _fill_view(c.inputs[i], v)
+    if inv.output is not None:
+        c.has_output = 1
+        _fill_view(c.output, inv.output)
+    p = inv.params
+
+    if kind in kernels.ELEMENTWISE or kind == "fused_chain" or kind == "mov_copy":
+        c.kind = _clib.BM_K_EWISE
+        if kind == "fused_chain":
+            elem = _NPSTR_TO_ELEM[np.dtype(p["compute_dtype"]).str]
+            program = p["program"]
+        elif kind == "mov_copy":
+            elem = ins[0].buf.elem_type
+            program = (("load", 0),)
+        else:
+            elem = ins[0].buf.elem_type
+            program = _single_stage_program(kind, inv.scalars, len(ins))
+        c.compute_dtype = _clib.DTYPE_CODE[elem]
+        pb = _ProgramBuilder(c, elem)
+        for st in program:
+            pb.stage(st)
+        pb.finish()
+        return c
+    if kind in _REDUCE_OP or kind == "fused_reduce":
+        c.kind = _clib.BM_K_REDUCE
+        if kind == "fused_reduce":
+            elem = _NPSTR_TO_ELEM[np.dtype(p["compute_dtype"]).str]
+            program = p["program"]
+            c.reduce_op = _REDUCE_OP[p["op"]]
+        else:
+            elem = ins[0].buf.elem_type
+            c.reduce_op = _REDUCE_OP[kind]
+            program = (("load", 0), ("load", 1)) if kind == "reduce_dot" else (("load", 0),)
+        c.compute_dtype = _clib.DTYPE_CODE[elem]
+        pb = _ProgramBuilder(c, elem)
+        for st in program:
+            pb.stage(st)
+        pb.finish()
+        return c
+    if kind in _RDIM_OP:
+        c.kind = _clib.BM_K_RDIM
+        c.reduce_op = _RDIM_OP[kind]
+        c.dim = int(p["dim"])
+        c.compute_dtype = _clib.DTYPE_CODE[ins[0].buf.elem_type]
+        return c
+    if kind == "gemm":
+        c.kind = _clib.BM_K_GEMM
+        c.trans_a = int(p.get("trans_a", 0))
+        c.trans_b = int(p.get("trans_b", 0))
+        c.compute_dtype = _clib.DTYPE_CODE[ins[0].buf.elem_type]
+        return c
+    if kind == "mov_transpose":
+        c.kind = _clib.BM_K_TRANSPOSE
+        return c
+    if kind in _MOVE_SUB:
+        c.kind = _clib.BM_K_STRIDED_COPY
+        c.sub_kind = _MOVE_SUB[kind]
+        if kind == "mov_diagvec_extract":
+            c.iparams[0] = int(p["k"])
+        if kind == "gen_repmat":
+            c.iparams[0] = int(p["rows_out"])
+        return c
+    if kind == "gen_fill_const":
+        c.kind = _clib.BM_K_FILL
+        out_dt = kernels.NP_DTYPE[inv.output.buf.elem_type]
+        gen_val = scalar_for(inv.scalars[0], p["gen_type"])
+        with np.errstate(invalid="ignore", over="ignore"):
+            bits = np.array([gen_val]).astype(out_dt)
+        raw = bits.tobytes() + b"\0" * (8 - out_dt.itemsize)
+        c.iparams[0] = int(np.frombuffer(raw, dtype=np.int64)[0])
+        return c
+    if kind == "gen_eye":
+        c.kind = _clib.BM_K_EYE
+        out_dt = kernels.NP_DTYPE[inv.output.buf.elem_type]
+        one = np.array([kernels.NP_DTYPE[p["gen_type"]].type(1)]).astype(out_dt)
+        raw = one.tobytes() + b"\0" * (8 - out_dt.itemsize)
+        c.iparams[0] = int(np.frombuffer(raw, dtype=np.int64)[0])
+        c.iparams[2] = int(p["rows"])
+        return c
+    if kind == "gen_linspace":
+        c.kind = _clib.BM_K_LINSPACE
+        c.compute_dtype = _clib.DTYPE_CODE[p["gen_type"]]
+        c.fscalars[0] = float(inv.scalars[0])
+        c.fscalars[1] = float(inv.scalars[1])
+        c.n_scalars = 2
+        c.iparams[0] = int(p["n"])
+        return c
+    if kind in ("gen_randu", "gen_randn"):
+        c.kind = _clib.BM_K_RANDU if kind == "gen_randu" else _clib.BM_K_RANDN
+        c.compute_dtype = _clib.DTYPE_CODE[p["gen_type"]]
+        c.iparams[0] = rng_key(int(p["seed"]), int(p["stream"]))
+        return c
+    raise NotImplementedError(f"kernel kind {kind!r} is not provided by the B200 device library")
+
+
+_M64 = (1 << 64) - 1
+
+
+def _mix64_int(x: int) -> int:
+    z = (x + 0x9E3779B97F4A7C15) & _M64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return z ^ (z >> 31)
+
+
+def rng_key(seed: int, stream: int) -> int:
+    """Per-fill key of the counter RNG (kernels.py:243), as a signed int64."""
+    key = _mix64_int((seed & _M64) ^ _mix64_int(stream & _M64))
+    return key - (1 << 64) if key >= (1 << 63) else key
+
+
+# ---------------------------------------------------------------------------
+# runtime
+
+class Runtime:
+    def __init__(self, descriptor: DeviceDescriptor, print_info: bool):
+        self.descriptor = descriptor
+        self.counters = Counters()
+        self._lock = threading.RLock()
+        self._next_buffer_id = 0
+        self._next_stream_id = 0
+        self.seed = int(os.environ.get(SEED_ENV, "42"))
+        self._section_mark = Counters()
+        self._live: dict[int, int] = {}     # buffer_id -> device pointer
+        self._lib = _clib.lib()
+        self._jit_base = self._native_counters()
+        if print_info:
+            d = descriptor
+            print(f"b200mat runtime: backend={d.backend_name} device={d.device_id} gpu={d.gpu_name} "
+                  f"sms={d.sm_count} arch=sm_100a f64=yes jit_cache={'on' if os.environ.get('BM_CACHE_DIR', '1') else 'off'}")
+
+    # -- instrumentation -----------------------------------------------------------
+    def _native_counters(self) -> _clib.Counters:
+        c = _clib.Counters()
+        self._lib.bm_get_counters(ctypes.byref(c))
+        return c
+
+    def kernel_inventory_size(self) -> int:
+        return len(kernels.ALL_KINDS)
+
+    def _sync_jit_counters(self) -> None:
+        n = self._native_counters()
+        self.counters.compiles = n.jit_compiles - self._jit_base.jit_compiles
+        self.counters.cache_hits = n.jit_cache_hits - self._jit_base.jit_cache_hits
+
+    # -- memory ------------------------------------------------------------------------
+    def acquire_memory(self, n: int, elem_type: str) -> DeviceBuffer:
+        if n < 0:
+            raise ValueError("negative buffer length")
+        if elem_type not in kernels.ELEM_TYPES:
+            raise TypeError(f"unknown element type {elem_type!r}")
+        ptr = ctypes.c_void_p()
+        _clib.check(self._lib.bm_alloc(n * kernels.itemsize(elem_type), ctypes.byref(ptr)), "acquire_memory")
+        with self._lock:
+            buf = DeviceBuffer(self.descriptor.device_id, self._next_buffer_id, n, elem_type, ptr.value or 0)
+            self._next_buffer_id += 1
+            self._live[buf.buffer_id] = buf.ptr
+            self.counters.buffers_acquired += 1
+        return buf
+
+    def _retire(self, buf: DeviceBuffer) -> int:
+        with self._lock:
+            ptr = self._live.pop(buf.buffer_id, None)
+            if ptr is None:
+                raise BufferError_(f"double release of buffer #{buf.buffer_id}")
+            self.counters.buffers_released += 1
+        return ptr
+
+    def release(self, buf: DeviceBuffer) -> None:
+        """Release now; the handle becomes invalid (the memory returns to the
+        pool once work already queued on the stream has finished)."""
+        _clib.check(self._lib.bm_free(self._retire(buf)), "release")
+
+    def release_deferred(self, buf: DeviceBuffer) -> None:
+        """Stream-ordered release (runtime.py:449-451): cudaFreeAsync."""
+        _clib.check(self._lib.bm_free_async(self._retire(buf)), "release_deferred")
+
+    def live(self, buf: DeviceBuffer) -> bool:
+        return buf.buffer_id in self._live
+
+    def next_stream_id(self) -> int:
+        with self._lock:
+            s = self._next_stream_id
+            self._next_stream_id += 1
+        return s
+
+    # -- queue ---------------------------------------------------------------------------
+    def _validate(self, inv: KernelInvocation) -> None:
+        views = list(inv.inputs) + ([inv.output] if inv.output is not None else [])
+        for v in views:
+            if v.buf.device_id != self.descriptor.device_id:
+                raise BufferError_("cross-device buffer mix")
+            if v.buf.buffer_id not in self._live:
+                raise BufferError_(f"use of released buffer #{v.buf.buffer_id}")
+            if not _view_bounds_ok(v):
+                raise BufferError_(f"view out of bounds ({v!r})")
+
+    def enqueue(self, inv: KernelInvocation) -> None:
+        self._validate(inv)
+        c = build_invocation(inv)
+        _clib.check(self._lib.bm_enqueue(ctypes.byref(c)), inv.kind)
+        with self._lock:
+            self.counters.launches += 1
+
+    def synchronise(self) -> None:
+        _clib.check(self._lib.bm_sync(), "synchronise")
+
+    def execute_reduce(self, inv: KernelInvocation):
+        """Enqueue a reducing invocation, wait, and return its scalar as a
+        numpy scalar of the element type (one device-to-host transfer)."""
+        self._validate(inv)
+        c = build_invocation(inv)
+        elem = {v: k for k, v in _clib.DTYPE_CODE.items()}[c.compute_dtype]
+        dt = kernels.NP_DTYPE[elem]
+        raw = (ctypes.c_char * 8)()
+        rc = self._lib.bm_execute_reduce(ctypes.byref(c), raw)
+        with self._lock:
+            self.counters.launches += 1
+        _clib.check(rc, inv.kind)
+        value = np.frombuffer(bytes(raw)[: dt.itemsize], dtype=dt)[0]
+        nbytes = kernels.itemsize(inv.inputs[0].buf.elem_type) if inv.inputs else 8
+        with self._lock:
+            self.counters.transfers_d2h += 1
+            self.counters.bytes_d2h += nbytes
+        return value
+
+    # -- transfers --------------------------------------------------------------------------
+    def copy_h2d(self, host: np.ndarray, buf: DeviceBuffer, offset: int = 0) -> None:
+        if buf.buffer_id not in self._live:
+            raise BufferError_(f"use of released buffer #{buf.buffer_id}")
+        arr = np.ascontiguousarray(np.asarray(host).reshape(-1).astype(kernels.NP_DTYPE[buf.elem_type], copy=False))
+        if offset < 0 or offset + arr.shape[0] > buf.length:
+            raise BufferError_("host copy out of bounds")
+        isz = arr.itemsize
+        _clib.check(self._lib.bm_h2d(buf.ptr + offset * isz, arr.ctypes.data, arr.nbytes), "copy_h2d")
+        with self._lock:
+            self.counters.transfers_h2d += 1
+            self.counters.bytes_h2d += arr.nbytes
+
+    def copy_d2h(self, buf: DeviceBuffer, offset: int = 0, count: int = -1) -> np.ndarray:
+        if buf.buffer_id not in self._live:
+            raise BufferError_(f"use of released buffer #{buf.buffer_id}")
+        dt = kernels.NP_DTYPE[buf.elem_type]
+        n = buf.length - offset if count < 0 else count
+        if offset < 0 or n < 0 or offset + n > buf.length:
+            raise BufferError_("device copy out of bounds")
+        out = np.empty(n, dtype=dt)
+        if n:
+            _clib.check(self._lib.bm_d2h(out.ctypes.data, buf.ptr + offset * dt.itemsize, out.nbytes), "copy_d2h")
+        else:
+            self.synchronise()
+        with self._lock:
+            self.counters.transfers_d2h += 1
+            self.counters.bytes_d2h += out.nbytes
+        return out
+
+    def copy_d2d(self, src: DeviceBuffer, dst: DeviceBuffer, count: int = -1) -> None:
+        """Device-side memcpy on the stream; neither a launch nor a host transfer."""
+        for b in (src, dst):
+            if b.buffer_id not in self._live:
+                raise BufferError_(f"use of released buffer #{b.buffer_id}")
+        n = src.length if count < 0 else count
+        if n > src.length or n > dst.length:
+            raise BufferError_("d2d copy out of bounds")
+        nbytes = n * kernels.itemsize(src.elem_type)
+        _clib.check(self._lib.bm_d2d(dst.ptr, src.ptr, nbytes), "copy_d2d")
+
+    def read_scalar(self, buf: DeviceBuffer, index: int):
+        return self.read_elems(buf, [index])[0]
+
+    def read_elems(self, buf: DeviceBuffer, indices) -> np.ndarray:
+        if buf.buffer_id not in self._live:
+            raise BufferError_(f"use of released buffer #{buf.buffer_id}")
+        idx = np.ascontiguousarray(np.asarray(indices, dtype=np.int64).reshape(-1))
+        if idx.size and (idx.min() < 0 or idx.max() >= buf.length):
+            raise BufferError_("element index out of bounds")
+        dt = kernels.NP_DTYPE[buf.elem_type]
+        out = np.empty(idx.shape[0], dtype=dt)
+        _clib.check(self._lib.bm_read_elems(buf.ptr, _clib.DTYPE_CODE[buf.elem_type],
+                                            idx.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), idx.shape[0],
+                                            out.ctypes.data), "read_elems")
+        with self._lock:
+            self.counters.transfers_d2h += 1
+            self.counters.bytes_d2h += out.nbytes
+        return out
+
+    def write_scalar(self, buf: DeviceBuffer, index: int, value) -> None:
+        if buf.buffer_id not in self._live:
+            raise BufferError_(f"use of released buffer #{buf.buffer_id}")
+        if not 0 <= index < buf.length:
+            raise BufferError_("element index out of bounds")
+        dt = kernels.NP_DTYPE[buf.elem_type]
+        arr = np.array([value]).astype(dt)
+        _clib.check(self._lib.bm_write_elem(buf.ptr, _clib.DTYPE_CODE[buf.elem_type], index, arr.ctypes.data),
+                    "write_scalar")
+        with self._lock:
+            self.counters.transfers_h2d += 1
+            self.counters.bytes_h2d += dt.itemsize
+
+    # -- counters ---------------------------------------------------------------------------
+    def counters_snapshot(self) -> Counters:
+        with self._lock:
+            self._sync_jit_counters()
+            return self.counters.copy()
+
+    def counters_reset_section(self) -> Counters:
+        with self._lock:
+            self._sync_jit_counters()
+            delta = self.counters - self._section_mark
+            self._section_mark = self.counters.copy()
+        return delta
+
+    def stop(self) -> None:
+        _clib.check(self._lib.bm_sync(), "shutdown")
+
+
+# ---------------------------------------------------------------------------
+# singleton management (runtime.py:563-690)
+
+_runtime: Runtime | None = None
+_runtime_lock = threading.Lock()
+_generation = 0
+
+
+def device_count() -> int:
+    n = ctypes.c_int(0)
+    rc = _clib.lib().bm_device_count(ctypes.byref(n))
+    return n.value if rc == 0 else 0
+
+
+def _make_descriptor(backend: str, device_id: int, worker_count: int | None) -> DeviceDescriptor:
+    if backend not in BACKENDS:
+        raise BackendError(f"unknown backend {backend!r}; valid backends: {', '.join(BACKENDS)}")
+    if backend == "reference" and device_id != 0:
+        raise BackendError("reference backend exposes a single device id 0")
+    if worker_count is not None and worker_count < 1:
+        raise BackendError("worker_count must be >= 1")
+    n = device_count()
+    if n == 0:
+        raise BackendError(f"no CUDA device available: {_clib.last_error()} (there is no CPU fallback)")
+    if not 0 <= device_id < n:
+        raise BackendError(f"device id {device_id} out of range: {n} CUDA device(s) visible")
+    return DeviceDescriptor(backend, device_id, worker_count or 1, True)
+
+
+def init(backend: str | None = None, print_info: bool = False, device_id: int = 0,
+         worker_count: int | None = None) -> None:
+    """Select and start the device; at most once before shutdown()."""
+    global _runtime, _generation
+    with _runtime_lock:
+        if _runtime is not None:
+            raise BackendError("runtime already initialised; call shutdown() first")
+        if backend is None:
+            backend = os.environ.get(BACKEND_ENV) or "b200"
+        desc = _make_descriptor(backend, device_id, worker_count)
+        lib = _clib.lib()
+        _clib.check(lib.bm_init(desc.device_id), "bm_init")
+        name = ctypes.create_string_buffer(128)
+        sms = ctypes.c_int()
+        lib.bm_device_info(name, 128, ctypes.byref(sms), None, None, None)
+        desc = replace(desc, gpu_name=name.value.decode(), sm_count=sms.value)
+        _runtime = Runtime(desc, print_info)
+        _generation += 1
+
+
+def shutdown() -> None:
+    """Drain the stream, free every live buffer, clear the singleton."""
+    global _runtime, _generation
+    with _runtime_lock:
+        if _runtime is None:
+            return
+        rt = _runtime
+        _generation += 1
+        try:
+            rt.stop()
+        finally:
+            with rt._lock:
+                for bid, ptr in list(rt._live.items()):
+                    rt._lib.bm_free_async(ptr)
+                    rt.counters.buffers_released += 1
+                rt._live.clear()
+            _clib.lib().bm_shutdown()
+            _runtime = None
+
+
+def get_runtime() -> Runtime:
+    rt = _runtime
+    if rt is None:
+        try:
+            init()
+        except BackendError:
+            if _runtime is None:
+                raise
+        rt = _runtime
+    return rt
+
+
+def is_initialised() -> bool:
+    return _runtime is not None
+
+
+def generation() -> int:
+    return _generation
+
+
+def release_if_current(gen: int, buf: DeviceBuffer) -> None:
+    """GC finalizer hook: stream-ordered release iff the owning runtime lives."""
+    rt = _runtime
+    if rt is None or gen != _generation:
+        return
+    try:
+        rt.release_deferred(buf)
+    except Exception:
+        pass
+
+
+def set_seed(seed: int) -> None:
+    rt = get_runtime()
+    with rt._lock:
+        rt.seed = int(seed)
+        rt._next_stream_id = 0
+
+
+def counters() -> Counters:
+    return get_runtime().counters_snapshot()
+
+
+def synchronise() -> None:
+    if _runtime is not None:
+        _runtime.synchronise()
+
+
+class wall_clock:
+    """tic/toc timer (runtime.py:693-703)."""
+
+    def __init__(self):
+        self._t0 = time.perf_counter()
+
+    def tic(self) -> None:
+        self._t0 = time.perf_counter()
+
+    def toc(self) -> float:
+        return time.perf_counter() - self._t0
+
+
+class _PinnedBlock:
+    def __init__(self, nbytes: int):
+        ptr = ctypes.c_void_p()
+        _clib.check(_clib.lib().bm_host_alloc_pinned(max(nbytes, 1), ctypes.byref(ptr)), "pinned alloc")
+        self.ptr = ptr.value
+        self.nbytes = nbytes
+
+    def __del__(self):
+        try:
+            _clib.lib().bm_host_free_pinned(self.ptr)
+        except Exception:
+            pass
+
+
+def pinned_array(shape, dtype) -> np.ndarray:
+    """A numpy array in page-locked host memory (fast, asynchronous-capable
+    host<->device copies).  The memory lives as long as the array."""
+    dt = np.dtype(dtype)
+    n = int(np.prod(shape)) * dt.itemsize
+    block = _PinnedBlock(n)
+    buf = (ctypes.c_char * max(n, 1)).from_address(block.ptr)
+    arr = np.frombuffer(buf, dtype=dt, count=int(np.prod(shape))).reshape(shape)
+    arr.setflags(write=True)
+    _pinned_owners[id(arr)] = block
+    import weakref
+    weakref.finalize(arr, _pinned_owners.pop, id(arr), None)
+    return arr
+
+
+_pinned_owners: dict = {}
+
+
+def check_elem_type(elem_type: str) -> None:
+    if elem_type not in kernels.ELEM_TYPES:
+        raise ElemTypeError(f"unknown element type {elem_type!r}")

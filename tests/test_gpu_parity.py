@@ -1,0 +1,271 @@
+"""GPU parity: the CUDA path against the reference's golden vectors and the
+CPU oracle on the same seeded inputs.
+
+Bars: IEEE-exact element-wise ops, integer ops, casts and the
+reduction *order* are bit-exact; transcendental ops are ULP-bounded
+(rtol 2e-6, the reference's own test precedent, tests/test_kernels.py:36-45);
+dot/norm within 1e-5 (f32) / 1e-12 (f64); GEMM normwise within 1e-5 / 1e-12.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+
+def same(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    assert a.dtype == b.dtype, (a.dtype, b.dtype)
+    assert a.shape == b.shape, (a.shape, b.shape)
+    if a.tobytes() != b.tobytes():
+        bad = np.argwhere(a.reshape(-1).view(np.uint8) != b.reshape(-1).view(np.uint8))
+        raise AssertionError(f"not bit-identical; first differing byte {bad[:3].ravel()} "
+                             f"{a.reshape(-1)[:4]} vs {b.reshape(-1)[:4]}")
+
+
+def ulp_close(a, b, rtol):
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    np.testing.assert_allclose(a, b, rtol=rtol, atol=0)
+
+
+def normwise(got, want, tol):
+    got, want = np.asarray(got, dtype=np.float64), np.asarray(want, dtype=np.float64)
+    err = np.abs(got - want).max() / max(np.abs(want).max(), 1.0)
+    assert err <= tol, err
+
+
+def rel_err(got, want):
+    return abs(float(got) - float(want)) / max(abs(float(want)), 1.0)
+
+
+# ---- element-wise ----------------------------------------------------------------------------
+
+def test_config1_chain_and_accu_vs_reference(dm):
+    g = golden("chains")
+    for tag in ("a", "b", "c"):
+        A, B, C, D = (dm.Matrix.from_numpy(g[f"{tag}_{x}"]) for x in "ABCD")
+        same(dm.evaluate(2 * A + B % C - D).to_numpy(), g[f"{tag}_chain_noexp"])
+        # exp differs from numpy's SIMD expf by ulps; cancellation in 2A+BC-exp(D)
+        # makes a relative-per-element bound meaningless, so use the reference's
+        # own metric (tests/dag_util.py:84-95): max|err| / max(max|want|, 1)
+        normwise(dm.evaluate(2 * A + B % C - dm.exp(D)).to_numpy(), g[f"{tag}_chain_exp"], 1e-6)
+        # the reduction order is the reference's: bit-exact without transcendentals
+        same(np.float32(dm.accu(2 * A + B % C - D)), g[f"{tag}_accu_noexp"])
+        assert rel_err(dm.accu(2 * A + B % C - dm.exp(D)), g[f"{tag}_accu_exp"]) <= 1e-5
+        # sqrt and the arithmetic are IEEE-exact: bit-identical
+        same(dm.evaluate(dm.sqrt(dm.absolute(A - 0.5) + 1.0) / (B + 1) * 3 - C % D + 0.25).to_numpy(),
+             g[f"{tag}_deep"])
+
+
+@pytest.mark.parametrize("name", ["exp", "log", "log10", "sqrt", "square", "abs", "cos", "sin", "tan", "acos",
+                                  "asin", "atan"])
+def test_unary_vs_reference(dm, name):
+    g = golden("ops")
+    fn = getattr(dm, "absolute" if name == "abs" else name)
+    for dt, key in (("f32", "xf"), ("f64", "xd")):
+        got = dm.evaluate(fn(dm.Matrix.from_numpy(g[key]))).to_numpy()
+        if name in ("sqrt", "square", "abs"):
+            same(got, g[f"{dt}_{name}"])
+        else:
+            ulp_close(got, g[f"{dt}_{name}"], 2e-6 if dt == "f32" else 1e-12)
+    ulp_close(dm.evaluate(dm.power(dm.Matrix.from_numpy(g["xf"]), 3)).to_numpy(), g["f32_pow3"], 1e-6)
+    ulp_close(dm.evaluate(dm.power(dm.Matrix.from_numpy(g["xd"]), 2.5)).to_numpy(), g["f64_pow2_5"], 1e-13)
+
+
+def test_integer_ops_bit_exact(dm):
+    g = golden("ops")
+    mi, mj, mu = (dm.Matrix.from_numpy(g[k]) for k in ("xi", "yi", "xu"))
+    same(dm.evaluate(mi % mi + 3 - mj * 7).to_numpy(), g["i32_chain"])
+    same(dm.evaluate(mi / 7).to_numpy(), g["i32_div_scalar"])
+    same(dm.evaluate(1000 / (mj % mj + 1)).to_numpy(), g["i32_div_pre"])
+    same(dm.evaluate(mi / mj).to_numpy(), g["i32_div_glue"])
+    same(dm.evaluate(dm.square(mi * 1000)).to_numpy(), g["i32_square"])
+    same(dm.evaluate(dm.absolute(mj)).to_numpy(), g["i32_abs"])
+    same(dm.evaluate(dm.power(mj, 3)).to_numpy(), g["i32_pow"])
+    same(dm.evaluate(dm.sqrt(dm.absolute(mi))).to_numpy(), g["i32_sqrt"])
+    same(dm.evaluate(mu * 3 + 7 - mu / 5).to_numpy(), g["u64_chain"])
+    same(dm.evaluate(5 - mu).to_numpy(), g["u64_minus_pre"])
+    same(dm.evaluate(mu / dm.evaluate(mu * 0)).to_numpy(), g["u64_div0"])
+
+
+def test_casts_bit_exact(dm):
+    g = golden("casts")
+    for src, key in (("edge_f64", "edge"), ("edge_f32", "edge_f32"), ("iv", "iv"), ("uv", "uv")):
+        m = dm.Matrix.from_numpy(g[src])
+        for k in [k for k in g if k.startswith(key + "_to_")]:
+            t = k.rsplit("_", 1)[1]
+            got = dm.evaluate(dm.conv_to(m, t)).to_numpy()
+            want = g[k]
+            if want.dtype.kind == "f":
+                # NaN payloads differ between x86 and the GPU; compare NaN-aware
+                np.testing.assert_array_equal(np.isnan(got), np.isnan(want))
+                ok = ~np.isnan(want)
+                same(got[ok], want[ok])
+            else:
+                same(got, want)
+
+
+def test_fused_two_way_conversion_equals_convert_after(dm):
+    rng = np.random.default_rng(17)
+    a = dm.Matrix.from_numpy(rng.random((9, 9), dtype=np.float32))
+    scaled = 10 * a + 1
+    for target in ("f64", "i32", "u64"):
+        fused = dm.evaluate(dm.conv_to(scaled, target)).to_numpy()
+        plain = dm.evaluate(scaled)
+        conv = dm.evaluate(dm.conv_to(plain, target), fuse=False).to_numpy()
+        same(fused, conv)
+
+
+def test_strided_views(dm):
+    rng = np.random.default_rng(3)
+    x = rng.random((40, 30), dtype=np.float32)
+    m = dm.Matrix.from_numpy(x)
+    same(dm.evaluate(2 * m.submat(3, 4, 33, 24) + 1).to_numpy(),
+         O.apply_scalar("eop_scalar_plus", O.apply_scalar("eop_scalar_times", x[3:34, 4:25], 2, np.float32), 1,
+                        np.float32))
+    same(dm.evaluate(m.row(5) * 3).to_numpy(), (x[5:6, :] * np.float32(3)))
+    same(dm.evaluate(m.diag() + 0).to_numpy(), np.diagonal(x).reshape(-1, 1).copy())
+
+
+def test_large_vector_vectorised_and_tail(dm):
+    n = (1 << 16) * 2 + 17
+    rng = np.random.default_rng(5)
+    v = rng.random(n, dtype=np.float32)
+    mv = dm.Matrix.from_numpy(v.reshape(-1, 1))
+    same(dm.evaluate(2 * mv).to_numpy().reshape(-1), v * np.float32(2))
+
+
+# ---- scalar reductions ------------------------------------------------------------------------
+
+def test_accu_dot_norm_vs_reference(dm):
+    g = golden("reduce")
+    for key in [k for k in g if k.endswith("_accu") and k[0] == "f"]:
+        base = key[: -len("_accu")]
+        x, y = g[base + "_x"], g[base + "_y"]
+        mx, my = dm.Matrix.from_numpy(x.reshape(-1, 1)), dm.Matrix.from_numpy(y.reshape(-1, 1))
+        tol = 1e-5 if x.dtype == np.float32 else 1e-12
+        same(np.array(dm.accu(mx), dtype=x.dtype), g[key])          # numpy order reproduced
+        assert rel_err(dm.dot(mx, my), g[base + "_dot"]) <= tol
+        assert rel_err(dm.norm(mx, 2), g[base + "_norm2"]) <= tol
+        assert dm.norm(mx, "inf") == float(g[base + "_norminf"])
+        assert dm.norm(mx, "-inf") == float(g[base + "_normm"])
+        assert rel_err(dm.norm(mx, 3), g[base + "_norm3"]) <= (1e-5 if x.dtype == np.float32 else 1e-12)
+    assert dm.accu(dm.Matrix.from_numpy(g["i32_x"].reshape(-1, 1))) == int(g["i32_accu"])
+    assert dm.accu(dm.Matrix.from_numpy(g["u64_x"].reshape(-1, 1))) == int(g["u64_accu"])
+
+
+def test_min_max_nan_semantics(dm):
+    g = golden("reduce")
+    for case in ("nan_first", "nan_second_block", "nan_two"):
+        m = dm.Matrix.from_numpy(g[f"mm_{case}_x"].reshape(-1, 1))
+        for op, key in (("min", "reduce_min"), ("max", "reduce_max")):
+            got = np.float32(getattr(dm, f"reduce_{op}")(m))
+            want = g[f"mm_{case}_{key}"]
+            assert (np.isnan(got) and np.isnan(want)) or got == want, (case, op, got, want)
+
+
+def test_min_max_empty_raises(dm):
+    e = dm.Col(0)
+    with pytest.raises(ValueError):
+        dm.reduce_min(e)
+    assert dm.accu(dm.Matrix(0, 0)) == 0
+
+
+@pytest.mark.parametrize("n", [1, 5, 127, 128, 129, 2047, 2048, 2049, 8192 * 5 + 3, 1 << 20, (1 << 20) + 999])
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_accu_bit_exact_sizes(dm, n, dt):
+    rng = np.random.default_rng(n)
+    v = (rng.standard_normal(n) * np.exp2(rng.integers(-16, 16, n))).astype(dt)
+    m = dm.Matrix.from_numpy(v.reshape(-1, 1))
+    same(np.array(dm.accu(m), dtype=dt), O.reduce_accu(v))
+
+
+def test_accu_fused_expression_bit_exact_large(dm):
+    rng = np.random.default_rng(0)
+    A, B, C, D = (rng.random((1024, 1024), dtype=np.float32) for _ in range(4))
+    mA, mB, mC, mD = (dm.Matrix.from_numpy(x) for x in (A, B, C, D))
+    flat = [x.reshape(-1, order="F") for x in (A, B, C, D)]
+    prog = (("load", 0), ("scalar", "eop_scalar_times", 2), ("load", 1), ("load", 2), ("glue", "eglue_schur"),
+            ("glue", "eglue_plus"), ("load", 3), ("glue", "eglue_minus"))
+    same(np.float32(dm.accu(2 * mA + mB % mC - mD)), O.reduce_accu(O.run_program(prog, flat, np.float32)))
+
+
+# ---- per-dimension reductions ------------------------------------------------------------------
+
+def test_rdim_vs_reference(dm):
+    g = golden("rdim")
+    for key in [k for k in g if k.count("_") == 1]:
+        a = g[key]
+        m = dm.Matrix.from_numpy(a)
+        for op in ("sum", "min", "max", "mean", "var", "stddev"):
+            for dim in (0, 1):
+                want = g.get(f"{key}_{op}{dim}")
+                if want is None:
+                    continue
+                got = dm.evaluate(getattr(dm, op)(m, dim)).to_numpy()
+                if op in ("var", "stddev"):
+                    tol = 1e-5 if a.dtype == np.float32 else 1e-12
+                    np.testing.assert_allclose(got, want, rtol=tol, atol=tol)
+                else:
+                    same(got, want)
+
+
+@pytest.mark.parametrize("shape", [(16384, 64), (2048, 3000), (1000, 1000), (4096, 4096)])
+def test_rdim_large_bit_exact(dm, shape):
+    rng = np.random.default_rng(1)
+    a = rng.random(shape)
+    m = dm.Matrix.from_numpy(a)
+    for op in ("sum", "min", "max"):
+        for dim in (0, 1):
+            same(dm.evaluate(getattr(dm, op)(m, dim)).to_numpy(), O.rdim(op, a, dim))
+
+
+# ---- GEMM ----------------------------------------------------------------------------------------
+
+def test_gemm_vs_reference(dm):
+    g = golden("gemm")
+    for dt, tol in (("f32", 1e-5), ("f64", 1e-12)):
+        a, b, bt = (dm.Matrix.from_numpy(g[f"{dt}_{k}"]) for k in ("a", "b", "bt"))
+        for got, key in ((dm.gemm(a, b), "ab"), (dm.evaluate(a @ bt.t()), "abt")):
+            want = g[f"{dt}_{key}"]
+            err = np.abs(got.to_numpy().astype(np.float64) - want).max() / np.abs(want).max()
+            assert err <= tol, (dt, key, err)
+    same(dm.gemm(dm.Matrix.from_numpy(g["i32_a"]), dm.Matrix.from_numpy(g["i32_a"])).to_numpy(), g["i32_aa"])
+    z = dm.evaluate(dm.Matrix(3, 0) @ dm.Matrix(0, 4)).to_numpy()
+    same(z, g["f32_inner0"])
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("m,n,k", [(256, 256, 256), (512, 384, 1024), (1000, 777, 333), (128, 128, 4096)])
+@pytest.mark.parametrize("tb", [0, 1])
+def test_gemm_shapes(dm, dt, m, n, k, tb):
+    rng = np.random.default_rng(m + n + k)
+    a = rng.random((m, k)).astype(dt)
+    b = rng.random((n, k) if tb else (k, n)).astype(dt)
+    ma, mb = dm.Matrix.from_numpy(a), dm.Matrix.from_numpy(b)
+    got = dm.evaluate(ma @ (mb.t() if tb else mb)).to_numpy().astype(np.float64)
+    ref = a.astype(np.float64) @ (b.T if tb else b).astype(np.float64)
+    err = np.abs(got - ref).max() / np.abs(ref).max()
+    assert err <= (1e-5 if dt == np.float32 else 1e-12), err
+
+
+def test_logistic_step_vs_reference(dm):
+    g = golden("misc")
+    X, w, y = (dm.Matrix.from_numpy(g[k]) for k in ("lr_X", "lr_w", "lr_y"))
+    z = dm.evaluate(X @ w)
+    r = dm.evaluate(1 / (1 + dm.exp(0 - z)) - y)
+    gr = dm.evaluate(X.t() @ r)
+    ulp_close(r.to_numpy(), g["lr_r"], 1e-5)
+    np.testing.assert_allclose(gr.to_numpy(), g["lr_g"], rtol=1e-4, atol=1e-5)
+    assert rel_err(dm.accu(r), g["lr_s"]) <= 1e-4
+
+
+def test_rng_bit_exact(dm):
+    g = golden("misc")
+    for seed, elem in ((123, "f32"), (777, "f64")):
+        dm.set_seed(seed)
+        same(dm.Matrix(40, 25, fill="randu", elem_type=elem).to_numpy(), g[f"randu_{seed}"])
+        got = dm.Matrix(33, 17, fill="randn", elem_type=elem).to_numpy()
+        ulp_close(got, g[f"randn_{seed}"], 1e-6 if elem == "f32" else 1e-13)

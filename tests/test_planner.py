@@ -1,0 +1,191 @@
+"""Host-side planner behaviour (no device): plan shapes, fusion, transpose
+folding, fused reductions, and NVRTC compilation of the emitted programs."""
+import ctypes
+import itertools
+
+import numpy as np
+import pytest
+
+import paper_2308_03120_b200 as dm
+from paper_2308_03120_b200 import _clib, expr, kernels
+from paper_2308_03120_b200.runtime import DeviceBuffer, FlatView, KernelInvocation, build_invocation
+
+_ids = itertools.count(1)
+
+
+class FakeMatrix:
+    """Stands in for a device matrix: planning never touches memory."""
+
+    def __init__(self, rows, cols, elem="f32"):
+        self.n_rows, self.n_cols, self.elem_type = rows, cols, elem
+        bid = next(_ids)
+        self.mem = DeviceBuffer(0, bid, rows * cols, elem, 0x7f0000000000 + bid * 0x10000000)
+
+    @property
+    def n_elem(self):
+        return self.n_rows * self.n_cols
+
+    def _as_expr_node(self):
+        return expr.ExprNode("leaf", (self,), (), self.elem_type)
+
+
+def leaf(r, c, elem="f32"):
+    return FakeMatrix(r, c, elem)._as_expr_node()
+
+
+def test_config1_tree_is_one_fused_kernel():
+    A, B, C, D = (leaf(64, 64) for _ in range(4))
+    node = 2 * A + B % C - dm.exp(D)
+    p = dm.plan(node)
+    assert p.n_invocations == 1
+    assert p.steps[0].kernel == "fused_chain"
+    assert p.steps[0].params["program"] == (
+        ("load", 0), ("scalar", "eop_scalar_times", 2), ("load", 1), ("load", 2), ("glue", "eglue_schur"),
+        ("glue", "eglue_plus"), ("load", 3), ("unary", "eop_exp", None), ("glue", "eglue_minus"))
+
+
+def test_percent_and_star_are_schur():
+    A, B = leaf(3, 3), leaf(3, 3)
+    assert (A % B).kind == "eglue_schur"
+    assert (A * B).kind == "eglue_schur"
+    assert (A @ B).kind == "glue_times"
+
+
+def test_deep_chains_fuse_beyond_reference_cap():
+    node = leaf(4, 4)
+    for i in range(20):
+        node = dm.build_node("eop_scalar_plus", (node,), (i,))
+    assert dm.plan(node).n_invocations == 1
+    # reference plan shape on request (tests/test_integration.py:83-88: 8 + 8 + 4)
+    assert dm.plan(node, chain_max=kernels.REFERENCE_CHAIN_MAX).n_invocations == 3
+
+
+def test_input_limit_splits_wide_trees():
+    leaves = [leaf(8, 8) for _ in range(40)]
+    node = leaves[0]
+    for x in leaves[1:]:
+        node = node + x
+    p = dm.plan(node)
+    for s in p.steps:
+        assert len(s.inputs) <= kernels.FUSED_INPUTS_MAX
+        if s.kernel == "fused_chain":
+            assert len(s.params["program"]) <= 64
+
+
+def test_nt_gemm_has_no_transpose_pass():
+    A, B = leaf(32, 16), leaf(24, 16)
+    p = dm.plan(A @ B.t())
+    assert [s.kernel for s in p.steps] == ["gemm"]
+    assert p.steps[0].params == {"trans_a": 0, "trans_b": 1}
+    p = dm.plan(A.t() @ leaf(32, 5))
+    assert p.steps[0].params["trans_a"] == 1
+
+
+def test_gemm_with_elementwise_operands_takes_three():
+    a, b = leaf(4, 4), leaf(4, 4)
+    assert dm.plan((2 * a + 1) @ (b - 3)).n_invocations == 3
+
+
+def test_conv_over_product_stays_standalone():
+    a = leaf(4, 4)
+    p = dm.plan(dm.conv_to(a @ a, "f64"))
+    assert [s.kernel for s in p.steps] == ["gemm", "mov_copy"]
+
+
+def test_conv_of_leaf_folds_into_chain_load():
+    ints = leaf(2, 2, "i32")
+    p = dm.plan(dm.exp(dm.conv_to(ints, "f32")) + 1)
+    assert p.n_invocations == 1
+    assert p.steps[0].inputs[0][1].elem_type == "i32"
+
+
+def test_shared_leaf_loaded_once():
+    a = leaf(6, 6)
+    shared = 2 * a + 1
+    p = dm.plan((shared + shared) - shared)
+    assert len(p.steps[0].inputs) == 1
+
+
+def test_fused_reduction_plans():
+    A, B, C, D = (leaf(64, 64) for _ in range(4))
+    p = dm.plan_reduce("accu", 2 * A + B % C - dm.exp(D))
+    assert p.steps == [] and p.reduce.kernel == "fused_reduce"
+    assert len(p.reduce.inputs) == 4
+    x = leaf(100, 1)
+    p = dm.plan_reduce("dot", x, x)
+    assert len(p.reduce.inputs) == 1
+    assert p.reduce.params["program"] == (("load", 0), ("load", 0))
+    p = dm.plan_reduce("accu", leaf(3, 3) @ leaf(3, 3))
+    assert [s.kernel for s in p.steps] == ["gemm"] and p.n_invocations == 2
+
+
+def test_temp_schedule_releases_after_last_use():
+    a, b = leaf(4, 4), leaf(4, 4)
+    p = dm.plan((2 * a + 1) @ (b - 3))
+    final = p.result[1]
+    for slot, (born, dies) in p.temp_schedule.items():
+        if slot != final:
+            assert dies is not None and dies > born
+        else:
+            assert dies is None
+
+
+def test_shape_and_type_errors():
+    with pytest.raises(dm.DimensionError) as e:
+        dm.build_node("eglue_plus", (leaf(2, 3), leaf(3, 2)))
+    assert "eglue_plus" in str(e.value) and "2x3" in str(e.value) and "3x2" in str(e.value)
+    with pytest.raises(dm.DimensionError):
+        dm.build_node("glue_times", (leaf(2, 3), leaf(2, 5)))
+    with pytest.raises(dm.ElemTypeError):
+        dm.build_node("eglue_plus", (leaf(2, 2, "f32"), leaf(2, 2, "i32")))
+    with pytest.raises(ValueError):
+        dm.build_node("op_sum_dim", (leaf(2, 2),), (2,))
+
+
+def test_rewrites():
+    a = leaf(3, 4)
+    assert dm.trans(dm.trans(a)) is a
+    v = leaf(5, 1)
+    d = dm.diagmat(v)
+    assert dm.trans(d) is d
+    n = 2 * (3 * a)
+    assert n.kind == "eop_scalar_times" and n.aux[0] == 6 and n.operands[0] is a
+
+
+# ---- NVRTC compilation of emitted programs (no GPU needed) ---------------------------------------
+
+def _compile(kind, views, out, params, scalars=()):
+    inv = build_invocation(KernelInvocation(kind, tuple(views), out, scalars, params))
+    rc = _clib.lib().bm_jit_compile_only(ctypes.byref(inv))
+    assert rc == 0, _clib.last_error()
+
+
+def _flat(m, count=None, stride=1, offset=0):
+    return FlatView(m.mem, offset, m.n_elem if count is None else count, stride)
+
+
+@pytest.mark.parametrize("elem", ["f32", "f64", "i32", "u64"])
+def test_programs_compile_for_every_type(elem):
+    A, B = FakeMatrix(16, 16, elem), FakeMatrix(16, 16, elem)
+    out = FakeMatrix(16, 16, elem)
+    prog = (("load", 0), ("scalar", "eop_scalar_times", 3), ("load", 1), ("glue", "eglue_div"),
+            ("unary", "eop_abs", None), ("unary", "eop_sqrt", None), ("scalar", "eop_scalar_div_pre", 2))
+    params = {"program": prog, "compute_dtype": kernels.NP_DTYPE[elem].str}
+    _compile("fused_chain", [_flat(A), _flat(B)], _flat(out), params)
+    for op in ("accu", "min", "max"):
+        _compile("fused_reduce", [_flat(A), _flat(B)], None, dict(params, op=op))
+    dot = {"program": (("load", 0), ("load", 1)), "compute_dtype": kernels.NP_DTYPE[elem].str, "op": "dot"}
+    _compile("fused_reduce", [_flat(A), _flat(B)], None, dot)
+
+
+def test_all_unary_ops_compile():
+    A, out = FakeMatrix(8, 8), FakeMatrix(8, 8, "f64")
+    prog = [("load", 0)] + [("unary", op, 2 if op == "eop_pow" else None) for op in kernels.EOP_UNARY]
+    _compile("fused_chain", [_flat(A)], _flat(out), {"program": tuple(prog), "compute_dtype": "<f4"})
+
+
+def test_strided_and_converted_inputs_compile():
+    A, Bi, out = FakeMatrix(10, 10), FakeMatrix(10, 10, "i32"), FakeMatrix(50, 1, "u64")
+    prog = (("load", 0), ("load", 1), ("glue", "eglue_plus"))
+    _compile("fused_chain", [_flat(A, 50, 2), _flat(Bi, 50, 2, 1)], _flat(out, 50), {"program": prog,
+                                                                                      "compute_dtype": "<f4"})

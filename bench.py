@@ -326,7 +326,7 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
     # e2e through the public API with pinned host buffers
     pinned = []
     for x in host:
-        p = pinned_array(x.shape, np.float32)
+        p = pinned_array(x.shape, np.float32, order="F")
         p[...] = x
         pinned.append(p)
     e2e_steps = max(2, min(args.steps, 10))

@@ -30,6 +30,9 @@ template <> struct dtype_of<DT_F64> { typedef double T; };
 template <> struct dtype_of<DT_I32> { typedef int T; };
 template <> struct dtype_of<DT_U64> { typedef unsigned long long T; };
 
+template <bool C, typename A, typename B> struct cond_t { typedef A type; };
+template <typename A, typename B> struct cond_t<false, A, B> { typedef B type; };
+
 template <typename T> struct is_float_t { static const bool value = false; };
 template <> struct is_float_t<float> { static const bool value = true; };
 template <> struct is_float_t<double> { static const bool value = true; };

@@ -64,9 +64,98 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(int ta, int tb, i64 m, i
         }
 }
 
+// ---------------------------------------------------------------------------
+// matrix-vector products (the two GEMMs of the logistic step, SURVEY 8d
+// config 5, are X*w and X^T*r): HBM-bound, so no tensor cores; f64
+// accumulation for float types, fixed summation order (deterministic).
+
+// y[i] = sum_l A[i + l*lda] x[l]  (A column-major m x k, rows contiguous)
+template <typename T>
+__global__ void __launch_bounds__(256) gemv_n_kernel(const T* __restrict__ A, i64 lda, const T* __restrict__ x,
+                                                     i64 incx, T* __restrict__ y, i64 incy, i64 m, i64 k) {
+    typedef typename DotAcc<T>::type Acc;
+    const i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    Acc acc = 0;
+    i64 l = 0;
+    for (; l + 4 <= k; l += 4) {
+        const T a0 = A[i + (l + 0) * lda], a1 = A[i + (l + 1) * lda], a2 = A[i + (l + 2) * lda],
+                a3 = A[i + (l + 3) * lda];
+        acc = OpPlus::f(acc, OpTimes::f((Acc)a0, (Acc)x[(l + 0) * incx]));
+        acc = OpPlus::f(acc, OpTimes::f((Acc)a1, (Acc)x[(l + 1) * incx]));
+        acc = OpPlus::f(acc, OpTimes::f((Acc)a2, (Acc)x[(l + 2) * incx]));
+        acc = OpPlus::f(acc, OpTimes::f((Acc)a3, (Acc)x[(l + 3) * incx]));
+    }
+    for (; l < k; ++l) acc = OpPlus::f(acc, OpTimes::f((Acc)A[i + l * lda], (Acc)x[l * incx]));
+    y[i * incy] = cvt<T>(acc);
+}
+
+// partial[s][i] = sum over the s-th K slice of A[l + i*lda] x[l] (columns contiguous)
+template <typename T>
+__global__ void __launch_bounds__(256) gemv_t_partial_kernel(const T* __restrict__ A, i64 lda,
+                                                             const T* __restrict__ x, i64 incx,
+                                                             typename DotAcc<T>::type* __restrict__ part, i64 m,
+                                                             i64 k, i64 slice) {
+    typedef typename DotAcc<T>::type Acc;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const i64 i = (i64)blockIdx.x * (blockDim.x >> 5) + warp;
+    if (i >= m) return;
+    const i64 l0 = (i64)blockIdx.y * slice;
+    i64 l1 = l0 + slice;
+    if (l1 > k) l1 = k;
+    const T* col = A + i * lda;
+    Acc acc = 0;
+    for (i64 l = l0 + lane; l < l1; l += 32) acc = OpPlus::f(acc, OpTimes::f((Acc)col[l], (Acc)x[l * incx]));
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) acc = OpPlus::f(acc, warp_shfl_xor(acc, o));
+    if (lane == 0) part[(i64)blockIdx.y * m + i] = acc;
+}
+
+template <typename T>
+__global__ void gemv_t_finish_kernel(const typename DotAcc<T>::type* __restrict__ part, int nsplit, T* __restrict__ y,
+                                     i64 incy, i64 m) {
+    typedef typename DotAcc<T>::type Acc;
+    const i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    Acc acc = 0;
+    for (int s = 0; s < nsplit; ++s) acc = OpPlus::f(acc, part[(i64)s * m + i]);
+    y[i * incy] = cvt<T>(acc);
+}
+
 }  // namespace bm
 
 namespace bmi {
+
+// y = op(A) x, op(A) m x k; A column-major with leading dim lda.
+template <typename T>
+static int gemv(bool ta, int64_t m, int64_t k, const T* A, int64_t lda, const T* x, int64_t incx, T* y,
+                int64_t incy) {
+    typedef typename bm::DotAcc<T>::type Acc;
+    cudaStream_t s = st().stream;
+    if (!ta) {
+        bm::gemv_n_kernel<T><<<(unsigned)((m + 255) / 256), 256, 0, s>>>(A, lda, x, incx, y, incy, m, k);
+        BM_CUDA(cudaGetLastError());
+        st().launches++;
+        return BM_OK;
+    }
+    // op(A)(i, l) = A[l + i*lda]: one warp per output, K split for parallelism
+    int nsplit = 1;
+    while (nsplit < 64 && m * nsplit < 4LL * 148 * 8 * 4 && k / (nsplit * 2) >= 4096) nsplit *= 2;
+    const int64_t slice = (k + nsplit - 1) / nsplit;
+    Acc* part = nullptr;
+    BM_CUDA(cudaMallocAsync((void**)&part, (size_t)(nsplit * m) * sizeof(Acc), s));
+    dim3 grid((unsigned)((m + 7) / 8), (unsigned)nsplit);
+    bm::gemv_t_partial_kernel<T><<<grid, 256, 0, s>>>(A, lda, x, incx, part, m, k, slice);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) {
+        bm::gemv_t_finish_kernel<T><<<(unsigned)((m + 255) / 256), 256, 0, s>>>(part, nsplit, y, incy, m);
+        e = cudaGetLastError();
+    }
+    cudaFreeAsync(part, s);
+    if (e != cudaSuccess) return cuda_fail(e, "gemv");
+    st().launches += 2;
+    return BM_OK;
+}
 
 int gemm_tc_f32(int ta, int tb, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const float* B,
                 int64_t ldb, float* C, int64_t ldc, bool* handled);
@@ -108,6 +197,20 @@ int launch_gemm(const bm_invocation* inv) {
         return BM_OK;
     }
     const int algo = st().gemm_algo;
+    if (algo != 2 && (a.dtype == BM_F32 || a.dtype == BM_F64) && (n == 1 || m == 1)) {
+        // matrix-vector product: C = op(A) x  (n == 1)  or  C^T = op(B)^T a^T  (m == 1)
+        if (n == 1) {
+            const int64_t incx = tb ? b.lda : 1;
+            if (a.dtype == BM_F32)
+                return gemv<float>(ta != 0, m, k, (const float*)A, a.lda, (const float*)B, incx, (float*)C, 1);
+            return gemv<double>(ta != 0, m, k, (const double*)A, a.lda, (const double*)B, incx, (double*)C, 1);
+        }
+        // m == 1: C(0, j) = sum_l a(l) op(B)(l, j); op(B)^T is n x k: stored B (k x n) => transposed access
+        const int64_t incx = ta ? 1 : a.lda;
+        if (a.dtype == BM_F32)
+            return gemv<float>(tb == 0, n, k, (const float*)B, b.lda, (const float*)A, incx, (float*)C, c.lda);
+        return gemv<double>(tb == 0, n, k, (const double*)B, b.lda, (const double*)A, incx, (double*)C, c.lda);
+    }
     switch (a.dtype) {
         case BM_F32: {
             if (algo != 2) {

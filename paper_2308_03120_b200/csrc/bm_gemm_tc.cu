@@ -1,14 +1,402 @@
-// bm_gemm_tc.cu -- tensor-core GEMMs (placeholder: filled in next milestone)
+// bm_gemm_tc.cu -- tensor-core GEMMs for glue_times (reference kernels.py:704-708).
+//
+// f32: 3xTF32 on the 5th-generation tensor cores.  A pre-pass splits each
+// operand into tf32 hi = rna(x) and lo = rna(x - hi) and lays both out K-major
+// (the transpose of a column-major A or of B^T is folded into this pass, so
+// `A @ B.t()` never materialises a transposed matrix).  The GEMM kernel
+// streams 128x16 / 256x16 hi/lo tiles with TMA (SWIZZLE_64B) through a 4-stage
+// mbarrier pipeline; one elected thread issues tcgen05.mma kind::tf32
+// (lo*hi + hi*lo + hi*hi per k-step) into 128x256 f32 accumulators in TMEM;
+// eight epilogue warps drain TMEM with tcgen05.ld and store column-major C.
+// The dropped lo*lo term and the tf32 rounding of lo leave ~2^-22 relative
+// error per product; the accumulation is promoted to round-to-nearest f32
+// every 64 K (see below), so the result tracks an SGEMM.
+//
+// f64: DMMA (mma.sync.aligned.m8n8k4 f64) with cp.async double buffering.
+#include <cstring>
+
 #include "bm_internal.h"
+#include "bm_ptx.cuh"
+#include "bm_reduce.cuh"
+
+namespace bm {
+
+// ---------------------------------------------------------------------------
+// 3xTF32 split pre-pass: out[r * kp + c] for r < rp (M or N), c < kp (K)
+
+__device__ __forceinline__ float tf32_rna(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+// src_kmajor: op(src)(r, c) = src[c + r*ld]; otherwise src[r + c*ld]
+template <bool SRC_KMAJOR>
+__global__ void __launch_bounds__(256) split_tf32_kernel(const float* __restrict__ src, i64 ld, i64 rows, i64 k,
+                                                         float* __restrict__ hi, float* __restrict__ lo, i64 kp,
+                                                         i64 rp) {
+    __shared__ float tile[32][33];
+    const i64 r0 = (i64)blockIdx.y * 32, c0 = (i64)blockIdx.x * 32;
+    if (SRC_KMAJOR) {
+        for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+            const i64 r = r0 + j, c = c0 + threadIdx.x;
+            float v = 0.f;
+            if (r < rows && c < k) v = src[c + r * ld];
+            tile[j][threadIdx.x] = v;
+        }
+    } else {
+        // read with threadIdx.x along r (contiguous), park transposed
+        for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+            const i64 r = r0 + threadIdx.x, c = c0 + j;
+            float v = 0.f;
+            if (r < rows && c < k) v = src[r + c * ld];
+            tile[threadIdx.x][j] = v;
+        }
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        const i64 r = r0 + j, c = c0 + threadIdx.x;
+        if (r < rp && c < kp) {
+            const float x = tile[j][threadIdx.x];
+            const float h = tf32_rna(x);
+            hi[r * kp + c] = h;
+            lo[r * kp + c] = tf32_rna(x - h);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// tcgen05 kernel.
+//
+// Tile 128 x 256 x 16 (K-major SWIZZLE_64B operands), 4-stage TMA ring,
+// one elected thread issuing tcgen05.mma kind::tf32 into TMEM.  The tensor
+// core adds its K=8 products into the f32 accumulator with truncation, so a
+// long K chain drifts (max-normalised error ~1e-5 at K = 1024, 15x the
+// reference's OpenBLAS SGEMM).  The accumulator is therefore promoted every
+// 64 K: two TMEM buffers ping-pong, and eight epilogue warps add each finished
+// 128x256 chunk into round-to-nearest f32 registers while the MMAs run on
+// the other buffer (the same remedy DeepGEMM applies to FP8).
+
+#define TC_BM 128
+#define TC_BN 256
+#define TC_BK 16
+#define TC_STAGES 4
+#define TC_CHUNK_KB 4                      // K blocks per promoted chunk (64 K)
+#define TC_TILE_A (TC_BM * TC_BK * 4)
+#define TC_TILE_B (TC_BN * TC_BK * 4)
+#define TC_STAGE_BYTES (2 * TC_TILE_A + 2 * TC_TILE_B)
+#define TC_SMEM (TC_STAGES * TC_STAGE_BYTES + 1024 + 256)
+#define TC_THREADS 320                     // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
+
+// K-major operand, SWIZZLE_64B canonical layout: 8-row x 64-B atoms, atoms
+// 512 B apart along M/N (SBO); version 1 (sm_100); K offset via start address.
+__device__ __forceinline__ uint64_t sw64_kmajor_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
+    d |= (uint64_t)(16u >> 4) << 16;
+    d |= (uint64_t)(512u >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)4 << 61;
+    return d;
+}
+
+__host__ __device__ constexpr uint32_t tf32_idesc(int m, int n) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
+                       const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_blo,
+                       float* __restrict__ C, i64 m, i64 n, i64 ldc, int nk) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + TC_STAGES * TC_STAGE_BYTES);
+    uint64_t* empty = full + TC_STAGES;
+    uint64_t* acc_full = empty + TC_STAGES;   // [2]
+    uint64_t* acc_empty = acc_full + 2;       // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m0 = blockIdx.y * TC_BM, n0 = blockIdx.x * TC_BN;
+    const int nchunks = (nk + TC_CHUNK_KB - 1) / TC_CHUNK_KB;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < TC_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&acc_full[b], 1);
+            mbar_init(&acc_empty[b], 8);
+        }
+        mbar_fence_init();
+        tma_prefetch_desc(&tm_ahi);
+        tma_prefetch_desc(&tm_alo);
+        tma_prefetch_desc(&tm_bhi);
+        tma_prefetch_desc(&tm_blo);
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, 2 * TC_BN);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    auto tile_ahi = [&](int s) { return smem + s * TC_STAGE_BYTES; };
+    auto tile_alo = [&](int s) { return smem + s * TC_STAGE_BYTES + TC_TILE_A; };
+    auto tile_bhi = [&](int s) { return smem + s * TC_STAGE_BYTES + 2 * TC_TILE_A; };
+    auto tile_blo = [&](int s) { return smem + s * TC_STAGE_BYTES + 2 * TC_TILE_A + TC_TILE_B; };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int kb = 0; kb < nk; ++kb) {
+                const int s = kb % TC_STAGES;
+                if (kb >= TC_STAGES) mbar_wait(&empty[s], (uint32_t)(((kb / TC_STAGES) - 1) & 1));
+                mbar_expect_tx(&full[s], TC_STAGE_BYTES);
+                const int kc = kb * TC_BK;
+                tma_load_2d(tile_ahi(s), &tm_ahi, kc, m0, &full[s]);
+                tma_load_2d(tile_alo(s), &tm_alo, kc, m0, &full[s]);
+                tma_load_2d(tile_bhi(s), &tm_bhi, kc, n0, &full[s]);
+                tma_load_2d(tile_blo(s), &tm_blo, kc, n0, &full[s]);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = tf32_idesc(TC_BM, TC_BN);
+            for (int c = 0; c < nchunks; ++c) {
+                const int b = c & 1;
+                if (c >= 2) mbar_wait(&acc_empty[b], (uint32_t)(((c >> 1) - 1) & 1));
+                tc_fence_after();
+                const uint32_t d = tmem + (uint32_t)(b * TC_BN);
+                const int kb_end = (c + 1) * TC_CHUNK_KB < nk ? (c + 1) * TC_CHUNK_KB : nk;
+                for (int kb = c * TC_CHUNK_KB; kb < kb_end; ++kb) {
+                    const int s = kb % TC_STAGES;
+                    mbar_wait(&full[s], (uint32_t)((kb / TC_STAGES) & 1));
+                    tc_fence_after();
+                    const uint64_t ahi = sw64_kmajor_desc(smem_u32(tile_ahi(s)));
+                    const uint64_t alo = sw64_kmajor_desc(smem_u32(tile_alo(s)));
+                    const uint64_t bhi = sw64_kmajor_desc(smem_u32(tile_bhi(s)));
+                    const uint64_t blo = sw64_kmajor_desc(smem_u32(tile_blo(s)));
+#pragma unroll
+                    for (int kk = 0; kk < TC_BK / 8; ++kk) {
+                        const uint64_t adv = (uint64_t)((kk * 32) >> 4);   // 8 tf32 = 32 B along K
+                        const uint32_t first = (kb == c * TC_CHUNK_KB && kk == 0) ? 0u : 1u;
+                        mma_tf32(d, alo + adv, bhi + adv, idesc, first);
+                        mma_tf32(d, ahi + adv, blo + adv, idesc, 1u);
+                        mma_tf32(d, ahi + adv, bhi + adv, idesc, 1u);
+                    }
+                    mma_commit(&empty[s]);
+                }
+                mma_commit(&acc_full[b]);
+            }
+        }
+    } else {
+        // epilogue warps 2..9: TMEM lane quarter q = warp % 4, column half h
+        const int q = warp & 3;
+        const int h = (warp - 2) >> 2;
+        float acc[128];
+#pragma unroll
+        for (int i = 0; i < 128; ++i) acc[i] = 0.f;
+        for (int c = 0; c < nchunks; ++c) {
+            const int b = c & 1;
+            mbar_wait(&acc_full[b], (uint32_t)((c >> 1) & 1));
+            tc_fence_after();
+            const uint32_t base = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(b * TC_BN + h * 128);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                uint32_t v[32];
+                tmem_ld_32x32b_x32(base + (uint32_t)(j * 32), v);
+                tmem_ld_wait();
+#pragma unroll
+                for (int t = 0; t < 32; ++t) acc[j * 32 + t] += __uint_as_float(v[t]);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[b]);
+        }
+        const i64 row = (i64)m0 + 32 * q + lane;
+        if (row < m) {
+#pragma unroll
+            for (int t = 0; t < 128; ++t) {
+                const i64 col = (i64)n0 + h * 128 + t;
+                if (col < n) C[row + col * ldc] = acc[t];
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem, 2 * TC_BN);
+}
+
+// ---------------------------------------------------------------------------
+// f64: DMMA m8n8k4.  CTA tile 64x64, 4 warps of 32x32 (4x4 DMMA tiles each),
+// K staged 16 at a time through double-buffered shared memory (cp.async).
+
+__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(c[0]), "+d"(c[1])
+                 : "d"(a), "d"(b));
+}
+
+#define DM_BM 64
+#define DM_BN 64
+#define DM_BK 16
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(128) gemm_dmma_kernel(const double* __restrict__ A, i64 lda,
+                                                        const double* __restrict__ B, i64 ldb, double* __restrict__ C,
+                                                        i64 ldc, i64 m, i64 n, i64 k) {
+    // As[k][m], Bs[k][n] (+1 padding)
+    __shared__ double As[2][DM_BK][DM_BM + 1];
+    __shared__ double Bs[2][DM_BK][DM_BN + 1];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gid = lane >> 2, tig = lane & 3;
+    const i64 m0 = (i64)blockIdx.y * DM_BM, n0 = (i64)blockIdx.x * DM_BN;
+    const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    auto load = [&](int buf, i64 k0) {
+        for (int idx = threadIdx.x; idx < DM_BK * DM_BM; idx += 128) {
+            int kk, mm;
+            if (TA) { mm = idx / DM_BK; kk = idx % DM_BK; } else { kk = idx / DM_BM; mm = idx % DM_BM; }
+            const i64 gi = m0 + mm, gl = k0 + kk;
+            double v = 0.0;
+            if (gi < m && gl < k) v = TA ? A[gl + gi * lda] : A[gi + gl * lda];
+            As[buf][kk][mm] = v;
+        }
+        for (int idx = threadIdx.x; idx < DM_BK * DM_BN; idx += 128) {
+            int kk, nn;
+            if (TB) { kk = idx / DM_BN; nn = idx % DM_BN; } else { nn = idx / DM_BK; kk = idx % DM_BK; }
+            const i64 gj = n0 + nn, gl = k0 + kk;
+            double v = 0.0;
+            if (gj < n && gl < k) v = TB ? B[gj + gl * ldb] : B[gl + gj * ldb];
+            Bs[buf][kk][nn] = v;
+        }
+    };
+    load(0, 0);
+    __syncthreads();
+    int buf = 0;
+    for (i64 k0 = 0; k0 < k; k0 += DM_BK) {
+        if (k0 + DM_BK < k) load(buf ^ 1, k0 + DM_BK);
+#pragma unroll
+        for (int ks = 0; ks < DM_BK; ks += 4) {
+            double af[4], bf[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) af[i] = As[buf][ks + tig][wm + 8 * i + gid];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bf[j] = Bs[buf][ks + tig][wn + 8 * j + gid];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j], af[i], bf[j]);
+        }
+        __syncthreads();
+        buf ^= 1;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+                const i64 r = m0 + wm + 8 * i + gid, c = n0 + wn + 8 * j + 2 * tig + t;
+                if (r < m && c < n) C[r + c * ldc] = acc[i][j][t];
+            }
+}
+
+}  // namespace bm
+
 namespace bmi {
-int gemm_tc_f32(int, int, int64_t, int64_t, int64_t, const float*, int64_t, const float*, int64_t, float*, int64_t,
-                bool* handled) {
-    *handled = false;
+
+static int encode_kmajor(CUtensorMap* tm, const float* p, int64_t kp, int64_t rows_p, int box_rows) {
+    const cuuint64_t gdim[2] = {(cuuint64_t)kp, (cuuint64_t)rows_p};
+    const cuuint64_t gstride[1] = {(cuuint64_t)(kp * 4)};
+    const cuuint32_t box[2] = {TC_BK, (cuuint32_t)box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = drv().tensorMapEncodeTiled(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)p, gdim, gstride, box, estr,
+                                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cu_fail(r, "cuTensorMapEncodeTiled (gemm operand)");
     return BM_OK;
 }
-int gemm_dmma_f64(int, int, int64_t, int64_t, int64_t, const double*, int64_t, const double*, int64_t, double*,
-                  int64_t, bool* handled) {
-    *handled = false;
+
+static int split_operand(const float* src, int64_t ld, bool kmajor, int64_t rows, int64_t k, float* hi, float* lo,
+                         int64_t kp, int64_t rp) {
+    dim3 grid((unsigned)(kp / 32), (unsigned)(rp / 32));
+    if (kmajor)
+        bm::split_tf32_kernel<true><<<grid, dim3(32, 8), 0, st().stream>>>(src, ld, rows, k, hi, lo, kp, rp);
+    else
+        bm::split_tf32_kernel<false><<<grid, dim3(32, 8), 0, st().stream>>>(src, ld, rows, k, hi, lo, kp, rp);
+    BM_CUDA(cudaGetLastError());
+    st().launches++;
     return BM_OK;
 }
+
+int gemm_tc_f32(int ta, int tb, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const float* B,
+                int64_t ldb, float* C, int64_t ldc, bool* handled) {
+    *handled = false;
+    if (m * n * k < (int64_t)1 << 21) return BM_OK;   // tiny: the SIMT kernel is cheaper than the split pass
+    const int64_t mp = (m + TC_BM - 1) / TC_BM * TC_BM;
+    const int64_t np = (n + TC_BN - 1) / TC_BN * TC_BN;
+    const int64_t kp = (k + 31) / 32 * 32;   // split kernel tiles K by 32
+    if (mp / TC_BM > 65535 || np / TC_BN > (1LL << 31) - 1) return BM_OK;
+    cudaStream_t s = st().stream;
+    float* buf = nullptr;
+    const int64_t a_elems = mp * kp, b_elems = np * kp;
+    BM_CUDA(cudaMallocAsync((void**)&buf, (size_t)(2 * (a_elems + b_elems) * 4), s));
+    float *ahi = buf, *alo = buf + a_elems, *bhi = buf + 2 * a_elems, *blo = buf + 2 * a_elems + b_elems;
+    // op(A) is m x k; K-major iff A is stored transposed.  op(B) is k x n and we
+    // need its N x K K-major form: K-major iff B is NOT transposed.
+    int rc = split_operand(A, lda, ta != 0, m, k, ahi, alo, kp, mp);
+    if (!rc) rc = split_operand(B, ldb, tb == 0, n, k, bhi, blo, kp, np);
+    CUtensorMap tm[4];
+    if (!rc) rc = encode_kmajor(&tm[0], ahi, kp, mp, TC_BM);
+    if (!rc) rc = encode_kmajor(&tm[1], alo, kp, mp, TC_BM);
+    if (!rc) rc = encode_kmajor(&tm[2], bhi, kp, np, TC_BN);
+    if (!rc) rc = encode_kmajor(&tm[3], blo, kp, np, TC_BN);
+    if (!rc) {
+        static bool attr = false;
+        if (!attr) {
+            cudaError_t e = cudaFuncSetAttribute(bm::gemm_3xtf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 TC_SMEM);
+            if (e != cudaSuccess) rc = cuda_fail(e, "cudaFuncSetAttribute (3xTF32)");
+            attr = true;
+        }
+    }
+    if (!rc) {
+        dim3 grid((unsigned)(np / TC_BN), (unsigned)(mp / TC_BM));
+        bm::gemm_3xtf32_kernel<<<grid, TC_THREADS, TC_SMEM, s>>>(tm[0], tm[1], tm[2], tm[3], C, m, n, ldc, (int)(kp / TC_BK));
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) rc = cuda_fail(e, "3xTF32 GEMM launch");
+        else st().launches++;
+    }
+    cudaFreeAsync(buf, s);
+    if (!rc) *handled = true;
+    return rc;
+}
+
+int gemm_dmma_f64(int ta, int tb, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B,
+                  int64_t ldb, double* C, int64_t ldc, bool* handled) {
+    *handled = false;
+    if (m * n * k < (int64_t)1 << 18) return BM_OK;
+    dim3 grid((unsigned)((n + DM_BN - 1) / DM_BN), (unsigned)((m + DM_BM - 1) / DM_BM));
+    if (grid.y > 65535) return BM_OK;
+    cudaStream_t s = st().stream;
+    if (ta) {
+        if (tb) bm::gemm_dmma_kernel<true, true><<<grid, 128, 0, s>>>(A, lda, B, ldb, C, ldc, m, n, k);
+        else bm::gemm_dmma_kernel<true, false><<<grid, 128, 0, s>>>(A, lda, B, ldb, C, ldc, m, n, k);
+    } else {
+        if (tb) bm::gemm_dmma_kernel<false, true><<<grid, 128, 0, s>>>(A, lda, B, ldb, C, ldc, m, n, k);
+        else bm::gemm_dmma_kernel<false, false><<<grid, 128, 0, s>>>(A, lda, B, ldb, C, ldc, m, n, k);
+    }
+    BM_CUDA(cudaGetLastError());
+    st().launches++;
+    *handled = true;
+    return BM_OK;
+}
+
 }  // namespace bmi

@@ -25,10 +25,11 @@ namespace bm {
 #define BM_REDUCE_BLOCK 8192
 #define BM_TILE_PITCH 544
 #define BM_TILE_BYTES (16 * BM_TILE_PITCH)
-#define BM_RWARPS 8
-#define BM_MAX_GROUP 256                 // blocks per CTA
-#define BM_MAX_FINAL 4096                // CTA partials folded by the last CTA
-#define BM_REDUCE_SMEM (BM_RWARPS * BM_TILE_BYTES + 2 * BM_MAX_GROUP * 8)
+#define BM_RWARPS 16                     // default warps per (persistent) reduction CTA
+#define BM_REDUCE_SMEM (BM_RWARPS * BM_TILE_BYTES)
+#ifndef BM_UNIT_UNROLL
+#define BM_UNIT_UNROLL 4                 // rows of a pairwise unit loaded per batch
+#endif
 
 struct Args {
     const void* in[BM_MAXIN];   // element 0 of every input view
@@ -41,8 +42,8 @@ struct Args {
     void* partials;             // per-CTA partials scratch
     unsigned int* ticket;       // last-CTA-done counter (reset by the last CTA)
     void* result;               // device slot for the final value
-    i64 blocks;                 // number of REDUCE_BLOCK blocks
-    int group;                  // blocks per CTA (power of two, multiple of BM_RWARPS or == blocks)
+    i64 blocks;                 // number of REDUCE_BLOCK blocks (informational)
+    int group;                  // reductions: 1 = unit mode, 0 = block mode
     int vec_ok;                 // all views contiguous and 16-B aligned
 };
 
@@ -137,21 +138,27 @@ __device__ __forceinline__ void ewise_store(const Args& a) {
 // numpy pairwise summation
 
 // one warp-cooperative unit: 16 rows x (32 lanes x 16 B)
-template <typename T, class S>
-__device__ __forceinline__ T pw_unit(const S& s, i64 off, char* tile, bool vec_ok) {
+template <typename T, bool VEC, class S>
+__device__ __forceinline__ T pw_unit(const S& s, i64 off, char* tile) {
     constexpr int V = 16 / sizeof(T);
     constexpr int W = 32 * V;
     const int lane = threadIdx.x & 31;
-#pragma unroll 4
-    for (int r = 0; r < 16; ++r) {
-        T v[V];
-        if (vec_ok) {
-            s.template vec<V>(off + r * W + lane * V, v);
-        } else {
+    constexpr int UNR = BM_UNIT_UNROLL;
+    for (int r0 = 0; r0 < 16; r0 += UNR) {
+        T v[UNR][V];
 #pragma unroll
-            for (int k = 0; k < V; ++k) v[k] = s.at(off + r * W + lane * V + k);
+        for (int u = 0; u < UNR; ++u) {
+            const int r = r0 + u;
+            if constexpr (VEC) {
+                s.template vec<V>(off + r * W + lane * V, v[u]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < V; ++k) v[u][k] = s.at(off + r * W + lane * V + k);
+            }
         }
-        *reinterpret_cast<uint4*>(tile + r * BM_TILE_PITCH + lane * 16) = *reinterpret_cast<const uint4*>(v);
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+            *reinterpret_cast<uint4*>(tile + (r0 + u) * BM_TILE_PITCH + lane * 16) = *reinterpret_cast<const uint4*>(v[u]);
     }
     __syncwarp();
     T res;
@@ -209,7 +216,7 @@ __device__ T pw_balanced(const S& s, i64 off, i64 count, char* tile, bool vec_ok
     int lvl[24];
     int sp = 0;
     for (i64 u = 0; u < count; ++u) {
-        T v = pw_unit<T>(s, off + u * U, tile, vec_ok);
+        T v = vec_ok ? pw_unit<T, true>(s, off + u * U, tile) : pw_unit<T, false>(s, off + u * U, tile);
         int l = 0;
         while (sp > 0 && lvl[sp - 1] == l) { v = stk[sp - 1] + v; --sp; ++l; }
         stk[sp] = v; lvl[sp] = l; ++sp;
@@ -316,12 +323,16 @@ __device__ __forceinline__ T block_minmax(const S& s, i64 off, i64 len, bool vec
     constexpr int V = 16 / sizeof(T);
     const int lane = threadIdx.x & 31;
     T acc = s.at(off);  // len >= 1
-    if (vec_ok && len == BM_REDUCE_BLOCK) {
-        for (i64 i = lane * V; i < len; i += 32 * V) {
-            T v[V];
-            s.template vec<V>(off + i, v);
+    if (vec_ok && len % (4 * 32 * V) == 0) {
+        for (i64 i = lane * V; i < len; i += 4 * 32 * V) {
+            T v[4][V];
 #pragma unroll
-            for (int k = 0; k < V; ++k) acc = IS_MAX ? np_max(acc, v[k]) : np_min(acc, v[k]);
+            for (int u = 0; u < 4; ++u) s.template vec<V>(off + i + u * 32 * V, v[u]);
+            asm volatile("" ::: "memory");   // keep the four loads in flight together
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int k = 0; k < V; ++k) acc = IS_MAX ? np_max(acc, v[u][k]) : np_min(acc, v[u][k]);
         }
     } else {
         for (i64 i = lane; i < len; i += 32) {
@@ -349,13 +360,22 @@ __device__ __forceinline__ typename DotAcc<T>::type block_dot(const S2& s, i64 o
     constexpr int V = 16 / sizeof(T);
     const int lane = threadIdx.x & 31;
     A acc = 0;
-    if (vec_ok && len == BM_REDUCE_BLOCK) {
-        for (i64 i = lane * V; i < len; i += 32 * V) {
-            T x[V], y[V];
-            s.template vec2<V>(off + i, x, y);
+    if (vec_ok && len % (4 * 32 * V) == 0) {
+        A acc2 = 0;
+        for (i64 i = lane * V; i < len; i += 4 * 32 * V) {
+            T x[4][V], y[4][V];
 #pragma unroll
-            for (int k = 0; k < V; ++k) acc = OpPlus::f(acc, OpTimes::f((A)x[k], (A)y[k]));
+            for (int u = 0; u < 4; ++u) s.template vec2<V>(off + i + u * 32 * V, x[u], y[u]);
+            asm volatile("" ::: "memory");   // keep the eight loads in flight together
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int k = 0; k < V; ++k) {
+                    if (u & 1) acc2 = OpPlus::f(acc2, OpTimes::f((A)x[u][k], (A)y[u][k]));
+                    else acc = OpPlus::f(acc, OpTimes::f((A)x[u][k], (A)y[u][k]));
+                }
         }
+        acc = OpPlus::f(acc, acc2);
     } else {
         for (i64 i = lane; i < len; i += 32) {
             T x, y;
@@ -394,78 +414,142 @@ __device__ A cta_combine_pairwise(A* v, A* w, int cnt) {
 }
 
 // ---------------------------------------------------------------------------
-// flat reduction kernel body.  CTA c owns blocks [c*group, (c+1)*group); its
-// warps take blocks round-robin; block partials are folded inside the CTA
-// with combine_pairwise, CTA partials by the last CTA to finish.  Because a
-// CTA's range is an aligned power-of-two run of blocks, this equals one
-// combine_pairwise over all blocks ("reduction order").
+// flat reduction kernel body.
+//
+// Work items are either the 2048/1024-element pairwise units of every full
+// REDUCE_BLOCK block ("unit mode", used when there are few blocks per SM, so
+// the work balances across all 148 SMs) or whole blocks ("block mode"); the
+// ragged tail block is one extra item.  Items are dealt to CTAs round-robin
+// (one persistent CTA per SM), every item writes one partial to global
+// scratch, and the last CTA to finish folds them: units -> block partials
+// with numpy's balanced tree, then blocks with combine_pairwise -- streamed by
+// each thread over an aligned power-of-two run of blocks with a binary-counter
+// stack (identical to combine_pairwise's level order), then across threads.
+// No float atomics: the result is the reference's bits.
+
+template <typename A, int OP>
+struct Fold {
+    // combine of two block partials (combine_pairwise op, kernels.py:779-798)
+    __device__ static __forceinline__ A blocks(A a, A b) { return combine_op<A, OP>(a, b); }
+    // combine of two unit partials inside one block (numpy's tree / ndarray.min)
+    __device__ static __forceinline__ A units(A a, A b) {
+        if (OP == 2) return np_min(a, b);
+        if (OP == 3) return np_max(a, b);
+        return OpPlus::f(a, b);
+    }
+};
+
+// combine_pairwise over `count` values produced by get(i), streamed with a
+// binary-counter stack; equals the reference's level-by-level fold.
+template <typename A, int OP, class G>
+__device__ __forceinline__ A stream_pairwise(i64 count, const G& get) {
+    A stk[40];
+    int lvl[40];
+    int sp = 0;
+    for (i64 i = 0; i < count; ++i) {
+        A v = get(i);
+        int l = 0;
+        while (sp > 0 && lvl[sp - 1] == l) { v = Fold<A, OP>::blocks(stk[sp - 1], v); --sp; ++l; }
+        stk[sp] = v; lvl[sp] = l; ++sp;
+    }
+    A v = stk[sp - 1];
+    for (int k = sp - 2; k >= 0; --k) v = Fold<A, OP>::blocks(stk[k], v);
+    return v;
+}
+
+template <typename T, int OP, class S>
+__device__ __forceinline__ void reduce_item_store(const Args& a, const S& s, i64 item, i64 off, i64 len, char* tile,
+                                                  bool vec_ok, bool unit) {
+    typedef typename DotAcc<T>::type DA;
+    const int lane = threadIdx.x & 31;
+    if constexpr (OP == 4) {
+        const DA v = block_dot<T>(s, off, len, vec_ok);
+        if (lane == 0) reinterpret_cast<DA*>(a.partials)[item] = v;
+    } else if constexpr (OP == 2 || OP == 3) {
+        const T v = block_minmax<T, OP == 3>(s, off, len, vec_ok);
+        if (lane == 0) reinterpret_cast<T*>(a.partials)[item] = v;
+    } else {
+        T v;
+        if constexpr (is_float_t<T>::value) {
+            if (unit) v = vec_ok ? pw_unit<T, true>(s, off, tile) : pw_unit<T, false>(s, off, tile);
+            else v = block_accu<T>(s, off, len, tile, vec_ok);
+        } else {
+            v = block_accu<T>(s, off, len, tile, vec_ok);
+        }
+        if (lane == 0) reinterpret_cast<T*>(a.partials)[item] = v;
+    }
+}
+
 template <typename T, int OP, class S>
 __device__ void reduce_flat(const Args& a, const S& s) {
     typedef typename DotAcc<T>::type DA;
+    typedef typename cond_t<OP == 4, DA, T>::type P;   // partial type
     extern __shared__ __align__(16) char smem[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nw = blockDim.x >> 5;
+    const int warp = threadIdx.x >> 5;
     char* tile = smem + warp * BM_TILE_BYTES;
-    // partial slots (room for double)
-    double* slots_d = reinterpret_cast<double*>(smem + BM_RWARPS * BM_TILE_BYTES);
-    const i64 b0 = (i64)blockIdx.x * a.group;
-    i64 b1 = b0 + a.group;
-    if (b1 > a.blocks) b1 = a.blocks;
-    const int cnt = (int)(b1 - b0);
     const bool vec_ok = a.vec_ok != 0;
-    for (i64 b = b0 + warp; b < b1; b += BM_RWARPS) {
-        const i64 off = b * BM_REDUCE_BLOCK;
-        i64 len = a.n - off;
-        if (len > BM_REDUCE_BLOCK) len = BM_REDUCE_BLOCK;
-        if constexpr (OP == 1) {
-            const T v = block_accu<T>(s, off, len, tile, vec_ok);
-            if (lane == 0) reinterpret_cast<T*>(slots_d)[b - b0] = v;
-        } else if constexpr (OP == 2 || OP == 3) {
-            const T v = block_minmax<T, OP == 3>(s, off, len, vec_ok);
-            if (lane == 0) reinterpret_cast<T*>(slots_d)[b - b0] = v;
+    const bool unit_mode = a.group != 0;          // group != 0: unit mode
+    constexpr i64 UE = PwUnit<T>::value;          // elements per unit
+    constexpr int UPB = BM_REDUCE_BLOCK / UE;     // units per block
+    const i64 nfull = a.n / BM_REDUCE_BLOCK;      // full blocks
+    const i64 tail = a.n - nfull * BM_REDUCE_BLOCK;
+    const i64 nitems_full = unit_mode ? nfull * UPB : nfull;
+    const i64 nitems = nitems_full + (tail ? 1 : 0);
+    // CTA c owns the contiguous item range [c*q + min(c, r), ...) (q, r: quotient
+    // and remainder of nitems / grid), its warps take the range round-robin
+    const i64 q = nitems / gridDim.x, rem = nitems % gridDim.x;
+    const i64 first = (i64)blockIdx.x * q + ((i64)blockIdx.x < rem ? blockIdx.x : rem);
+    const i64 cnt = q + ((i64)blockIdx.x < rem ? 1 : 0);
+    for (i64 k = warp; k < cnt; k += nw) {
+        const i64 item = first + k;
+        if (item < nitems_full) {
+            const i64 off = item * (unit_mode ? UE : BM_REDUCE_BLOCK);
+            reduce_item_store<T, OP>(a, s, item, off, unit_mode ? UE : BM_REDUCE_BLOCK, tile, vec_ok, unit_mode);
         } else {
-            const DA v = block_dot<T>(s, off, len, vec_ok);
-            if (lane == 0) reinterpret_cast<DA*>(slots_d)[b - b0] = v;
+            reduce_item_store<T, OP>(a, s, item, nfull * BM_REDUCE_BLOCK, tail, tile, vec_ok, false);
         }
     }
-    __syncthreads();
     __shared__ bool am_last;
-    if constexpr (OP == 4) {
-        const DA v = cta_combine_pairwise<DA, 1>(reinterpret_cast<DA*>(slots_d), reinterpret_cast<DA*>(slots_d) + BM_MAX_GROUP, cnt);
-        if (threadIdx.x == 0) reinterpret_cast<DA*>(a.partials)[blockIdx.x] = v;
-    } else {
-        const T v = cta_combine_pairwise<T, OP>(reinterpret_cast<T*>(slots_d), reinterpret_cast<T*>(slots_d) + BM_MAX_GROUP, cnt);
-        if (threadIdx.x == 0) reinterpret_cast<T*>(a.partials)[blockIdx.x] = v;
-    }
     __threadfence();
-    if (threadIdx.x == 0) {
-        const unsigned int t = atomicAdd(a.ticket, 1u);
-        am_last = (t == gridDim.x - 1);
-    }
+    __syncthreads();
+    if (threadIdx.x == 0) am_last = (atomicAdd(a.ticket, 1u) == gridDim.x - 1);
     __syncthreads();
     if (!am_last) return;
     __threadfence();
-    const int nparts = gridDim.x;
-    // reuse the tile region for the final fold (gridDim.x <= BM_MAX_FINAL)
-    if constexpr (OP == 4) {
-        DA* v = reinterpret_cast<DA*>(smem);
-        for (int i = threadIdx.x; i < nparts; i += blockDim.x) v[i] = reinterpret_cast<volatile DA*>(a.partials)[i];
-        __syncthreads();
-        const DA r = cta_combine_pairwise<DA, 1>(v, v + BM_MAX_FINAL, nparts);
-        if (threadIdx.x == 0) {
-            reinterpret_cast<DA*>(a.result)[0] = r;
-            *a.ticket = 0u;
-        }
-    } else {
-        T* v = reinterpret_cast<T*>(smem);
-        for (int i = threadIdx.x; i < nparts; i += blockDim.x) v[i] = reinterpret_cast<volatile T*>(a.partials)[i];
-        __syncthreads();
-        const T r = cta_combine_pairwise<T, OP>(v, v + BM_MAX_FINAL, nparts);
-        if (threadIdx.x == 0) {
-            T fin = r;
-            if constexpr (OP == 1 && is_float_t<T>::value) fin = r + T(0);  // numpy: 0 + pairwise(...) (-0 -> +0)
-            reinterpret_cast<T*>(a.result)[0] = fin;
-            *a.ticket = 0u;
-        }
+    // ---- final fold (last CTA) ----
+    const volatile P* parts = reinterpret_cast<const volatile P*>(a.partials);
+    const i64 nblocks = nfull + (tail ? 1 : 0);
+    auto block_partial = [&](i64 b) -> P {
+        if (b == nfull) return parts[nitems - 1];          // ragged tail block
+        if (!unit_mode) return parts[b];
+        // numpy's balanced tree over the block's units
+        P v[UPB];
+#pragma unroll
+        for (int u = 0; u < UPB; ++u) v[u] = parts[b * UPB + u];
+#pragma unroll
+        for (int w = 1; w < UPB; w <<= 1)
+#pragma unroll
+            for (int u = 0; u + w < UPB; u += 2 * w) v[u] = Fold<P, OP>::units(v[u], v[u + w]);
+        return v[0];
+    };
+    // aligned power-of-two run of blocks per thread
+    i64 g = 1;
+    while (g * blockDim.x < nblocks) g <<= 1;
+    P* vals = reinterpret_cast<P*>(smem);
+    const i64 b0 = (i64)threadIdx.x * g;
+    if (b0 < nblocks) {
+        const i64 m = (b0 + g <= nblocks) ? g : nblocks - b0;
+        vals[threadIdx.x] = stream_pairwise<P, OP>(m, [&](i64 i) { return block_partial(b0 + i); });
+    }
+    const int nthr_vals = (int)((nblocks + g - 1) / g);
+    __syncthreads();
+    const P r = cta_combine_pairwise<P, OP>(vals, vals + blockDim.x, nthr_vals);
+    if (threadIdx.x == 0) {
+        P fin = r;
+        if constexpr (OP == 1 && is_float_t<T>::value) fin = r + T(0);  // numpy: 0 + pairwise(...) (-0 -> +0)
+        reinterpret_cast<P*>(a.result)[0] = fin;
+        *a.ticket = 0u;
     }
 }
 

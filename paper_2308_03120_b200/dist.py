@@ -32,12 +32,16 @@ def column_block(total_cols: int, rank: int, world: int) -> tuple[int, int]:
     return start, base + (1 if rank < extra else 0)
 
 
-def bind_torch_stream() -> None:
-    """Run the device library on torch's current CUDA stream so NCCL
-    collectives issued by torch.distributed are stream-ordered with it."""
+def bind_torch_stream():
+    """Make one CUDA stream current for both torch and the device library, so
+    NCCL collectives issued by torch.distributed and torch.cuda.Event timing
+    are stream-ordered with the library's kernels.  Returns the stream."""
     import torch
     rt = _rt.get_runtime()
-    _clib.check(rt._lib.bm_set_stream(ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)), "bind stream")
+    s = torch.cuda.Stream()
+    torch.cuda.set_stream(s)
+    _clib.check(rt._lib.bm_set_stream(ctypes.c_void_p(s.cuda_stream)), "bind stream")
+    return s
 
 
 def partial_dtype(op: str, elem: str) -> str:

@@ -701,14 +701,16 @@ class _PinnedBlock:
             pass
 
 
-def pinned_array(shape, dtype) -> np.ndarray:
+def pinned_array(shape, dtype, order: str = "F") -> np.ndarray:
     """A numpy array in page-locked host memory (fast, asynchronous-capable
-    host<->device copies).  The memory lives as long as the array."""
+    host<->device copies).  Column-major by default, the layout
+    Matrix.from_numpy uploads without a host-side copy.  The memory lives as
+    long as the array."""
     dt = np.dtype(dtype)
     n = int(np.prod(shape)) * dt.itemsize
     block = _PinnedBlock(n)
     buf = (ctypes.c_char * max(n, 1)).from_address(block.ptr)
-    arr = np.frombuffer(buf, dtype=dt, count=int(np.prod(shape))).reshape(shape)
+    arr = np.frombuffer(buf, dtype=dt, count=int(np.prod(shape))).reshape(shape, order=order)
     arr.setflags(write=True)
     _pinned_owners[id(arr)] = block
     import weakref

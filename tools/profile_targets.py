@@ -1,0 +1,43 @@
+"""Run one hot-path workload a few times so ncu can capture its kernel.
+Usage: python tools/profile_targets.py cfg1|gemm_f32|gemm_f64|rdim0|rdim1|dot"""
+import pathlib
+import sys
+
+import numpy as np
+
+sys.path.insert(0, str(pathlib.Path(__file__).resolve().parents[1]))
+
+
+def main(which: str) -> None:
+    import paper_2308_03120_b200 as dm
+    from paper_2308_03120_b200 import runtime as R
+    dm.init("b200")
+    rt = R.get_runtime()
+    if which == "cfg1":
+        rng = np.random.default_rng(0)
+        A, B, C, D = (dm.Matrix.from_numpy(rng.random((4096, 4096), dtype=np.float32)) for _ in range(4))
+        for _ in range(4):
+            dm.accu(2 * A + B % C - dm.exp(D))
+    elif which in ("gemm_f32", "gemm_f64"):
+        elem = which[-3:]
+        n = 8192
+        A = dm.Matrix(n, n, fill="randu", elem_type=elem)
+        B = dm.Matrix(n, n, fill="randu", elem_type=elem)
+        for _ in range(3):
+            dm.evaluate(A @ B.t())
+    elif which in ("rdim0", "rdim1"):
+        m = dm.Matrix(16384, 16384, fill="randu", elem_type="f64")
+        for op in ("sum", "max"):
+            for _ in range(2):
+                dm.evaluate(getattr(dm, op)(m, int(which[-1])))
+    elif which == "dot":
+        a = dm.Col(1 << 30, fill="randu")
+        b = dm.Col(1 << 30, fill="randu")
+        for _ in range(3):
+            dm.dot(a, b)
+    dm.synchronise()
+    dm.shutdown()
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])

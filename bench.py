@@ -263,6 +263,30 @@ def secondary_suite(dm, torch) -> dict:
             del A, B, C
     except Exception as e:  # pragma: no cover
         out["gemm_error"] = repr(e)[:200]
+    try:  # config 5: logistic-regression gradient step on 2^20 x 1024 f32
+        nrow, ncol = 1 << 20, 1024
+        dm.set_seed(5)
+        X = dm.Matrix(nrow, ncol, fill="randn")
+        w = dm.evaluate(0.03 * dm.Matrix(ncol, 1, fill="randn"))
+        y = dm.evaluate(dm.conv_to(dm.conv_to(2 * dm.Matrix(nrow, 1, fill="randu"), "i32"), "f32"))
+
+        def step():
+            z = dm.evaluate(X @ w)
+            r = dm.evaluate(1 / (1 + dm.exp(0 - z)) - y)
+            g = dm.evaluate(X.t() @ r)
+            return r, g
+
+        def timed():
+            r, g = step()
+            dm.accu(r)
+
+        t = best_ms(timed, reps=3)
+        nbytes = 2 * 4 * nrow * ncol
+        out["logistic_step_1Mx1024_f32"] = {"ms": t, "GB/s": nbytes / t / 1e6, "frac": nbytes / t / 1e6 / peak_hbm,
+                                            "note": "z=X@w, r=1/(1+exp(-z))-y, g=X.t()@r, accu(r); X read twice"}
+        del X
+    except Exception as e:  # pragma: no cover
+        out["logistic_error"] = repr(e)[:200]
     return out
 
 

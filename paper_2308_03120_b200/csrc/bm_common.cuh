@@ -226,6 +226,36 @@ template <typename T> __device__ __forceinline__ T np_max(T a, T b) {
 
 template <typename T> __device__ __forceinline__ T warp_shfl_xor(T v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
 
+// Branch-free running min/max with numpy's NaN propagation (ndarray.min/max):
+// any NaN makes the result NaN, otherwise the extreme value.  Order-free, so
+// lanes and threads may split the range arbitrarily.
+template <typename T> __device__ __forceinline__ T lowest_val();
+template <typename T> __device__ __forceinline__ T highest_val();
+template <typename T, bool IS_MAX>
+struct MinMaxAcc {
+    T v;
+    bool nan;
+    __device__ __forceinline__ MinMaxAcc() : v(IS_MAX ? lowest_val<T>() : highest_val<T>()), nan(false) {}
+    __device__ __forceinline__ void add(T x) {
+        nan |= (x != x);
+        v = IS_MAX ? ((x > v) ? x : v) : ((x < v) ? x : v);
+    }
+    __device__ __forceinline__ void merge(const MinMaxAcc& o) {
+        nan |= o.nan;
+        v = IS_MAX ? ((o.v > v) ? o.v : v) : ((o.v < v) ? o.v : v);
+    }
+    __device__ __forceinline__ void warp_merge() {
+#pragma unroll
+        for (int m = 16; m >= 1; m >>= 1) {
+            MinMaxAcc o;
+            o.v = warp_shfl_xor(v, m);
+            o.nan = __shfl_xor_sync(0xffffffffu, (int)nan, m) != 0;
+            merge(o);
+        }
+    }
+    __device__ __forceinline__ T result() const { return nan ? T(__longlong_as_double(0x7ff8000000000000LL)) : v; }
+};
+
 template <typename T> __device__ __forceinline__ T lowest_val();
 template <> __device__ __forceinline__ float lowest_val<float>() { return -__int_as_float(0x7f800000); }
 template <> __device__ __forceinline__ double lowest_val<double>() { return -__longlong_as_double(0x7ff0000000000000LL); }

@@ -55,14 +55,23 @@ __global__ void __launch_bounds__(256) rdim0_kernel(const T* __restrict__ a, i64
                 r = sum;
             }
         } else if constexpr (OP == 2 || OP == 3) {
-            T acc = col[0];
-            for (i64 i = lane; i < rows; i += 32) acc = (OP == 3) ? np_max(acc, col[i]) : np_min(acc, col[i]);
+            constexpr int V = 16 / sizeof(T);
+            MinMaxAcc<T, OP == 3> acc;
+            i64 i = 0;
+            if (vec_ok) {
+                for (; i + 4 * 32 * V <= rows; i += 4 * 32 * V) {
+                    T v[4][V];
 #pragma unroll
-            for (int m = 16; m >= 1; m >>= 1) {
-                const T o = warp_shfl_xor(acc, m);
-                acc = (OP == 3) ? np_max(acc, o) : np_min(acc, o);
+                    for (int u = 0; u < 4; ++u) s.template vec<V>(i + u * 32 * V + lane * V, v[u]);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                        for (int k = 0; k < V; ++k) acc.add(v[u][k]);
+                }
             }
-            r = acc;
+            for (i64 j = i + lane; j < rows; j += 32) acc.add(col[j]);
+            acc.warp_merge();
+            r = acc.result();
         } else {
             // unbiased variance, two passes in f64 (kernels.py:519-527)
             if (rows < 2) {
@@ -134,8 +143,8 @@ __global__ void __launch_bounds__(160, 1) rdim1_tma_kernel(const __grid_constant
     const int r = (warp - 1) * 32 + lane;  // row within the slab
     const bool active = r < RT && row0 + r < rows;
     T acc = T(0);
+    MinMaxAcc<T, OP == 3> mm;
     double dacc = 0.0, mean = 0.0;
-    bool first = true;
     i64 t = 0;
     for (int p = 0; p < passes; ++p) {
         for (i64 j = 0; j < ntiles; ++j, ++t) {
@@ -148,11 +157,7 @@ __global__ void __launch_bounds__(160, 1) rdim1_tma_kernel(const __grid_constant
                 if constexpr (OP == 1 || OP == 5) {
                     for (int c = 0; c < nc; ++c) acc = OpPlus::f(acc, tile[c * RT + r]);
                 } else if constexpr (OP == 2 || OP == 3) {
-                    for (int c = 0; c < nc; ++c) {
-                        const T x = tile[c * RT + r];
-                        if (first) { acc = x; first = false; }
-                        else acc = (OP == 3) ? np_max(acc, x) : np_min(acc, x);
-                    }
+                    for (int c = 0; c < nc; ++c) mm.add(tile[c * RT + r]);
                 } else {
                     if (p == 0) {
                         for (int c = 0; c < nc; ++c) dacc += cvt<double>(tile[c * RT + r]);
@@ -178,6 +183,7 @@ __global__ void __launch_bounds__(160, 1) rdim1_tma_kernel(const __grid_constant
     T res;
     if constexpr (OP == 5) res = OpDiv::f(acc, KScal<T>::f((double)cols, cols));
     else if constexpr (OP == 6) res = (cols < 2) ? T(0) : cvt<T>(dacc / (double)(cols - 1));
+    else if constexpr (OP == 2 || OP == 3) res = mm.result();
     else res = acc;
     out[row0 + r] = res;
 }

@@ -45,6 +45,7 @@ struct Args {
     i64 blocks;                 // number of REDUCE_BLOCK blocks (informational)
     int group;                  // reductions: 1 = unit mode, 0 = block mode
     int vec_ok;                 // all views contiguous and 16-B aligned
+    int smem_bytes;             // dynamic shared memory of the launch
 };
 
 // ---------------------------------------------------------------------------
@@ -322,30 +323,22 @@ template <typename T, bool IS_MAX, class S>
 __device__ __forceinline__ T block_minmax(const S& s, i64 off, i64 len, bool vec_ok) {
     constexpr int V = 16 / sizeof(T);
     const int lane = threadIdx.x & 31;
-    T acc = s.at(off);  // len >= 1
+    MinMaxAcc<T, IS_MAX> acc;
     if (vec_ok && len % (4 * 32 * V) == 0) {
         for (i64 i = lane * V; i < len; i += 4 * 32 * V) {
             T v[4][V];
 #pragma unroll
             for (int u = 0; u < 4; ++u) s.template vec<V>(off + i + u * 32 * V, v[u]);
-            asm volatile("" ::: "memory");   // keep the four loads in flight together
 #pragma unroll
             for (int u = 0; u < 4; ++u)
 #pragma unroll
-                for (int k = 0; k < V; ++k) acc = IS_MAX ? np_max(acc, v[u][k]) : np_min(acc, v[u][k]);
+                for (int k = 0; k < V; ++k) acc.add(v[u][k]);
         }
     } else {
-        for (i64 i = lane; i < len; i += 32) {
-            const T x = s.at(off + i);
-            acc = IS_MAX ? np_max(acc, x) : np_min(acc, x);
-        }
+        for (i64 i = lane; i < len; i += 32) acc.add(s.at(off + i));
     }
-#pragma unroll
-    for (int m = 16; m >= 1; m >>= 1) {
-        const T o = warp_shfl_xor(acc, m);
-        acc = IS_MAX ? np_max(acc, o) : np_min(acc, o);
-    }
-    return acc;
+    acc.warp_merge();
+    return acc.result();
 }
 
 // dot partials accumulate in double for float inputs (the reference block
@@ -518,33 +511,51 @@ __device__ void reduce_flat(const Args& a, const S& s) {
     if (!am_last) return;
     __threadfence();
     // ---- final fold (last CTA) ----
+    // Block partials are staged into shared memory with coalesced, independent
+    // loads (all threads), one aligned power-of-two chunk of blocks at a time,
+    // folded there with combine_pairwise; chunk results fold the same way.
     const volatile P* parts = reinterpret_cast<const volatile P*>(a.partials);
     const i64 nblocks = nfull + (tail ? 1 : 0);
-    auto block_partial = [&](i64 b) -> P {
-        if (b == nfull) return parts[nitems - 1];          // ragged tail block
-        if (!unit_mode) return parts[b];
-        // numpy's balanced tree over the block's units
-        P v[UPB];
+    const int smem_vals = (int)(a.smem_bytes / sizeof(P));
+    int chunk = 1;
+    while (2 * chunk <= smem_vals) chunk <<= 1;
+    chunk >>= 1;                                   // ping-pong halves
+    P* buf = reinterpret_cast<P*>(smem);
+    P* buf2 = buf + chunk;
+    __shared__ P chunk_res[1024];
+    const i64 nchunks = (nblocks + chunk - 1) / chunk;
+    P r = P(0);
+    for (i64 ck = 0; ck < nchunks; ++ck) {
+        const i64 c0 = ck * chunk;
+        const int cn = (int)((nblocks - c0) < chunk ? (nblocks - c0) : chunk);
+        if (unit_mode) {
+            for (int i = threadIdx.x; i < cn; i += blockDim.x) {
+                const i64 b = c0 + i;
+                if (b == nfull) {
+                    buf[i] = parts[nitems - 1];
+                } else {
+                    P v[UPB];
 #pragma unroll
-        for (int u = 0; u < UPB; ++u) v[u] = parts[b * UPB + u];
+                    for (int u = 0; u < UPB; ++u) v[u] = parts[b * UPB + u];
 #pragma unroll
-        for (int w = 1; w < UPB; w <<= 1)
+                    for (int w = 1; w < UPB; w <<= 1)
 #pragma unroll
-            for (int u = 0; u + w < UPB; u += 2 * w) v[u] = Fold<P, OP>::units(v[u], v[u + w]);
-        return v[0];
-    };
-    // aligned power-of-two run of blocks per thread
-    i64 g = 1;
-    while (g * blockDim.x < nblocks) g <<= 1;
-    P* vals = reinterpret_cast<P*>(smem);
-    const i64 b0 = (i64)threadIdx.x * g;
-    if (b0 < nblocks) {
-        const i64 m = (b0 + g <= nblocks) ? g : nblocks - b0;
-        vals[threadIdx.x] = stream_pairwise<P, OP>(m, [&](i64 i) { return block_partial(b0 + i); });
+                        for (int u = 0; u + w < UPB; u += 2 * w) v[u] = Fold<P, OP>::units(v[u], v[u + w]);
+                    buf[i] = v[0];
+                }
+            }
+        } else {
+            for (int i = threadIdx.x; i < cn; i += blockDim.x) buf[i] = parts[c0 + i];
+        }
+        __syncthreads();
+        const P cr = cta_combine_pairwise<P, OP>(buf, buf2, cn);
+        if (threadIdx.x == 0) chunk_res[ck] = cr;     // host guarantees nchunks <= 1024
+        __syncthreads();
     }
-    const int nthr_vals = (int)((nblocks + g - 1) / g);
-    __syncthreads();
-    const P r = cta_combine_pairwise<P, OP>(vals, vals + blockDim.x, nthr_vals);
+    if (threadIdx.x == 0) {
+        // combine_pairwise over the chunk results (aligned power-of-two groups)
+        r = stream_pairwise<P, OP>(nchunks, [&](i64 i) { return chunk_res[i]; });
+    }
     if (threadIdx.x == 0) {
         P fin = r;
         if constexpr (OP == 1 && is_float_t<T>::value) fin = r + T(0);  // numpy: 0 + pairwise(...) (-0 -> +0)

@@ -44,6 +44,51 @@ static int combine_typed(const void* parts, int64_t count, int op, void* out) {
     return set_error(BM_ERR_ARG, "combine: bad reduce op");
 }
 
+template <typename P, int OP, int UPB, bool NORM>
+static int fold_typed(const void* parts, int64_t nitems, int64_t nfull, bool unit_mode, int chunk, int nchunks,
+                      void* result) {
+    static void* scratch = nullptr;
+    if (!scratch) BM_CUDA(cudaMalloc(&scratch, 8 * 8192));
+    const int smem = 2 * chunk * (int)sizeof(P);
+    static bool attr = false;
+    if (!attr) {
+        BM_CUDA(cudaFuncSetAttribute(bm::fold_chunks_kernel<P, OP, UPB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     160 * 1024));
+        attr = true;
+    }
+    bm::fold_chunks_kernel<P, OP, UPB><<<nchunks, 512, smem, st().stream>>>(
+        (const P*)parts, nitems, nfull, unit_mode ? 1 : 0, chunk, (P*)scratch);
+    BM_CUDA(cudaGetLastError());
+    bm::fold_final_kernel<P, OP, NORM><<<1, 32, 0, st().stream>>>((const P*)scratch, nchunks, (P*)result);
+    BM_CUDA(cudaGetLastError());
+    st().launches += 2;
+    return BM_OK;
+}
+
+int launch_fold(int dtype, int op, const void* parts, int64_t nitems, int64_t nfull, bool unit_mode, int chunk,
+                int nchunks, void* result) {
+#define BM_FOLD(P, UPB, NORM)                                                                                     \
+    switch (op) {                                                                                                  \
+        case BM_R_ACCU: return fold_typed<P, 1, UPB, NORM>(parts, nitems, nfull, unit_mode, chunk, nchunks, result); \
+        case BM_R_MIN: return fold_typed<P, 2, UPB, false>(parts, nitems, nfull, unit_mode, chunk, nchunks, result); \
+        case BM_R_MAX: return fold_typed<P, 3, UPB, false>(parts, nitems, nfull, unit_mode, chunk, nchunks, result); \
+    }
+    if (op == BM_R_DOT) {
+        if (dtype == BM_F32) return fold_typed<double, 1, 4, false>(parts, nitems, nfull, unit_mode, chunk, nchunks, result);
+        if (dtype == BM_F64) return fold_typed<double, 1, 8, false>(parts, nitems, nfull, unit_mode, chunk, nchunks, result);
+        if (dtype == BM_I32) return fold_typed<int, 1, 4, false>(parts, nitems, nfull, unit_mode, chunk, nchunks, result);
+        return fold_typed<unsigned long long, 1, 8, false>(parts, nitems, nfull, unit_mode, chunk, nchunks, result);
+    }
+    switch (dtype) {
+        case BM_F32: BM_FOLD(float, 4, true) break;
+        case BM_F64: BM_FOLD(double, 8, true) break;
+        case BM_I32: BM_FOLD(int, 4, false) break;
+        case BM_U64: BM_FOLD(unsigned long long, 8, false) break;
+    }
+#undef BM_FOLD
+    return set_error(BM_ERR_ARG, "fold: bad dtype/op");
+}
+
 int combine_partials(const void* parts, int64_t count, int dtype, int op, void* out) {
     if (count < 1 || count > 2048) return set_error(BM_ERR_ARG, "combine: partial count out of range");
     switch (dtype) {

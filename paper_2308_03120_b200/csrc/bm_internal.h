@@ -71,6 +71,8 @@ int launch_rdim(const bm_invocation* inv);
 int launch_gemm(const bm_invocation* inv);
 int launch_misc(const bm_invocation* inv);
 int combine_partials(const void* dev_partials, int64_t count, int dtype, int op, void* dev_out);
+int launch_fold(int dtype, int op, const void* partials, int64_t nitems, int64_t nfull, bool unit_mode, int chunk,
+                int nchunks, void* result);
 
 // grid heuristics
 inline int ewise_grid(int64_t n_vec_units) {

@@ -46,6 +46,7 @@ struct Args {
     int group;                  // reductions: 1 = unit mode, 0 = block mode
     int vec_ok;                 // all views contiguous and 16-B aligned
     int smem_bytes;             // dynamic shared memory of the launch
+    int ext_fold;               // 1: leave the partials for the separate fold kernels
 };
 
 // ---------------------------------------------------------------------------
@@ -503,6 +504,7 @@ __device__ void reduce_flat(const Args& a, const S& s) {
             reduce_item_store<T, OP>(a, s, item, nfull * BM_REDUCE_BLOCK, tail, tile, vec_ok, false);
         }
     }
+    if (a.ext_fold) return;   // large reductions: folded by fold_chunks_kernel / fold_final_kernel
     __shared__ bool am_last;
     __threadfence();
     __syncthreads();
@@ -562,6 +564,51 @@ __device__ void reduce_flat(const Args& a, const S& s) {
         reinterpret_cast<P*>(a.result)[0] = fin;
         *a.ticket = 0u;
     }
+}
+
+// ---------------------------------------------------------------------------
+// External fold for large reductions: CTA k folds the aligned chunk k of
+// block partials (combine_pairwise in shared memory), then one CTA folds the
+// chunk results.  Equal to one combine_pairwise over all blocks (aligned
+// power-of-two groups fold independently).
+
+template <typename P, int OP, int UPB>
+__global__ void __launch_bounds__(512) fold_chunks_kernel(const P* __restrict__ parts, i64 nitems, i64 nfull,
+                                                          int unit_mode, int chunk, P* __restrict__ out) {
+    extern __shared__ __align__(16) char smem[];
+    P* buf = reinterpret_cast<P*>(smem);
+    P* buf2 = buf + chunk;
+    const i64 nblocks = nfull + (nitems > (unit_mode ? nfull * UPB : nfull) ? 1 : 0);
+    const i64 c0 = (i64)blockIdx.x * chunk;
+    const int cn = (int)((nblocks - c0) < chunk ? (nblocks - c0) : chunk);
+    for (int i = threadIdx.x; i < cn; i += blockDim.x) {
+        const i64 b = c0 + i;
+        if (b == nfull) {
+            buf[i] = parts[nitems - 1];
+        } else if (unit_mode) {
+            P v[UPB];
+#pragma unroll
+            for (int u = 0; u < UPB; ++u) v[u] = parts[b * UPB + u];
+#pragma unroll
+            for (int w = 1; w < UPB; w <<= 1)
+#pragma unroll
+                for (int u = 0; u + w < UPB; u += 2 * w) v[u] = Fold<P, OP>::units(v[u], v[u + w]);
+            buf[i] = v[0];
+        } else {
+            buf[i] = parts[b];
+        }
+    }
+    __syncthreads();
+    const P r = cta_combine_pairwise<P, OP>(buf, buf2, cn);
+    if (threadIdx.x == 0) out[blockIdx.x] = r;
+}
+
+template <typename P, int OP, bool NORMALISE>
+__global__ void __launch_bounds__(32) fold_final_kernel(const P* __restrict__ chunks, int n, P* __restrict__ result) {
+    if (threadIdx.x != 0) return;
+    P r = stream_pairwise<P, OP>(n, [&](i64 i) { return chunks[i]; });
+    if (NORMALISE) r = r + P(0);
+    result[0] = r;
 }
 
 }  // namespace bm

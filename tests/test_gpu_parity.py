@@ -269,3 +269,19 @@ def test_rng_bit_exact(dm):
         same(dm.Matrix(40, 25, fill="randu", elem_type=elem).to_numpy(), g[f"randu_{seed}"])
         got = dm.Matrix(33, 17, fill="randn", elem_type=elem).to_numpy()
         ulp_close(got, g[f"randn_{seed}"], 1e-6 if elem == "f32" else 1e-13)
+
+
+@pytest.mark.slow
+def test_large_reductions_external_fold(dm):
+    """n large enough that the final fold runs as separate chunk kernels."""
+    n = (1 << 28) + 12345
+    rng = np.random.default_rng(11)
+    v = rng.random(n, dtype=np.float32)
+    w = rng.random(n, dtype=np.float32)
+    mv, mw = dm.Matrix.from_numpy(v.reshape(-1, 1)), dm.Matrix.from_numpy(w.reshape(-1, 1))
+    same(np.float32(dm.accu(mv)), O.reduce_accu(v))
+    same(np.float32(dm.reduce_max(mv)), np.float32(O.reduce_max(v)))
+    same(np.float32(dm.reduce_min(mv)), np.float32(O.reduce_min(v)))
+    assert rel_err(dm.dot(mv, mw), O.reduce_dot(v, w)) <= 1e-5
+    vd = v[: 1 << 27].astype(np.float64)
+    same(np.float64(dm.accu(dm.Matrix.from_numpy(vd.reshape(-1, 1)))), O.reduce_accu(vd))

@@ -229,8 +229,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 }
 
 // ---------------------------------------------------------------------------
-// f64: DMMA m8n8k4.  CTA tile 64x64, 4 warps of 32x32 (4x4 DMMA tiles each),
-// K staged 16 at a time through double-buffered shared memory (cp.async).
+// f64: DMMA m8n8k4 (mma.sync f64 runs on the FP64 tensor path of sm_100).
+// CTA tile 128x128, 8 warps of 64x32 (8x4 DMMA tiles each, 64 f64
+// accumulators per lane), K staged 16 at a time through a 3-stage cp.async
+// (LDGSTS) ring so global latency overlaps the DMMAs.  Out-of-range elements
+// are zero-filled by cp.async's src-size operand.
 
 __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
@@ -238,67 +241,94 @@ __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
                  : "d"(a), "d"(b));
 }
 
-#define DM_BM 64
-#define DM_BN 64
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src),
+                 "r"(valid ? 8 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+#define DM_BM 128
+#define DM_BN 128
 #define DM_BK 16
+#define DM_ST 3
+#define DM_LD (DM_BM + 8)
+#define DM_SMEM (DM_ST * 2 * DM_BK * DM_LD * 8)
 
 template <bool TA, bool TB>
-__global__ void __launch_bounds__(128) gemm_dmma_kernel(const double* __restrict__ A, i64 lda,
-                                                        const double* __restrict__ B, i64 ldb, double* __restrict__ C,
-                                                        i64 ldc, i64 m, i64 n, i64 k) {
-    // As[k][m], Bs[k][n] (+1 padding)
-    __shared__ double As[2][DM_BK][DM_BM + 1];
-    __shared__ double Bs[2][DM_BK][DM_BN + 1];
+__global__ void __launch_bounds__(256, 1) gemm_dmma_kernel(const double* __restrict__ A, i64 lda,
+                                                           const double* __restrict__ B, i64 ldb,
+                                                           double* __restrict__ C, i64 ldc, i64 m, i64 n, i64 k) {
+    extern __shared__ __align__(16) double dsm[];
+    double* As = dsm;                                  // [ST][BK][LD]
+    double* Bs = dsm + DM_ST * DM_BK * DM_LD;          // [ST][BK][LD]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int gid = lane >> 2, tig = lane & 3;
     const i64 m0 = (i64)blockIdx.y * DM_BM, n0 = (i64)blockIdx.x * DM_BN;
-    const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
-    double acc[4][4][2];
+    const int wm = (warp >> 2) * 64, wn = (warp & 3) * 32;
+    double acc[8][4][2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    auto load = [&](int buf, i64 k0) {
-        for (int idx = threadIdx.x; idx < DM_BK * DM_BM; idx += 128) {
+    auto load = [&](int st, i64 k0) {
+        double* as = As + st * DM_BK * DM_LD;
+        double* bs = Bs + st * DM_BK * DM_LD;
+#pragma unroll
+        for (int t = 0; t < (DM_BK * DM_BM) / 256; ++t) {
+            const int idx = threadIdx.x + t * 256;
             int kk, mm;
             if (TA) { mm = idx / DM_BK; kk = idx % DM_BK; } else { kk = idx / DM_BM; mm = idx % DM_BM; }
             const i64 gi = m0 + mm, gl = k0 + kk;
-            double v = 0.0;
-            if (gi < m && gl < k) v = TA ? A[gl + gi * lda] : A[gi + gl * lda];
-            As[buf][kk][mm] = v;
+            const bool ok = gi < m && gl < k;
+            const double* src = ok ? (TA ? A + gl + gi * lda : A + gi + gl * lda) : A;
+            cp_async8(as + kk * DM_LD + mm, src, ok);
         }
-        for (int idx = threadIdx.x; idx < DM_BK * DM_BN; idx += 128) {
+#pragma unroll
+        for (int t = 0; t < (DM_BK * DM_BN) / 256; ++t) {
+            const int idx = threadIdx.x + t * 256;
             int kk, nn;
             if (TB) { kk = idx / DM_BN; nn = idx % DM_BN; } else { nn = idx / DM_BK; kk = idx % DM_BK; }
             const i64 gj = n0 + nn, gl = k0 + kk;
-            double v = 0.0;
-            if (gj < n && gl < k) v = TB ? B[gj + gl * ldb] : B[gl + gj * ldb];
-            Bs[buf][kk][nn] = v;
+            const bool ok = gj < n && gl < k;
+            const double* src = ok ? (TB ? B + gj + gl * ldb : B + gl + gj * ldb) : B;
+            cp_async8(bs + kk * DM_LD + nn, src, ok);
         }
     };
-    load(0, 0);
-    __syncthreads();
-    int buf = 0;
-    for (i64 k0 = 0; k0 < k; k0 += DM_BK) {
-        if (k0 + DM_BK < k) load(buf ^ 1, k0 + DM_BK);
+    const i64 nk = (k + DM_BK - 1) / DM_BK;
+#pragma unroll
+    for (int st = 0; st < DM_ST - 1; ++st) {
+        if (st < nk) load(st, st * DM_BK);
+        cp_async_commit();
+    }
+    for (i64 kb = 0; kb < nk; ++kb) {
+        cp_async_wait<DM_ST - 2>();
+        __syncthreads();
+        // prefetch stage kb + ST - 1 into the buffer consumed at kb - 1
+        const i64 nxt = kb + DM_ST - 1;
+        if (nxt < nk) load((int)(nxt % DM_ST), nxt * DM_BK);
+        cp_async_commit();
+        const double* as = As + (kb % DM_ST) * DM_BK * DM_LD;
+        const double* bs = Bs + (kb % DM_ST) * DM_BK * DM_LD;
 #pragma unroll
         for (int ks = 0; ks < DM_BK; ks += 4) {
-            double af[4], bf[4];
+            double af[8], bf[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) af[i] = As[buf][ks + tig][wm + 8 * i + gid];
+            for (int i = 0; i < 8; ++i) af[i] = as[(ks + tig) * DM_LD + wm + 8 * i + gid];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) bf[j] = Bs[buf][ks + tig][wn + 8 * j + gid];
+            for (int j = 0; j < 4; ++j) bf[j] = bs[(ks + tig) * DM_LD + wn + 8 * j + gid];
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < 8; ++i)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j], af[i], bf[j]);
         }
-        __syncthreads();
-        buf ^= 1;
     }
+    cp_async_wait<0>();
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j)
 #pragma unroll
@@ -386,12 +416,20 @@ int gemm_dmma_f64(int ta, int tb, int64_t m, int64_t n, int64_t k, const double*
     dim3 grid((unsigned)((n + DM_BN - 1) / DM_BN), (unsigned)((m + DM_BM - 1) / DM_BM));
     if (grid.y > 65535) return BM_OK;
     cudaStream_t s = st().stream;
+    static bool attr = false;
+    if (!attr) {
+        BM_CUDA(cudaFuncSetAttribute(bm::gemm_dmma_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, DM_SMEM));
+        BM_CUDA(cudaFuncSetAttribute(bm::gemm_dmma_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, DM_SMEM));
+        BM_CUDA(cudaFuncSetAttribute(bm::gemm_dmma_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, DM_SMEM));
+        BM_CUDA(cudaFuncSetAttribute(bm::gemm_dmma_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, DM_SMEM));
+        attr = true;
+    }
     if (ta) {
-        if (tb) bm::gemm_dmma_kernel<true, true><<<grid, 128, 0, s>>>(A, lda, B, ldb, C, ldc, m, n, k);
-        else bm::gemm_dmma_kernel<true, false><<<grid, 128, 0, s>>>(A, lda, B, ldb, C, ldc, m, n, k);
+        if (tb) bm::gemm_dmma_kernel<true, true><<<grid, 256, DM_SMEM, s>>>(A, lda, B, ldb, C, ldc, m, n, k);
+        else bm::gemm_dmma_kernel<true, false><<<grid, 256, DM_SMEM, s>>>(A, lda, B, ldb, C, ldc, m, n, k);
     } else {
-        if (tb) bm::gemm_dmma_kernel<false, true><<<grid, 128, 0, s>>>(A, lda, B, ldb, C, ldc, m, n, k);
-        else bm::gemm_dmma_kernel<false, false><<<grid, 128, 0, s>>>(A, lda, B, ldb, C, ldc, m, n, k);
+        if (tb) bm::gemm_dmma_kernel<false, true><<<grid, 256, DM_SMEM, s>>>(A, lda, B, ldb, C, ldc, m, n, k);
+        else bm::gemm_dmma_kernel<false, false><<<grid, 256, DM_SMEM, s>>>(A, lda, B, ldb, C, ldc, m, n, k);
     }
     BM_CUDA(cudaGetLastError());
     st().launches++;

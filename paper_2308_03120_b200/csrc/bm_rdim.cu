@@ -18,6 +18,7 @@
 
 #include "bm_internal.h"
 #include "bm_ptx.cuh"
+#define BM_UNIT_UNROLL 16   // single input: all 16 rows of a pairwise unit in flight
 #include "bm_reduce.cuh"
 
 namespace bm {
@@ -26,7 +27,7 @@ namespace bm {
 // dim 0
 
 template <typename T, int OP>
-__global__ void __launch_bounds__(256) rdim0_kernel(const T* __restrict__ a, i64 rows, i64 cols, i64 lda, T* out,
+__global__ void __launch_bounds__(256, 2) rdim0_kernel(const T* __restrict__ a, i64 rows, i64 cols, i64 lda, T* out,
                                                     int vec_ok) {
     extern __shared__ __align__(16) char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -250,7 +251,7 @@ static int rdim_launch(const bm_view& in, void* out_base, int dim) {
         if (cols == 0) return BM_OK;
         const bool vec = (((uintptr_t)a & 15u) == 0) && ((lda * sz) % 16 == 0);
         int grid = (int)((cols + 7) / 8);
-        const int cap = st().sm_count * 3;
+        const int cap = st().sm_count * 2;   // 2 resident CTAs per SM (registers)
         if (grid > cap) grid = cap;
         static bool attr = false;
         if (!attr) {

@@ -556,7 +556,8 @@ class _Lowerer:
         prog = self._fit_program(root, elem)
         shape = shape_of(root)
         if prog.n_stages == 1 and len(prog.stages) == len(prog.inputs) + 1 and \
-                all(prog.stages[i] == ("load", i) for i in range(len(prog.inputs))):
+                all(prog.stages[i] == ("load", i) for i in range(len(prog.inputs))) and \
+                all(self._ref_elem(r) == elem for r in prog.inputs):
             # one stage over distinct inputs: the reference's dedicated kernel name
             st = prog.stages[-1]
             scal = (st[2],) if len(st) > 2 and st[2] is not None else ()
@@ -565,6 +566,9 @@ class _Lowerer:
         return self.emit("fused_chain", prog.inputs, ["flat"] * len(prog.inputs), shape, want, "flat",
                          params={"program": tuple(prog.stages), "compute_dtype": NP_DTYPE[elem].str},
                          absorbed_from=elem)
+
+    def _ref_elem(self, ref) -> str:
+        return ref[1].elem_type if ref[0] == "leaf" else self.slots[ref[1]].elem_type
 
     def _generator(self, node: ExprNode, want: str):
         shape = shape_of(node)

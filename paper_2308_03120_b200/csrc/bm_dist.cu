@@ -74,16 +74,18 @@ int launch_fold(int dtype, int op, const void* parts, int64_t nitems, int64_t nf
         case BM_R_MAX: return fold_typed<P, 3, UPB, false>(parts, nitems, nfull, unit_mode, chunk, nchunks, result); \
     }
     if (op == BM_R_DOT) {
-        if (dtype == BM_F32) return fold_typed<double, 1, 4, false>(parts, nitems, nfull, unit_mode, chunk, nchunks, result);
-        if (dtype == BM_F64) return fold_typed<double, 1, 8, false>(parts, nitems, nfull, unit_mode, chunk, nchunks, result);
-        if (dtype == BM_I32) return fold_typed<int, 1, 4, false>(parts, nitems, nfull, unit_mode, chunk, nchunks, result);
-        return fold_typed<unsigned long long, 1, 8, false>(parts, nitems, nfull, unit_mode, chunk, nchunks, result);
+        if (dtype == BM_F32) return fold_typed<double, 1, 8, false>(parts, nitems, nfull, unit_mode, chunk, nchunks, result);
+        if (dtype == BM_F64) return fold_typed<double, 1, 16, false>(parts, nitems, nfull, unit_mode, chunk, nchunks, result);
+        if (dtype == BM_I32) return fold_typed<int, 1, 8, false>(parts, nitems, nfull, unit_mode, chunk, nchunks, result);
+        return fold_typed<unsigned long long, 1, 16, false>(parts, nitems, nfull, unit_mode, chunk, nchunks, result);
     }
     switch (dtype) {
-        case BM_F32: BM_FOLD(float, 4, true) break;
-        case BM_F64: BM_FOLD(double, 8, true) break;
-        case BM_I32: BM_FOLD(int, 4, false) break;
-        case BM_U64: BM_FOLD(unsigned long long, 8, false) break;
+        // unit-mode items are half-units (bm_reduce.cuh PwHalf): 8 per block
+        // for 4-byte types, 16 for 8-byte types
+        case BM_F32: BM_FOLD(float, 8, true) break;
+        case BM_F64: BM_FOLD(double, 16, true) break;
+        case BM_I32: BM_FOLD(int, 8, false) break;
+        case BM_U64: BM_FOLD(unsigned long long, 16, false) break;
     }
 #undef BM_FOLD
     return set_error(BM_ERR_ARG, "fold: bad dtype/op");

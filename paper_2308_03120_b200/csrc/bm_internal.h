@@ -19,8 +19,13 @@ struct State {
     int sm_count = 0;
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;     // current stream (own or external)
-    void* partials = nullptr;          // reduction scratch (per-CTA partials)
-    unsigned int* ticket = nullptr;    // last-CTA counter, zero between launches
+    // reduction scratch, double-buffered: consecutive reductions alternate so
+    // that a launch overlapping its predecessor's final fold (programmatic
+    // dependent launch) never touches the predecessor's partials or ticket
+    void* partials[2] = {nullptr, nullptr};
+    int64_t partials_cap = 0;          // capacity of each, in 8-byte entries
+    int flip = 0;                      // buffer of the next reduction
+    unsigned int* ticket = nullptr;    // two last-CTA counters (at +0 and +32), zero between launches
     void* result = nullptr;            // device slot of the final value
     void* host_slot = nullptr;         // pinned 64 B for scalar results
     std::recursive_mutex mu;           // serialises stream use across host threads
@@ -58,7 +63,9 @@ struct Driver {
     PFN_cuModuleLoadData_v2000 moduleLoadData = nullptr;
     PFN_cuModuleGetFunction_v2000 moduleGetFunction = nullptr;
     PFN_cuLaunchKernel_v4000 launchKernel = nullptr;
+    PFN_cuLaunchKernelEx_v11060 launchKernelEx = nullptr;
     PFN_cuFuncSetAttribute_v9000 funcSetAttribute = nullptr;
+    PFN_cuFuncGetAttribute_v2020 funcGetAttribute = nullptr;
     PFN_cuTensorMapEncodeTiled_v12000 tensorMapEncodeTiled = nullptr;
     bool ok = false;
 };

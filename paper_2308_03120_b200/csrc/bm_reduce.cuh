@@ -10,21 +10,26 @@
 // exactly, so f32/f64 accu is bit-identical to the reference for every
 // element-wise program whose element values are bit-identical.
 //
-// Fast path for one 128-element numpy leaf ("chunk"): a warp loads 16 rows of
-// 512 B fully coalesced (16-B vectors), parks them in a padded shared tile
-// (row pitch 544 B) and re-reads them transposed so each lane owns the
-// interleaved accumulators of one chunk; the 34-unit pitch makes both the
-// row writes and the transposed 16-B reads bank-conflict free.  Per warp
-// that is one "unit" of 2048 f32 / 1024 f64 elements.
+// Fast path for numpy leaves of 128 elements: a warp loads 8 rows of 512 B
+// fully coalesced (16-B vectors), parks them in a padded shared tile (row
+// pitch 544 B) and re-reads them transposed so that each lane owns some of
+// the 8 interleaved accumulators of one leaf; the 34-unit pitch makes both
+// the row writes and the transposed 8-B reads bank-conflict free.  Per warp
+// that is one "half-unit" of 1024 f32 / 512 f64 elements, a balanced subtree
+// of numpy's split of an 8192-element block.
 #pragma once
 #include "bm_common.cuh"
 
 namespace bm {
 
+#ifndef BM_TRACE
+#define BM_TRACE(k)   // fold timing hook (tools/fold_micro.cu)
+#endif
+
 #define BM_MAXIN 16
 #define BM_REDUCE_BLOCK 8192
 #define BM_TILE_PITCH 544
-#define BM_TILE_BYTES (16 * BM_TILE_PITCH)
+#define BM_TILE_BYTES (8 * BM_TILE_PITCH)   // one half-unit (8 rows of 512 B)
 #define BM_RWARPS 16                     // default warps per (persistent) reduction CTA
 #define BM_REDUCE_SMEM (BM_RWARPS * BM_TILE_BYTES)
 #ifndef BM_UNIT_UNROLL
@@ -47,6 +52,7 @@ struct Args {
     int vec_ok;                 // all views contiguous and 16-B aligned
     int smem_bytes;             // dynamic shared memory of the launch
     int ext_fold;               // 1: leave the partials for the separate fold kernels
+    int grab;                   // items a warp takes per counter fetch (dynamic scheduling)
 };
 
 // ---------------------------------------------------------------------------
@@ -139,14 +145,65 @@ __device__ __forceinline__ void ewise_store(const Args& a) {
 // ---------------------------------------------------------------------------
 // numpy pairwise summation
 
-// one warp-cooperative unit: 16 rows x (32 lanes x 16 B)
+// Half a unit: 8 rows of 512 B (8 numpy leaves of f32, 4 of f64; 1024 / 512
+// elements).  A half-unit is a balanced subtree of the 8192-element block, so
+// half-unit partials fold into block partials exactly like units do; halving
+// the work item doubles the item count, which balances the persistent CTAs'
+// warps (config 1: 16384 items over 2368 warps, 6.9 rounds
+// instead of 3.5 -> 4).
+template <typename T> struct PwHalf { static const int value = 32 * 8 * (16 / sizeof(T)); };
+
+// numpy pairwise value of the 8 rows parked in `tile` (pitch BM_TILE_PITCH);
+// returned in every lane.  8-byte transposed reads: for both element sizes
+// the 32 lanes of one read cover all 32 banks twice (2 wavefronts, ideal).
+template <typename T>
+__device__ __forceinline__ T pw_half_tile(const char* tile) {
+    const int lane = threadIdx.x & 31;
+    if constexpr (sizeof(T) == 4) {
+        // 8 leaves (rows) x 4 lanes; lane (c, q) owns accumulators 2q, 2q+1
+        const int c = lane >> 2, q = lane & 3;
+        const char* base = tile + c * BM_TILE_PITCH + q * 8;
+        uint2 w = *reinterpret_cast<const uint2*>(base);
+        T r0 = __uint_as_float(w.x), r1 = __uint_as_float(w.y);
+#pragma unroll
+        for (int i = 1; i < 16; ++i) {
+            w = *reinterpret_cast<const uint2*>(base + i * 32);
+            r0 = r0 + __uint_as_float(w.x);
+            r1 = r1 + __uint_as_float(w.y);
+        }
+        T t = r0 + r1;                   // r[2q] + r[2q+1]
+        t = t + warp_shfl_xor(t, 1);     // (r0+r1)+(r2+r3) | (r4+r5)+(r6+r7)
+        t = t + warp_shfl_xor(t, 2);     // leaf (128)
+        t = t + warp_shfl_xor(t, 4);     // 256
+        t = t + warp_shfl_xor(t, 8);     // 512
+        t = t + warp_shfl_xor(t, 16);    // 1024
+        return t;
+    } else {
+        // 4 leaves (2 rows each) x 8 lanes; lane (c, j) owns accumulator j
+        const int c = lane >> 3, j = lane & 7;
+        const char* base = tile + 2 * c * BM_TILE_PITCH + j * 8;
+        T r = *reinterpret_cast<const T*>(base);
+#pragma unroll
+        for (int i = 1; i < 16; ++i) r = r + *reinterpret_cast<const T*>(base + (i >> 3) * BM_TILE_PITCH + (i & 7) * 64);
+        T t = r;
+        t = t + warp_shfl_xor(t, 1);
+        t = t + warp_shfl_xor(t, 2);
+        t = t + warp_shfl_xor(t, 4);     // leaf (128)
+        t = t + warp_shfl_xor(t, 8);     // 256
+        t = t + warp_shfl_xor(t, 16);    // 512
+        return t;
+    }
+}
+
+// one warp-cooperative half-unit: 8 rows x (32 lanes x 16 B)
 template <typename T, bool VEC, class S>
-__device__ __forceinline__ T pw_unit(const S& s, i64 off, char* tile) {
+__device__ __forceinline__ T pw_half(const S& s, i64 off, char* tile) {
     constexpr int V = 16 / sizeof(T);
     constexpr int W = 32 * V;
     const int lane = threadIdx.x & 31;
-    constexpr int UNR = BM_UNIT_UNROLL;
-    for (int r0 = 0; r0 < 16; r0 += UNR) {
+    constexpr int UNR = BM_UNIT_UNROLL < 8 ? BM_UNIT_UNROLL : 8;
+#pragma unroll
+    for (int r0 = 0; r0 < 8; r0 += UNR) {
         T v[UNR][V];
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
@@ -163,62 +220,20 @@ __device__ __forceinline__ T pw_unit(const S& s, i64 off, char* tile) {
             *reinterpret_cast<uint4*>(tile + (r0 + u) * BM_TILE_PITCH + lane * 16) = *reinterpret_cast<const uint4*>(v[u]);
     }
     __syncwarp();
-    T res;
-    if (sizeof(T) == 4) {
-        // lane = 2*chunk + half; accumulators 4*half .. 4*half+3
-        const int c = lane >> 1, h = lane & 1;
-        const char* base = tile + c * BM_TILE_PITCH + h * 16;
-        uint4 q = *reinterpret_cast<const uint4*>(base);
-        T r0 = reinterpret_cast<const T*>(&q)[0], r1 = reinterpret_cast<const T*>(&q)[1];
-        T r2 = reinterpret_cast<const T*>(&q)[2], r3 = reinterpret_cast<const T*>(&q)[3];
-#pragma unroll
-        for (int i = 1; i < 16; ++i) {
-            q = *reinterpret_cast<const uint4*>(base + i * 32);
-            r0 = r0 + reinterpret_cast<const T*>(&q)[0];
-            r1 = r1 + reinterpret_cast<const T*>(&q)[1];
-            r2 = r2 + reinterpret_cast<const T*>(&q)[2];
-            r3 = r3 + reinterpret_cast<const T*>(&q)[3];
-        }
-        const T sh = (r0 + r1) + (r2 + r3);
-        T ch = sh + warp_shfl_xor(sh, 1);
-        ch = ch + warp_shfl_xor(ch, 2);
-        ch = ch + warp_shfl_xor(ch, 4);
-        ch = ch + warp_shfl_xor(ch, 8);
-        ch = ch + warp_shfl_xor(ch, 16);
-        res = ch;
-    } else {
-        // lane = 4*chunk + quarter; accumulators 2*quarter, 2*quarter+1
-        const int c = lane >> 2, qq = lane & 3;
-        T r0 = 0, r1 = 0;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            const uint4 q = *reinterpret_cast<const uint4*>(tile + (2 * c + (i >> 3)) * BM_TILE_PITCH + (i & 7) * 64 + qq * 16);
-            const T x0 = reinterpret_cast<const T*>(&q)[0], x1 = reinterpret_cast<const T*>(&q)[1];
-            if (i == 0) { r0 = x0; r1 = x1; } else { r0 = r0 + x0; r1 = r1 + x1; }
-        }
-        T t = r0 + r1;
-        t = t + warp_shfl_xor(t, 1);
-        t = t + warp_shfl_xor(t, 2);
-        t = t + warp_shfl_xor(t, 4);
-        t = t + warp_shfl_xor(t, 8);
-        t = t + warp_shfl_xor(t, 16);
-        res = t;
-    }
+    const T res = pw_half_tile<T>(tile);
     __syncwarp();
     return res;
 }
 
-template <typename T> struct PwUnit { static const int value = 32 * 16 * (16 / sizeof(T)); };
-
-// balanced pairwise tree over `count` = 2^k consecutive units
+// balanced pairwise tree over `count` = 2^k consecutive half-units
 template <typename T, class S>
 __device__ T pw_balanced(const S& s, i64 off, i64 count, char* tile, bool vec_ok) {
-    constexpr i64 U = PwUnit<T>::value;
+    constexpr i64 U = PwHalf<T>::value;
     T stk[24];
     int lvl[24];
     int sp = 0;
     for (i64 u = 0; u < count; ++u) {
-        T v = vec_ok ? pw_unit<T, true>(s, off + u * U, tile) : pw_unit<T, false>(s, off + u * U, tile);
+        T v = vec_ok ? pw_half<T, true>(s, off + u * U, tile) : pw_half<T, false>(s, off + u * U, tile);
         int l = 0;
         while (sp > 0 && lvl[sp - 1] == l) { v = stk[sp - 1] + v; --sp; ++l; }
         stk[sp] = v; lvl[sp] = l; ++sp;
@@ -255,7 +270,7 @@ __device__ __forceinline__ T pw_leaf(const S& s, i64 off, i64 n) {
 // take the coalesced fast path.  Warp-uniform control flow.
 template <typename T, class S>
 __device__ __noinline__ T pw_generic(const S& s, i64 off, i64 n, char* tile, bool vec_ok) {
-    constexpr i64 U = PwUnit<T>::value;
+    constexpr i64 U = PwHalf<T>::value;
     if (n <= 128) return pw_leaf<T>(s, off, n);
     i64 f_off[48], f_n[48];
     int f_state[48];  // 0 = unvisited, 1 = left pending, 2 = right pending
@@ -307,7 +322,7 @@ __device__ __noinline__ T pw_generic(const S& s, i64 off, i64 n, char* tile, boo
 template <typename T, class S>
 __device__ __forceinline__ T block_accu(const S& s, i64 off, i64 len, char* tile, bool vec_ok) {
     if constexpr (is_float_t<T>::value) {
-        if (len == BM_REDUCE_BLOCK) return pw_balanced<T>(s, off, BM_REDUCE_BLOCK / PwUnit<T>::value, tile, vec_ok);
+        if (len == BM_REDUCE_BLOCK) return pw_balanced<T>(s, off, BM_REDUCE_BLOCK / PwHalf<T>::value, tile, vec_ok);
         return pw_generic<T>(s, off, len, tile, vec_ok);
     } else {
         // integers wrap: any summation order gives the same bits
@@ -451,72 +466,177 @@ __device__ __forceinline__ A stream_pairwise(i64 count, const G& get) {
     return v;
 }
 
-template <typename T, int OP, class S>
-__device__ __forceinline__ void reduce_item_store(const Args& a, const S& s, i64 item, i64 off, i64 len, char* tile,
-                                                  bool vec_ok, bool unit) {
-    typedef typename DotAcc<T>::type DA;
+// combine_pairwise (kernels.py:380-392) over n <= 256 values in shared memory,
+// level by level in place (pairs, odd element carried), by one warp; the
+// result is returned in every lane.
+template <typename A, int OP>
+__device__ __forceinline__ A warp_combine_pairwise(A* t, int n) {
     const int lane = threadIdx.x & 31;
-    if constexpr (OP == 4) {
-        const DA v = block_dot<T>(s, off, len, vec_ok);
-        if (lane == 0) reinterpret_cast<DA*>(a.partials)[item] = v;
-    } else if constexpr (OP == 2 || OP == 3) {
-        const T v = block_minmax<T, OP == 3>(s, off, len, vec_ok);
-        if (lane == 0) reinterpret_cast<T*>(a.partials)[item] = v;
-    } else {
-        T v;
-        if constexpr (is_float_t<T>::value) {
-            if (unit) v = vec_ok ? pw_unit<T, true>(s, off, tile) : pw_unit<T, false>(s, off, tile);
-            else v = block_accu<T>(s, off, len, tile, vec_ok);
-        } else {
-            v = block_accu<T>(s, off, len, tile, vec_ok);
+    while (n > 1) {
+        const int half = n >> 1;
+        A r[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int i = lane + 32 * j;
+            if (i < half) r[j] = Fold<A, OP>::blocks(t[2 * i], t[2 * i + 1]);
         }
-        if (lane == 0) reinterpret_cast<T*>(a.partials)[item] = v;
+        const A carry = t[n - 1];
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int i = lane + 32 * j;
+            if (i < half) t[i] = r[j];
+        }
+        if ((n & 1) && lane == 0) t[half] = carry;
+        __syncwarp();
+        n = half + (n & 1);
+    }
+    return t[0];
+}
+
+// combine_pairwise (kernels.py:380-392) over `cnt` values in shared memory,
+// executed by the whole CTA; the result is valid in thread 0.
+// combine_pairwise of n values equals the right-nested fold of balanced trees
+// over the binary segments of n, so: every aligned group of
+// 256 values is a balanced subtree folded by one warp (8 values per lane in
+// registers, then a shuffle butterfly that keeps left/right operand order),
+// the ragged tail (< 256 values) is folded level by level by one warp, and
+// one warp folds the group values plus the tail value the same way (the
+// tail is innermost, exactly like an appended leaf).  Two barriers instead
+// of one per level.
+// `scratch` holds at least cnt / 256 + 1 values; cnt <= 65535.
+template <typename A, int OP>
+__device__ A cta_fold_pairwise(A* v, A* scratch, int cnt) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int G = cnt >> 8, tail = cnt & 255;
+    for (int g = warp; g < G; g += nw) {
+        const A* p = v + g * 256 + lane * 8;
+        A x[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = p[k];
+        const A b0 = Fold<A, OP>::blocks(Fold<A, OP>::blocks(x[0], x[1]), Fold<A, OP>::blocks(x[2], x[3]));
+        const A b1 = Fold<A, OP>::blocks(Fold<A, OP>::blocks(x[4], x[5]), Fold<A, OP>::blocks(x[6], x[7]));
+        A c = Fold<A, OP>::blocks(b0, b1);
+#pragma unroll
+        for (int m = 1; m < 32; m <<= 1) {
+            const A o = warp_shfl_xor(c, m);
+            c = (lane & m) ? Fold<A, OP>::blocks(o, c) : Fold<A, OP>::blocks(c, o);
+        }
+        if (lane == 0) scratch[g] = c;
+    }
+    if (tail && warp == nw - 1) {
+        const A tv = warp_combine_pairwise<A, OP>(v + G * 256, tail);
+        if (lane == 0) scratch[G] = tv;
+    }
+    __syncthreads();
+    A res = A(0);
+    if (warp == 0) res = warp_combine_pairwise<A, OP>(scratch, G + (tail ? 1 : 0));
+    __syncthreads();
+    return res;
+}
+
+// Block values of blocks [c0, c0 + cn) into buf.  Block mode: the item
+// partials are the block values.  Unit mode: numpy's balanced tree over each
+// block's UPB half-unit partials (kernels.py:459-460 via ndarray.sum), read
+// with coalesced 16-B loads -- a vector holds VP consecutive partials of one
+// block and the VPB lanes holding one block combine by shuffles (left/right
+// operand order kept).  The ragged tail block is the last item partial.
+// Executed by the whole CTA; the caller synchronises before reading buf.
+template <typename P, int OP, int UPB>
+__device__ __forceinline__ void stage_block_values(const P* parts, i64 c0, int cn, i64 nfull, i64 nitems,
+                                                   bool unit_mode, P* buf) {
+    if (!unit_mode) {
+        for (int i = threadIdx.x; i < cn; i += blockDim.x) buf[i] = __ldcg(parts + (c0 + i));
+        return;
+    }
+    constexpr int VP = 16 / (int)sizeof(P);
+    constexpr int VPB = UPB / VP;
+    static_assert(VPB >= 1 && VPB <= 32 && (32 % VPB) == 0, "block vectors must tile a warp");
+    const int lane = threadIdx.x & 31;
+    const i64 full_end = (c0 + cn < nfull) ? c0 + cn : nfull;
+    const int nvec = full_end > c0 ? (int)((full_end - c0) * VPB) : 0;
+    const uint4* pv = reinterpret_cast<const uint4*>(parts + c0 * UPB);
+    constexpr int BATCH = 4;
+    for (int base = 0; base < nvec; base += BATCH * (int)blockDim.x) {
+        uint4 q[BATCH];
+#pragma unroll
+        for (int k = 0; k < BATCH; ++k) {
+            const int j = base + (int)threadIdx.x + k * (int)blockDim.x;
+            if (j < nvec) q[k] = __ldcg(pv + j);
+        }
+#pragma unroll
+        for (int k = 0; k < BATCH; ++k) {
+            const int j = base + (int)threadIdx.x + k * (int)blockDim.x;
+            const P* t = reinterpret_cast<const P*>(&q[k]);
+            P x;
+            if constexpr (VP == 4) {
+                x = Fold<P, OP>::units(Fold<P, OP>::units(t[0], t[1]), Fold<P, OP>::units(t[2], t[3]));
+            } else {
+                x = Fold<P, OP>::units(t[0], t[1]);
+            }
+#pragma unroll
+            for (int m = 1; m < VPB; m <<= 1) {
+                const P o = warp_shfl_xor(x, m);
+                x = (lane & m) ? Fold<P, OP>::units(o, x) : Fold<P, OP>::units(x, o);
+            }
+            if (j < nvec && (lane % VPB) == 0) buf[j / VPB] = x;
+        }
+    }
+    if (threadIdx.x == 0 && nfull >= c0 && nfull < c0 + cn && nitems > nfull * UPB) buf[nfull - c0] = __ldcg(parts + (nitems - 1));
+}
+
+// partial of one work item (a half-unit, a block or the ragged tail block),
+// valid in every lane
+template <typename T, int OP, class S>
+__device__ __forceinline__ typename cond_t<OP == 4, typename DotAcc<T>::type, T>::type reduce_item(
+    const S& s, i64 off, i64 len, char* tile, bool vec_ok, bool unit) {
+    if constexpr (OP == 4) {
+        return block_dot<T>(s, off, len, vec_ok);
+    } else if constexpr (OP == 2 || OP == 3) {
+        return block_minmax<T, OP == 3>(s, off, len, vec_ok);
+    } else {
+        if constexpr (is_float_t<T>::value) {
+            if (unit) return vec_ok ? pw_half<T, true>(s, off, tile) : pw_half<T, false>(s, off, tile);
+        }
+        return block_accu<T>(s, off, len, tile, vec_ok);
     }
 }
 
-template <typename T, int OP, class S>
-__device__ void reduce_flat(const Args& a, const S& s) {
+// Last-CTA fold of the item partials (ticket): unit partials -> block
+// partials with numpy's balanced tree (UPB items per block), then the blocks
+// with combine_pairwise.
+template <typename T, int OP, int UPB>
+__device__ void last_cta_fold(const Args& a, i64 nitems, i64 nfull, bool has_tail, bool unit_mode) {
     typedef typename DotAcc<T>::type DA;
     typedef typename cond_t<OP == 4, DA, T>::type P;   // partial type
     extern __shared__ __align__(16) char smem[];
-    const int nw = blockDim.x >> 5;
-    const int warp = threadIdx.x >> 5;
-    char* tile = smem + warp * BM_TILE_BYTES;
-    const bool vec_ok = a.vec_ok != 0;
-    const bool unit_mode = a.group != 0;          // group != 0: unit mode
-    constexpr i64 UE = PwUnit<T>::value;          // elements per unit
-    constexpr int UPB = BM_REDUCE_BLOCK / UE;     // units per block
-    const i64 nfull = a.n / BM_REDUCE_BLOCK;      // full blocks
-    const i64 tail = a.n - nfull * BM_REDUCE_BLOCK;
-    const i64 nitems_full = unit_mode ? nfull * UPB : nfull;
-    const i64 nitems = nitems_full + (tail ? 1 : 0);
-    // CTA c owns the contiguous item range [c*q + min(c, r), ...) (q, r: quotient
-    // and remainder of nitems / grid), its warps take the range round-robin
-    const i64 q = nitems / gridDim.x, rem = nitems % gridDim.x;
-    const i64 first = (i64)blockIdx.x * q + ((i64)blockIdx.x < rem ? blockIdx.x : rem);
-    const i64 cnt = q + ((i64)blockIdx.x < rem ? 1 : 0);
-    for (i64 k = warp; k < cnt; k += nw) {
-        const i64 item = first + k;
-        if (item < nitems_full) {
-            const i64 off = item * (unit_mode ? UE : BM_REDUCE_BLOCK);
-            reduce_item_store<T, OP>(a, s, item, off, unit_mode ? UE : BM_REDUCE_BLOCK, tile, vec_ok, unit_mode);
-        } else {
-            reduce_item_store<T, OP>(a, s, item, nfull * BM_REDUCE_BLOCK, tail, tile, vec_ok, false);
-        }
-    }
-    if (a.ext_fold) return;   // large reductions: folded by fold_chunks_kernel / fold_final_kernel
+    const i64 tail = has_tail ? 1 : 0;
+    // Ticket: the barrier orders the CTA's partial stores before thread 0's
+    // gpu-scope release (cumulative), the acq_rel atomic makes every CTA's
+    // partials visible to the last one.  One fence per CTA, not per thread:
+    // this sits on the critical path after the slowest CTA.  a.ticket[0] is
+    // the ticket, a.ticket[1] the dynamic item counter; the last CTA resets both.
     __shared__ bool am_last;
-    __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) am_last = (atomicAdd(a.ticket, 1u) == gridDim.x - 1);
+    BM_TRACE(0);
+    if (threadIdx.x == 0) {
+        unsigned prev;
+        asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(a.ticket) : "memory");
+        am_last = (prev == gridDim.x - 1);
+    }
     __syncthreads();
     if (!am_last) return;
-    __threadfence();
+    if (a.ext_fold) {   // large reductions: folded by fold_chunks_kernel / fold_final_kernel
+        if (threadIdx.x == 0) { a.ticket[0] = 0u; a.ticket[1] = 0u; }
+        return;
+    }
+    BM_TRACE(1);
     // ---- final fold (last CTA) ----
     // Block partials are staged into shared memory with coalesced, independent
     // loads (all threads), one aligned power-of-two chunk of blocks at a time,
     // folded there with combine_pairwise; chunk results fold the same way.
-    const volatile P* parts = reinterpret_cast<const volatile P*>(a.partials);
+    // (L2 loads, ordered after the other CTAs' stores by the acquire above)
+    const P* parts = reinterpret_cast<const P*>(a.partials);
     const i64 nblocks = nfull + (tail ? 1 : 0);
     const int smem_vals = (int)(a.smem_bytes / sizeof(P));
     int chunk = 1;
@@ -530,27 +650,11 @@ __device__ void reduce_flat(const Args& a, const S& s) {
     for (i64 ck = 0; ck < nchunks; ++ck) {
         const i64 c0 = ck * chunk;
         const int cn = (int)((nblocks - c0) < chunk ? (nblocks - c0) : chunk);
-        if (unit_mode) {
-            for (int i = threadIdx.x; i < cn; i += blockDim.x) {
-                const i64 b = c0 + i;
-                if (b == nfull) {
-                    buf[i] = parts[nitems - 1];
-                } else {
-                    P v[UPB];
-#pragma unroll
-                    for (int u = 0; u < UPB; ++u) v[u] = parts[b * UPB + u];
-#pragma unroll
-                    for (int w = 1; w < UPB; w <<= 1)
-#pragma unroll
-                        for (int u = 0; u + w < UPB; u += 2 * w) v[u] = Fold<P, OP>::units(v[u], v[u + w]);
-                    buf[i] = v[0];
-                }
-            }
-        } else {
-            for (int i = threadIdx.x; i < cn; i += blockDim.x) buf[i] = parts[c0 + i];
-        }
+        stage_block_values<P, OP, UPB>(parts, c0, cn, nfull, nitems, unit_mode, buf);
         __syncthreads();
-        const P cr = cta_combine_pairwise<P, OP>(buf, buf2, cn);
+        BM_TRACE(2);
+        const P cr = cta_fold_pairwise<P, OP>(buf, buf2, cn);
+        BM_TRACE(3);
         if (threadIdx.x == 0) chunk_res[ck] = cr;     // host guarantees nchunks <= 1024
         __syncthreads();
     }
@@ -562,8 +666,62 @@ __device__ void reduce_flat(const Args& a, const S& s) {
         P fin = r;
         if constexpr (OP == 1 && is_float_t<T>::value) fin = r + T(0);  // numpy: 0 + pairwise(...) (-0 -> +0)
         reinterpret_cast<P*>(a.result)[0] = fin;
-        *a.ticket = 0u;
+        a.ticket[0] = 0u;
+        a.ticket[1] = 0u;
     }
+    BM_TRACE(4);
+}
+
+template <typename T, int OP, class S>
+__device__ void reduce_flat(const Args& a, const S& s) {
+    typedef typename DotAcc<T>::type DA;
+    typedef typename cond_t<OP == 4, DA, T>::type P;   // partial type
+    extern __shared__ __align__(16) char smem[];
+    const int nw = blockDim.x >> 5;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    char* tile = smem + warp * BM_TILE_BYTES;
+    const bool vec_ok = a.vec_ok != 0;
+    const bool unit_mode = a.group != 0;          // group != 0: unit mode
+    constexpr i64 UE = PwHalf<T>::value;          // elements per unit-mode item (half-unit)
+    constexpr int UPB = BM_REDUCE_BLOCK / UE;     // items per block
+    const i64 nfull = a.n / BM_REDUCE_BLOCK;      // full blocks
+    const i64 tail = a.n - nfull * BM_REDUCE_BLOCK;
+    const i64 nitems_full = unit_mode ? nfull * UPB : nfull;
+    const i64 nitems = nitems_full + (tail ? 1 : 0);
+    P* parts = reinterpret_cast<P*>(a.partials);
+    // Dynamic item scheduling: a warp takes `grab` consecutive items at a
+    // time; its first run is static, the rest come from a global counter,
+    // fetched one run ahead so the atomic's latency hides behind the current
+    // run.  A CTA that starts late (its SM still folding the previous
+    // reduction) simply takes fewer runs.  `grab` keeps the counter below
+    // about one atomic per 2 ns for light items (one input).
+    const i64 G = a.grab > 0 ? a.grab : 1;
+    const i64 nwarps_total = (i64)gridDim.x * nw;
+    i64 run = (i64)blockIdx.x * nw + warp;
+    while (run * G < nitems) {
+        unsigned nxt = 0;
+        if (lane == 0) nxt = atomicAdd(a.ticket + 1, 1u);
+        const i64 i_end = (run + 1) * G < nitems ? (run + 1) * G : nitems;
+        for (i64 item = run * G; item < i_end; ++item) {
+            P v;
+            if (item < nitems_full) {
+                const i64 off = item * (unit_mode ? UE : BM_REDUCE_BLOCK);
+                v = reduce_item<T, OP>(s, off, unit_mode ? UE : BM_REDUCE_BLOCK, tile, vec_ok, unit_mode);
+            } else {
+                v = reduce_item<T, OP>(s, nfull * BM_REDUCE_BLOCK, tail, tile, vec_ok, false);
+            }
+            if (lane == 0) parts[item] = v;
+        }
+        run = nwarps_total + (i64)__shfl_sync(0xffffffffu, nxt, 0);
+    }
+    // Programmatic dependent launch (bm_jit.cu launch_reduce): everything
+    // above only read this launch's inputs and wrote this launch's scratch;
+    // wait for the predecessor to complete before the ticket (the scratch
+    // of the launch before that is this one's), then let the successor start
+    // on the SMs this grid frees while its last CTA folds.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    last_cta_fold<T, OP, UPB>(a, nitems, nfull, tail != 0, unit_mode);
 }
 
 // ---------------------------------------------------------------------------
@@ -581,25 +739,9 @@ __global__ void __launch_bounds__(512) fold_chunks_kernel(const P* __restrict__ 
     const i64 nblocks = nfull + (nitems > (unit_mode ? nfull * UPB : nfull) ? 1 : 0);
     const i64 c0 = (i64)blockIdx.x * chunk;
     const int cn = (int)((nblocks - c0) < chunk ? (nblocks - c0) : chunk);
-    for (int i = threadIdx.x; i < cn; i += blockDim.x) {
-        const i64 b = c0 + i;
-        if (b == nfull) {
-            buf[i] = parts[nitems - 1];
-        } else if (unit_mode) {
-            P v[UPB];
-#pragma unroll
-            for (int u = 0; u < UPB; ++u) v[u] = parts[b * UPB + u];
-#pragma unroll
-            for (int w = 1; w < UPB; w <<= 1)
-#pragma unroll
-                for (int u = 0; u + w < UPB; u += 2 * w) v[u] = Fold<P, OP>::units(v[u], v[u + w]);
-            buf[i] = v[0];
-        } else {
-            buf[i] = parts[b];
-        }
-    }
+    stage_block_values<P, OP, UPB>(parts, c0, cn, nfull, nitems, unit_mode != 0, buf);
     __syncthreads();
-    const P r = cta_combine_pairwise<P, OP>(buf, buf2, cn);
+    const P r = cta_fold_pairwise<P, OP>(buf, buf2, cn);
     if (threadIdx.x == 0) out[blockIdx.x] = r;
 }
 

@@ -59,7 +59,9 @@ int load_driver() {
     BM_GET(cuModuleLoadData, moduleLoadData);
     BM_GET(cuModuleGetFunction, moduleGetFunction);
     BM_GET(cuLaunchKernel, launchKernel);
+    BM_GET(cuLaunchKernelEx, launchKernelEx);
     BM_GET(cuFuncSetAttribute, funcSetAttribute);
+    BM_GET(cuFuncGetAttribute, funcGetAttribute);
     BM_GET(cuTensorMapEncodeTiled, tensorMapEncodeTiled);
 #undef BM_GET
     d.ok = true;
@@ -109,7 +111,10 @@ int bm_init(int device) {
     BM_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
     uint64_t thr = UINT64_MAX;
     BM_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-    BM_CUDA(cudaMalloc(&s.partials, 8 * 8192));
+    BM_CUDA(cudaMalloc(&s.partials[0], 8 * 8192));
+    BM_CUDA(cudaMalloc(&s.partials[1], 8 * 8192));
+    s.partials_cap = 8192;
+    s.flip = 0;
     BM_CUDA(cudaMalloc(&s.ticket, 256));
     BM_CUDA(cudaMemset(s.ticket, 0, 256));
     BM_CUDA(cudaMalloc(&s.result, 256));
@@ -124,12 +129,14 @@ int bm_shutdown(void) {
     std::lock_guard<std::recursive_mutex> lk(s.mu);
     if (!s.initialised) return BM_OK;
     cudaError_t e = cudaDeviceSynchronize();
-    cudaFree(s.partials);
+    cudaFree(s.partials[0]);
+    cudaFree(s.partials[1]);
     cudaFree(s.ticket);
     cudaFree(s.result);
     cudaFreeHost(s.host_slot);
     cudaStreamDestroy(s.own_stream);
-    s.partials = s.result = s.host_slot = nullptr;
+    s.partials[0] = s.partials[1] = s.result = s.host_slot = nullptr;
+    s.partials_cap = 0;
     s.ticket = nullptr;
     s.own_stream = s.stream = nullptr;
     s.initialised = false;

@@ -189,3 +189,4 @@ def test_strided_and_converted_inputs_compile():
     prog = (("load", 0), ("load", 1), ("glue", "eglue_plus"))
     _compile("fused_chain", [_flat(A, 50, 2), _flat(Bi, 50, 2, 1)], _flat(out, 50), {"program": prog,
                                                                                       "compute_dtype": "<f4"})
+

@@ -1,5 +1,5 @@
 """Run one hot-path workload a few times so ncu can capture its kernel.
-Usage: python tools/profile_targets.py cfg1|gemm_f32|gemm_f64|rdim0|rdim1|dot"""
+Usage: python tools/profile_targets.py cfg1|accu1|gemm_f32|gemm_f64|rdim0|rdim1|dot"""
 import pathlib
 import sys
 
@@ -18,6 +18,11 @@ def main(which: str) -> None:
         A, B, C, D = (dm.Matrix.from_numpy(rng.random((4096, 4096), dtype=np.float32)) for _ in range(4))
         for _ in range(4):
             dm.accu(2 * A + B % C - dm.exp(D))
+    elif which == "accu1":
+        rng = np.random.default_rng(0)
+        A = dm.Matrix.from_numpy(rng.random((4096, 4096), dtype=np.float32))
+        for _ in range(4):
+            dm.accu(A)
     elif which in ("gemm_f32", "gemm_f64"):
         elem = which[-3:]
         n = 8192

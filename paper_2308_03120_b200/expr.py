@@ -534,6 +534,10 @@ class _Lowerer:
                 prog.stages.append(("unary", node.kind, node.aux[0] if node.aux else None))
 
         walk(root)
+        # `walk` refers to itself through its closure cell: clear the cell so
+        # that the program's operands (device matrices) are released by
+        # reference counting, not at the next garbage-collector pass
+        walk = None  # noqa: F841
         return prog
 
     def _fit_program(self, root: ExprNode, elem: str, extra_slots: int = 0) -> _Program:

@@ -285,3 +285,32 @@ def test_large_reductions_external_fold(dm):
     assert rel_err(dm.dot(mv, mw), O.reduce_dot(v, w)) <= 1e-5
     vd = v[: 1 << 27].astype(np.float64)
     same(np.float64(dm.accu(dm.Matrix.from_numpy(vd.reshape(-1, 1)))), O.reduce_accu(vd))
+
+
+def test_back_to_back_reductions_stay_ordered_with_stores(dm):
+    """Reductions launch as programmatic dependents (PDL) and overlap their
+    predecessor's final fold.  Interleave stores that rewrite the reduced
+    matrix with device-resident reductions and no host synchronisation: every
+    reduction must see exactly the store before it, and consecutive
+    reductions must not corrupt each other's scratch."""
+    import torch
+    from paper_2308_03120_b200 import dist as D
+    D.bind_torch_stream()   # torch's partial tensors and the kernels on one stream
+    n = 2048
+    base = np.random.default_rng(3).random((n, n), dtype=np.float32)
+    A = dm.Matrix.from_numpy(base)
+    X = dm.Matrix(n, n)
+    reds = []
+    for k in range(24):
+        dm.evaluate(A * float(k + 1), out=X)
+        r = D.ShardedReduction("accu", X)
+        r.launch()
+        r2 = D.ShardedReduction("accu", A * float(k + 1) + 1.0)   # back-to-back reduction, no store between
+        r2.launch()
+        reds.append((k, r, r2))
+    torch.cuda.synchronize()
+    flat = base.reshape(-1, order="F")
+    for k, r, r2 in reds:
+        scaled = (flat * np.float32(k + 1)).astype(np.float32)
+        same(np.float32(r.partial.cpu().numpy()[0]), O.reduce_accu(scaled))
+        same(np.float32(r2.partial.cpu().numpy()[0]), O.reduce_accu((scaled + np.float32(1)).astype(np.float32)))

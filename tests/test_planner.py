@@ -190,3 +190,25 @@ def test_strided_and_converted_inputs_compile():
     _compile("fused_chain", [_flat(A, 50, 2), _flat(Bi, 50, 2, 1)], _flat(out, 50), {"program": prog,
                                                                                       "compute_dtype": "<f4"})
 
+
+
+def test_planning_leaves_no_reference_cycles():
+    """Plans must not keep operands alive until a GC pass: device matrices
+    are released by reference counting (a cycle here made every e2e step
+    allocate fresh pool memory)."""
+    import gc
+    gc.collect()
+    gc.set_debug(gc.DEBUG_SAVEALL)
+    try:
+        e = 2 * leaf(64, 64) + leaf(64, 64) % leaf(64, 64) - dm.exp(leaf(64, 64))
+        p = expr.plan_reduce("accu", e)
+        del p
+        p = expr.plan(e)
+        del p, e
+        g = leaf(64, 64) @ leaf(64, 64).t()
+        p = expr.plan(g)
+        del p, g
+        assert gc.collect() == 0, [type(o).__name__ for o in gc.garbage][:20]
+    finally:
+        gc.set_debug(0)
+        gc.garbage.clear()

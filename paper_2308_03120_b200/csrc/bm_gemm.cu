@@ -122,6 +122,117 @@ __global__ void gemv_t_finish_kernel(const typename DotAcc<T>::type* __restrict_
     y[i * incy] = cvt<T>(acc);
 }
 
+// --- vectorised GEMVs (16-B loads, several KB in flight per warp) ---------
+//
+// gemv_n_vec: y = A x with A column-major m x k.  A CTA owns RB = 32*V rows
+// (one 16-B vector of V rows per lane) and its 8 warps split the k columns
+// into 8 contiguous slices; every lane keeps V f64 accumulators (fma, fixed
+// order), the slices are added in warp order through shared memory.  Each
+// warp has UNR column vectors (UNR x 512 B) in flight.
+template <typename T, int UNR>
+__global__ void __launch_bounds__(256) gemv_n_vec_kernel(const T* __restrict__ A, i64 lda, const T* __restrict__ x,
+                                                         i64 incx, T* __restrict__ y, i64 incy, i64 m, i64 k) {
+    typedef typename DotAcc<T>::type Acc;
+    constexpr int V = 16 / sizeof(T);
+    constexpr int RB = 32 * V;
+    __shared__ Acc red[8][RB];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const i64 row0 = (i64)blockIdx.x * RB + lane * V;
+    const i64 per = (k + 7) / 8;
+    const i64 l0 = warp * per;
+    const i64 l1 = (l0 + per < k) ? l0 + per : k;
+    Acc acc[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc[v] = 0;
+    if (row0 + V <= m) {
+        i64 l = l0;
+        for (; l + UNR <= l1; l += UNR) {
+            uint4 q[UNR];
+            T xv[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                q[u] = __ldcs(reinterpret_cast<const uint4*>(A + row0 + (l + u) * lda));
+                xv[u] = x[(l + u) * incx];
+            }
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const T* t = reinterpret_cast<const T*>(&q[u]);
+#pragma unroll
+                for (int v = 0; v < V; ++v) acc[v] = fma((Acc)t[v], (Acc)xv[u], acc[v]);
+            }
+        }
+        for (; l < l1; ++l) {
+            const uint4 q = __ldcs(reinterpret_cast<const uint4*>(A + row0 + l * lda));
+            const T* t = reinterpret_cast<const T*>(&q);
+            const Acc xl = (Acc)x[l * incx];
+#pragma unroll
+            for (int v = 0; v < V; ++v) acc[v] = fma((Acc)t[v], xl, acc[v]);
+        }
+    } else {
+        for (i64 l = l0; l < l1; ++l) {
+            const Acc xl = (Acc)x[l * incx];
+#pragma unroll
+            for (int v = 0; v < V; ++v)
+                if (row0 + v < m) acc[v] = fma((Acc)A[row0 + v + l * lda], xl, acc[v]);
+        }
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) red[warp][lane * V + v] = acc[v];
+    __syncthreads();
+    for (int r = threadIdx.x; r < RB; r += blockDim.x) {
+        const i64 gi = (i64)blockIdx.x * RB + r;
+        if (gi >= m) continue;
+        Acc sum = red[0][r];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) sum = sum + red[w][r];
+        y[gi * incy] = cvt<T>(sum);
+    }
+}
+
+// gemv_t_vec partials: part[s][j] = sum over rows [s*S, (s+1)*S) of
+// A[l + j*lda] x[l] (A column-major, column j contiguous).  One warp per
+// (column, slice), 16-B loads of both A and x (x stays in L2), UNR vectors
+// in flight per lane, f64 fma per lane then a shuffle tree.
+template <typename T, int UNR>
+__global__ void __launch_bounds__(256) gemv_t_vec_kernel(const T* __restrict__ A, i64 lda, const T* __restrict__ x,
+                                                         typename DotAcc<T>::type* __restrict__ part, i64 ncols,
+                                                         i64 nrows, i64 S) {
+    typedef typename DotAcc<T>::type Acc;
+    constexpr int V = 16 / sizeof(T);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const i64 j = (i64)blockIdx.x * 8 + warp;
+    if (j >= ncols) return;
+    const i64 r0 = (i64)blockIdx.y * S;
+    const i64 r1 = (r0 + S < nrows) ? r0 + S : nrows;
+    const T* col = A + j * lda;
+    Acc acc = 0;
+    i64 l = r0 + lane * V;
+    constexpr i64 STEP = 32 * V;
+    for (; l + (UNR - 1) * STEP + V <= r1; l += UNR * STEP) {
+        uint4 qa[UNR], qx[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            qa[u] = __ldcs(reinterpret_cast<const uint4*>(col + l + u * STEP));
+            qx[u] = __ldg(reinterpret_cast<const uint4*>(x + l + u * STEP));
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const T* ta = reinterpret_cast<const T*>(&qa[u]);
+            const T* tx = reinterpret_cast<const T*>(&qx[u]);
+#pragma unroll
+            for (int v = 0; v < V; ++v) acc = fma((Acc)ta[v], (Acc)tx[v], acc);
+        }
+    }
+    for (; l < r1; l += STEP) {
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+            if (l + v < r1) acc = fma((Acc)col[l + v], (Acc)x[l + v], acc);
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) acc = acc + warp_shfl_xor(acc, o);
+    if (lane == 0) part[(i64)blockIdx.y * ncols + j] = acc;
+}
+
 }  // namespace bm
 
 namespace bmi {
@@ -132,6 +243,34 @@ static int gemv(bool ta, int64_t m, int64_t k, const T* A, int64_t lda, const T*
                 int64_t incy) {
     typedef typename bm::DotAcc<T>::type Acc;
     cudaStream_t s = st().stream;
+    constexpr int V = 16 / sizeof(T);
+    const bool a_vec = ((uintptr_t)A % 16 == 0) && (lda % V == 0);
+    if (!ta && a_vec && m >= 32 * V) {
+        constexpr int RB = 32 * V;
+        bm::gemv_n_vec_kernel<T, 8><<<(unsigned)((m + RB - 1) / RB), 256, 0, s>>>(A, lda, x, incx, y, incy, m, k);
+        BM_CUDA(cudaGetLastError());
+        st().launches++;
+        return BM_OK;
+    }
+    if (ta && a_vec && incx == 1 && (uintptr_t)x % 16 == 0 && k >= 32 * V * 8) {
+        // op(A) = A^T: m outputs (columns of A), k rows; slices of S rows
+        int64_t S = 16384;
+        while (S > 4096 && m * ((k + S - 1) / S) < 4LL * 148 * 8 * 4) S >>= 1;
+        const int64_t nsplit = (k + S - 1) / S;
+        Acc* part = nullptr;
+        BM_CUDA(cudaMallocAsync((void**)&part, (size_t)(nsplit * m) * sizeof(Acc), s));
+        dim3 grid((unsigned)((m + 7) / 8), (unsigned)nsplit);
+        bm::gemv_t_vec_kernel<T, 4><<<grid, 256, 0, s>>>(A, lda, x, part, m, k, S);
+        cudaError_t e = cudaGetLastError();
+        if (e == cudaSuccess) {
+            bm::gemv_t_finish_kernel<T><<<(unsigned)((m + 255) / 256), 256, 0, s>>>(part, (int)nsplit, y, incy, m);
+            e = cudaGetLastError();
+        }
+        cudaFreeAsync(part, s);
+        if (e != cudaSuccess) return cuda_fail(e, "gemv");
+        st().launches += 2;
+        return BM_OK;
+    }
     if (!ta) {
         bm::gemv_n_kernel<T><<<(unsigned)((m + 255) / 256), 256, 0, s>>>(A, lda, x, incx, y, incy, m, k);
         BM_CUDA(cudaGetLastError());

@@ -113,3 +113,92 @@ def sharded_dot(a_local, b_local, group=None):
     r = ShardedReduction("dot", a_local, b_local, group=group)
     r.launch()
     return r.value().item()
+
+
+# ---------------------------------------------------------------------------
+# device buffers as torch tensors (zero copy), for the collectives only
+
+class _CudaArray:
+    """__cuda_array_interface__ over a device buffer (column-major flat)."""
+
+    def __init__(self, ptr: int, count: int, elem: str):
+        self.__cuda_array_interface__ = {
+            "shape": (count,), "typestr": kernels.NP_DTYPE[elem].str, "data": (ptr, False),
+            "version": 3, "strides": None, "stream": None}
+
+
+def torch_view(m):
+    """The column-major storage of a device matrix as a flat torch tensor
+    sharing its memory (no copy): what NCCL reads and writes."""
+    import torch
+    return torch.as_tensor(_CudaArray(m.mem.ptr, m.n_elem, m.elem_type), device="cuda")
+
+
+def _world(group=None) -> tuple[int, int]:
+    import torch.distributed as dist
+    if not dist.is_initialized():
+        return 0, 1
+    return dist.get_rank(group), dist.get_world_size(group)
+
+
+def broadcast_matrix(m, src: int = 0, group=None):
+    """Replicate a device matrix from rank `src` (config 4: A of A*B^T)."""
+    import torch.distributed as dist
+    if _world(group)[1] > 1:
+        dist.broadcast(torch_view(m), src, group=group)
+    return m
+
+
+def gather_columns(local, group=None):
+    """All-gather one rows x 1 partial per rank into a rows x world matrix,
+    column r = rank r's partial (column-major: a column is contiguous, so the
+    NCCL all-gather writes each rank's block in place)."""
+    import torch.distributed as dist
+    from .matrix import Matrix
+    rank, world = _world(group)
+    if world == 1:
+        return local
+    out = Matrix(local.n_elem, world, elem_type=local.elem_type)
+    dist.all_gather_into_tensor(torch_view(out), torch_view(local), group=group)
+    return out
+
+
+def sharded_reduce_dim(op: str, local_expr, dim: int, group=None):
+    """sum/min/max along `dim` of a column-block-sharded matrix.
+
+    dim 0 (one value per column): every rank owns its columns' results, no
+    communication.  dim 1 (one value per row): each rank reduces its columns
+    to a rows x 1 partial, the partials are all-gathered in rank order and
+    folded with the same device reduction along dim 1 -- a left-to-right fold
+    0 + p_0 + p_1 + ..., deterministic for a given world size (min/max are
+    exact).  Returns the local dim-0 block or the full dim-1 column."""
+    from . import ops
+    fn = {"sum": ops.sum, "min": ops.min, "max": ops.max}[op]
+    local = _expr.evaluate(fn(local_expr, dim))
+    if dim == 0 or _world(group)[1] == 1:
+        return local
+    return _expr.evaluate(fn(gather_columns(local, group), 1))
+
+
+def sharded_gemm_nt(a, b_local):
+    """C = A * B^T sharded over the rows of B (= the columns of C): rank r
+    holds B's row block r and A replicated (broadcast_matrix), and computes
+    its column block of C with no communication."""
+    return _expr.evaluate(a @ b_local.t())
+
+
+def sharded_logistic_step(x_local, w, y_local, group=None):
+    """One logistic-regression gradient step sharded by samples (row blocks
+    of X): z = X_r w, r = 1/(1+exp(-z)) - y_r,
+    g = sum_r X_r^T r_r (one all-gather of a 1024-vector, folded in rank
+    order) and s = accu(r) over all ranks.  Returns (g, s)."""
+    from . import ops
+    z = _expr.evaluate(x_local @ w)
+    r = _expr.evaluate(1 / (1 + ops.exp(0 - z)) - y_local)
+    g_local = _expr.evaluate(x_local.t() @ r)
+    if _world(group)[1] == 1:
+        return g_local, ops.accu(r)
+    g = _expr.evaluate(ops.sum(gather_columns(g_local, group), 1))
+    s = ShardedReduction("accu", r, group=group)
+    s.launch()
+    return g, s.value().item()

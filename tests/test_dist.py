@@ -78,3 +78,114 @@ def test_sharded_reduction_is_bit_identical_to_single_device(rows, cols):
     sharded, single, mx, mx1 = q.get(timeout=10)
     assert sharded == single          # aligned power-of-two block runs per rank
     assert mx == mx1
+
+
+# ---- row reductions, GEMM and the logistic step, sharded ---------------------------
+
+def _spawn(target, world, *args):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=target, args=(r, world, port, q) + args) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=180)
+    assert all(p.exitcode == 0 for p in procs)
+    return q.get(timeout=10)
+
+
+def _gather_columns(local: np.ndarray, world: int) -> np.ndarray:
+    """What dist.gather_columns does on the device: all-gather in rank order
+    into a rows x world column-major matrix (column r = rank r)."""
+    t = torch.from_numpy(np.ascontiguousarray(local.reshape(-1)))
+    out = torch.zeros(world * t.numel(), dtype=t.dtype)
+    dist.all_gather_into_tensor(out, t)
+    return out.numpy().reshape((t.numel(), world), order="F")
+
+
+def _rdim_worker(rank, world, port, q, rows, cols):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        full = np.random.default_rng(4).standard_normal((rows, cols))
+        start, count = column_block(cols, rank, world)
+        local = np.asfortranarray(full[:, start:start + count])
+        res = {}
+        for op in ("sum", "min", "max"):
+            part = O.rdim(op, local, 1).reshape(-1)                    # rows x 1 on this rank
+            gathered = _gather_columns(part, world)                    # rows x world, rank order
+            res[op] = O.rdim(op, gathered, 1).reshape(-1)              # the dim-1 fold of the partials
+            res[op + "_single"] = O.rdim(op, np.asfortranarray(full), 1).reshape(-1)
+            # dim 0: each rank's columns only, no communication
+            res[op + "_dim0_ok"] = bool(np.array_equal(O.rdim(op, local, 0).reshape(-1),
+                                                       O.rdim(op, np.asfortranarray(full), 0).reshape(-1)[start:start + count]))
+        if rank == 0:
+            q.put(res)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_row_reductions_match_single_device():
+    res = _spawn(_rdim_worker, 2, 300, 257)
+    for op in ("sum", "min", "max"):
+        assert res[op + "_dim0_ok"]
+        if op == "sum":
+            np.testing.assert_allclose(res[op], res[op + "_single"], rtol=1e-12)
+        else:
+            assert np.array_equal(res[op], res[op + "_single"])    # min/max are exact
+
+
+def _gemm_worker(rank, world, port, q, m, n, k):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(5)
+        a = rng.random((m, k)) if rank == 0 else np.zeros((m, k))
+        b = np.random.default_rng(6).random((n, k))
+        ta = torch.from_numpy(np.asfortranarray(a).reshape(-1, order="F").copy())
+        dist.broadcast(ta, 0)                                          # broadcast_matrix
+        a = ta.numpy().reshape((m, k), order="F")
+        start, count = column_block(n, rank, world)                    # rows of B = columns of C
+        c_local = a @ b[start:start + count].T                         # sharded_gemm_nt, no communication
+        blocks = [torch.zeros(m * column_block(n, r, world)[1], dtype=torch.float64) for r in range(world)]
+        dist.all_gather(blocks, torch.from_numpy(np.asfortranarray(c_local).reshape(-1, order="F").copy()))
+        if rank == 0:
+            c = np.concatenate([blk.numpy().reshape((m, -1), order="F") for blk in blocks], axis=1)
+            q.put(float(np.abs(c - a @ b.T).max()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_gemm_column_blocks_assemble_the_product():
+    assert _spawn(_gemm_worker, 2, 40, 34, 20) < 1e-12
+
+
+def _logistic_worker(rank, world, port, q, nrow, ncol):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(7)
+        X = rng.standard_normal((nrow, ncol)).astype(np.float32)
+        w = (0.03 * rng.standard_normal((ncol, 1))).astype(np.float32)
+        y = (rng.random((nrow, 1)) < 0.5).astype(np.float32)
+        start, count = column_block(nrow, rank, world)                 # samples = rows of X
+        xl, yl = X[start:start + count], y[start:start + count]
+        r = (1 / (1 + np.exp(-(xl.astype(np.float64) @ w))) - yl).astype(np.float32)
+        g_local = (xl.T.astype(np.float64) @ r).reshape(-1)
+        gathered = _gather_columns(g_local, world)
+        g = O.rdim("sum", gathered, 1).reshape(-1)                     # fold in rank order
+        s_parts = [torch.zeros(1, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(s_parts, torch.tensor([float(r.astype(np.float64).sum())], dtype=torch.float64))
+        if rank == 0:
+            rf = (1 / (1 + np.exp(-(X.astype(np.float64) @ w))) - y)
+            gf = (X.T.astype(np.float64) @ rf).reshape(-1)
+            q.put((float(np.abs(g - gf).max() / np.abs(gf).max()),
+                   abs(sum(p.item() for p in s_parts) - rf.sum()) / max(abs(rf.sum()), 1.0)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_logistic_step_matches_single_device():
+    gerr, serr = _spawn(_logistic_worker, 2, 1000, 64)
+    assert gerr < 1e-6 and serr < 1e-6

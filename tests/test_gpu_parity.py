@@ -314,3 +314,33 @@ def test_back_to_back_reductions_stay_ordered_with_stores(dm):
         scaled = (flat * np.float32(k + 1)).astype(np.float32)
         same(np.float32(r.partial.cpu().numpy()[0]), O.reduce_accu(scaled))
         same(np.float32(r2.partial.cpu().numpy()[0]), O.reduce_accu((scaled + np.float32(1)).astype(np.float32)))
+
+
+def test_sharded_helpers_at_world_size_one(dm):
+    """dist helpers on one GPU (no process group): the zero-copy torch view,
+    dim-0/dim-1 reductions, the NT GEMM block and the logistic step."""
+    import torch
+    from paper_2308_03120_b200 import dist as D
+    D.bind_torch_stream()
+    a = np.random.default_rng(8).random((300, 200))
+    m = dm.Matrix.from_numpy(a)
+    t = D.torch_view(m)
+    assert t.numel() == a.size and t.dtype == torch.float64
+    same(t.cpu().numpy(), np.asfortranarray(a).reshape(-1, order="F"))
+    t.mul_(2.0)
+    torch.cuda.synchronize()
+    same(m.to_numpy(), 2 * a)
+    for op in ("sum", "min", "max"):
+        for dim in (0, 1):
+            same(D.sharded_reduce_dim(op, m, dim).to_numpy(), O.rdim(op, 2 * a, dim))
+    b = np.random.default_rng(9).random((64, 200))
+    c = D.sharded_gemm_nt(m, dm.Matrix.from_numpy(b)).to_numpy()
+    normwise(c, (2 * a) @ b.T, 1e-12)
+    rng = np.random.default_rng(10)
+    X = rng.standard_normal((4096, 256)).astype(np.float32)
+    w = (0.03 * rng.standard_normal((256, 1))).astype(np.float32)
+    y = (rng.random((4096, 1)) < 0.5).astype(np.float32)
+    g, s = D.sharded_logistic_step(dm.Matrix.from_numpy(X), dm.Matrix.from_numpy(w), dm.Matrix.from_numpy(y))
+    rf = 1 / (1 + np.exp(-(X.astype(np.float64) @ w))) - y
+    normwise(g.to_numpy(), X.T.astype(np.float64) @ rf, 1e-5)
+    assert rel_err(s, rf.sum()) <= 1e-5

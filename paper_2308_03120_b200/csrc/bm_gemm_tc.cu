@@ -107,7 +107,7 @@ __host__ __device__ constexpr uint32_t tf32_idesc(int m, int n) {
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
                        const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_blo,
-                       float* __restrict__ C, i64 m, i64 n, i64 ldc, int nk) {
+                       float* __restrict__ C, i64 m, i64 n, i64 ldc, int nk, int group_m) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
@@ -118,7 +118,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m0 = blockIdx.y * TC_BM, n0 = blockIdx.x * TC_BN;
+    // Grouped raster: the linear CTA index walks groups of group_m tile rows
+    // column by column, so the ~148 CTAs resident at a time cover about
+    // group_m x (148 / group_m) tiles and share each A and B slab several ways
+    // through L2 (a plain row raster shares B ~1 way, which
+    // made the 32768^3 product DRAM-bound).
+    int m0, n0;
+    {
+        const int nm = (int)((m + TC_BM - 1) / TC_BM), nn = (int)((n + TC_BN - 1) / TC_BN);
+        const int t = blockIdx.x;
+        const int per_group = group_m * nn;
+        const int g = t / per_group, first_m = g * group_m;
+        const int gsize = (nm - first_m) < group_m ? (nm - first_m) : group_m;
+        const int r = t - g * per_group;
+        m0 = (first_m + r % gsize) * TC_BM;
+        n0 = (r / gsize) * TC_BN;
+    }
     const int nchunks = (nk + TC_CHUNK_KB - 1) / TC_CHUNK_KB;
 
     if (threadIdx.x == 0) {
@@ -398,8 +413,10 @@ int gemm_tc_f32(int ta, int tb, int64_t m, int64_t n, int64_t k, const float* A,
         }
     }
     if (!rc) {
-        dim3 grid((unsigned)(np / TC_BN), (unsigned)(mp / TC_BM));
-        bm::gemm_3xtf32_kernel<<<grid, TC_THREADS, TC_SMEM, s>>>(tm[0], tm[1], tm[2], tm[3], C, m, n, ldc, (int)(kp / TC_BK));
+        dim3 grid((unsigned)((np / TC_BN) * (mp / TC_BM)));
+        static const int group_m = std::getenv("BM_GEMM_GROUP") ? std::atoi(std::getenv("BM_GEMM_GROUP")) : 8;
+        bm::gemm_3xtf32_kernel<<<grid, TC_THREADS, TC_SMEM, s>>>(tm[0], tm[1], tm[2], tm[3], C, m, n, ldc, (int)(kp / TC_BK),
+                                                                  group_m > 0 ? group_m : 8);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) rc = cuda_fail(e, "3xTF32 GEMM launch");
         else st().launches++;

@@ -344,3 +344,23 @@ def test_sharded_helpers_at_world_size_one(dm):
     rf = 1 / (1 + np.exp(-(X.astype(np.float64) @ w))) - y
     normwise(g.to_numpy(), X.T.astype(np.float64) @ rf, 1e-5)
     assert rel_err(s, rf.sum()) <= 1e-5
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("elem,tol", [("f32", 1e-5), ("f64", 1e-12)])
+def test_gemm_nt_32768_sampled(dm, elem, tol):
+    """Config 4 at full size: C = A * B^T at 32768^3 (3xTF32 / DMMA), checked
+    on sampled entries against f64 dot products of the operand rows
+    (the CPU reference at this size costs minutes)."""
+    n = 32768
+    dm.set_seed(3)
+    A = dm.Matrix(n, n, fill="randu", elem_type=elem)
+    B = dm.Matrix(n, n, fill="randu", elem_type=elem)
+    C = dm.evaluate(A @ B.t())
+    rng = np.random.default_rng(12)
+    for i, j in zip(rng.integers(0, n, 12), rng.integers(0, n, 12)):
+        a = dm.evaluate(A.row(int(i))).to_numpy().astype(np.float64).reshape(-1)
+        b = dm.evaluate(B.row(int(j))).to_numpy().astype(np.float64).reshape(-1)
+        ref = float(a @ b)
+        got = C.at(int(i), int(j))
+        assert abs(got - ref) / abs(ref) <= tol, (i, j, got, ref)

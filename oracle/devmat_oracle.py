@@ -22,7 +22,7 @@ __all__ = ["NP_DTYPE", "REDUCE_BLOCK", "ELEM_BLOCK", "GEMM_PANEL", "cast_out", "
            "int_div", "apply_unary", "apply_scalar", "apply_glue", "run_program", "combine_pairwise",
            "block_ranges", "reduce_accu", "reduce_min", "reduce_max", "reduce_dot", "numpy_pairwise_sum",
            "rdim", "gemm", "norm_vector", "norm_matrix", "uniform_stream", "normal_stream",
-           "logistic_step", "tree_walk", "py_min", "py_max"]
+           "logistic_step", "tree_walk", "py_min", "py_max", "predicate_mask", "find_indices"]
 
 
 # ---------------------------------------------------------------------------
@@ -436,3 +436,20 @@ def _region(parent: np.ndarray, region: tuple) -> np.ndarray:
         return parent[:, region[1]:region[2] + 1]
     p, q, r, s = region[1:]
     return parent[p:r + 1, q:s + 1]
+
+
+# -- predicates (kernels.py:643-699) -------------------------------------------------------------
+
+def predicate_mask(x: np.ndarray, op: str, k) -> np.ndarray:
+    """_predicate_mask (kernels.py:643-657): the threshold cast to the element
+    type first (_scalar), then numpy's comparison (NaN compares false except !=)."""
+    kv = scalar_of(k, x.dtype)
+    return {">": np.greater, "<": np.less, ">=": np.greater_equal, "<=": np.less_equal,
+            "==": np.equal, "!=": np.not_equal}[op](x, kv)
+
+
+def find_indices(a: np.ndarray, op: str = "!=", k=0) -> np.ndarray:
+    """find (ops.py:207-229, kernels.py:660-662): ascending column-major linear
+    indices of the matches, as u64."""
+    flat = np.asfortranarray(a).reshape(-1, order="F")
+    return np.nonzero(predicate_mask(flat, op, k))[0].astype(np.uint64)

@@ -77,6 +77,8 @@ int launch_ewise_or_reduce(const bm_invocation* inv, bool to_device, void* dev_r
 int launch_rdim(const bm_invocation* inv);
 int launch_gemm(const bm_invocation* inv);
 int launch_misc(const bm_invocation* inv);
+int launch_pred_count(const bm_invocation* inv, void* dev_result);
+int launch_pred_find(const bm_invocation* inv);
 int combine_partials(const void* dev_partials, int64_t count, int dtype, int op, void* dev_out);
 int launch_fold(int dtype, int op, const void* partials, int64_t nitems, int64_t nfull, bool unit_mode, int chunk,
                 int nchunks, void* result);

@@ -318,6 +318,8 @@ int bm_enqueue(const bm_invocation* inv) {
             return launch_rdim(inv);
         case BM_K_GEMM:
             return launch_gemm(inv);
+        case BM_K_PRED_FIND:
+            return launch_pred_find(inv);
         default:
             return launch_misc(inv);
     }
@@ -325,11 +327,13 @@ int bm_enqueue(const bm_invocation* inv) {
 
 static int reduce_common(const bm_invocation* inv, bool to_device, void* dev_result) {
     BM_REQUIRE_INIT();
-    if (!inv || inv->kind != BM_K_REDUCE) return set_error(BM_ERR_ARG, "bm_execute_reduce: not a reduction");
+    if (!inv || (inv->kind != BM_K_REDUCE && inv->kind != BM_K_PRED_COUNT))
+        return set_error(BM_ERR_ARG, "bm_execute_reduce: not a reduction");
     for (int i = 0; i < inv->n_inputs; ++i) {
         int rc = check_view(inv->inputs[i], "input");
         if (rc) return rc;
     }
+    if (inv->kind == BM_K_PRED_COUNT) return launch_pred_count(inv, to_device ? dev_result : st().result);
     return launch_ewise_or_reduce(inv, to_device, dev_result);
 }
 

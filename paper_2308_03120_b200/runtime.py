@@ -334,6 +334,20 @@ def build_invocation(inv: KernelInvocation) -> _clib.Invocation:
         c.compute_dtype = _clib.DTYPE_CODE[p["gen_type"]]
         c.iparams[0] = rng_key(int(p["seed"]), int(p["stream"]))
         return c
+    if kind in ("pred_count", "pred_all_any", "pred_find_build"):
+        # element-vs-scalar predicates (kernels.py:643-699): the threshold is
+        # cast to the element type first (_scalar), the count is u64
+        c.kind = _clib.BM_K_PRED_FIND if kind == "pred_find_build" else _clib.BM_K_PRED_COUNT
+        elem = ins[0].buf.elem_type
+        c.iparams[0] = _clib.PRED_CODE[p["op"]]
+        k = scalar_for(p["threshold"], elem)
+        if kernels.NP_DTYPE[elem].kind in "iu":
+            c.iscalars[0] = int(np.array([k]).view(np.int64)[0]) if elem == "u64" else int(k)
+        else:
+            c.fscalars[0] = float(k)
+        c.n_scalars = 1
+        c.compute_dtype = _clib.BM_U64
+        return c
     raise NotImplementedError(f"kernel kind {kind!r} is not provided by the B200 device library")
 
 

@@ -364,3 +364,60 @@ def test_gemm_nt_32768_sampled(dm, elem, tol):
         ref = float(a @ b)
         got = C.at(int(i), int(j))
         assert abs(got - ref) / abs(ref) <= tol, (i, j, got, ref)
+
+
+# ---- predicates: find / all / any (ops.py:202-262) ----------------------------------------------
+
+def test_predicates_vs_reference(dm):
+    g = golden("pred")
+    for elem in ("f32", "f64", "i32", "u64"):
+        a = g[f"{elem}_x"]
+        m = dm.Matrix.from_numpy(a)
+        for name, op in (("gt", ">"), ("lt", "<"), ("ge", ">="), ("le", "<=")):
+            for ti, thr in enumerate((0.5, 2, -0.25)):
+                rel = {">": m > thr, "<": m < thr, ">=": m >= thr, "<=": m <= thr}[op]
+                idx = dm.find(rel)
+                assert idx.elem_type == "u64"
+                same(idx.to_numpy().reshape(-1), g[f"{elem}_find_{name}_{ti}"])
+                assert dm.all(rel) == bool(g[f"{elem}_all_{name}_{ti}"])
+                assert dm.any(rel) == bool(g[f"{elem}_any_{name}_{ti}"])
+        same(dm.find(m).to_numpy().reshape(-1), g[f"{elem}_find_nonzero"])
+        assert dm.all(m) == bool(g[f"{elem}_all_nonzero"]) and dm.any(m) == bool(g[f"{elem}_any_nonzero"])
+    same(dm.find(dm.Matrix(3, 3, fill="eye")).to_numpy().reshape(-1), g["eye_find"])
+    same(dm.find(dm.Matrix.from_numpy(g["f32_x"]) * 2 - 1 > 0.25).to_numpy().reshape(-1), g["expr_find"])
+
+
+def test_predicate_conventions_and_transfers(dm):
+    """tests/test_kernels.py:235-274 of the reference."""
+    assert dm.find(dm.Matrix(3, 3, fill="zeros")).n_rows == 0
+    m = dm.Matrix(4, 4, fill="ones")
+    assert dm.all(m) and dm.any(m) and dm.all(m < 2) and not dm.any(m > 5)
+    z = dm.Matrix(4, 4, fill="zeros")
+    assert not dm.any(z) and not dm.all(z)
+    e = dm.Matrix(0, 0)
+    assert dm.all(e) is True and dm.any(e) is False
+    dm.set_seed(33)
+    r = dm.Matrix(1000, 1000, fill="randu")
+    host = r.to_numpy()
+    dm.synchronise()
+    before = dm.counters()
+    count = dm.find(r > 0.3).n_rows
+    delta = dm.counters() - before
+    assert count == int((host > np.float32(0.3)).sum())
+    assert delta.transfers_d2h <= 2
+    idx = dm.find(dm.Matrix(3, 3, fill="eye"))
+    assert dm.accu(idx) == 12
+
+
+@pytest.mark.parametrize("n", [1, 4095, 4096, 4097, 1 << 20, (1 << 24) + 77])
+def test_find_large_vs_oracle(dm, n):
+    rng = np.random.default_rng(n)
+    v = rng.random(n, dtype=np.float32)
+    v[rng.random(n) < 0.01] = np.nan
+    m = dm.Matrix.from_numpy(v.reshape(-1, 1))
+    for op, thr in ((">", 0.7), ("<=", 0.01), ("!=", 0.5)):
+        rel = {">": m > thr, "<=": m <= thr}.get(op)
+        if rel is None:
+            from paper_2308_03120_b200.expr import Relational
+            rel = Relational(op, m, thr)
+        same(dm.find(rel).to_numpy().reshape(-1), O.find_indices(v, op, thr))

@@ -189,3 +189,20 @@ def test_cast_edge_cases():
     assert list(i32) == [imin, imin, imin, imin, imin, -1, 2, imin, imin, imin]
     assert [int(v) for v in u64] == [2 ** 63, 0, 2 ** 63, 3000000000, 2 ** 64 - 3000000000, 2 ** 64 - 1, 2, 0,
                                      2 ** 63, 0]
+
+
+def test_predicates_match_reference_golden():
+    g = golden("pred")
+    for elem in ("f32", "f64", "i32", "u64"):
+        a = g[f"{elem}_x"]
+        flat = np.asfortranarray(a).reshape(-1, order="F")
+        for name, op in (("gt", ">"), ("lt", "<"), ("ge", ">="), ("le", "<=")):
+            for ti, thr in enumerate((0.5, 2, -0.25)):
+                want = g[f"{elem}_find_{name}_{ti}"]
+                got = O.find_indices(a, op, thr)
+                assert np.array_equal(got, want), (elem, op, thr)
+                mask = O.predicate_mask(flat, op, thr)
+                assert bool(mask.all()) == bool(g[f"{elem}_all_{name}_{ti}"])
+                assert bool(mask.any()) == bool(g[f"{elem}_any_{name}_{ti}"])
+        assert np.array_equal(O.find_indices(a), g[f"{elem}_find_nonzero"])
+    assert list(g["eye_find"]) == [0, 4, 8]

@@ -206,6 +206,33 @@ def main() -> None:
     g["lr_r"], g["lr_g"] = r.to_numpy(), gr.to_numpy()
     g["lr_s"] = np.array(dm.accu(r), dtype=np.float32)
     np.savez_compressed(OUT / "misc.npz", **g)
+
+    # ---- 8. predicates: find / all / any (ops.py:202-262) ------------------------------------------
+    g = {}
+    rng = np.random.default_rng(8)
+    mats = {
+        "f32": rng.random((97, 61), dtype=np.float32),
+        "f64": rng.standard_normal((70, 40)),
+        "i32": rng.integers(-5, 6, (50, 33)).astype(np.int32),
+        "u64": rng.integers(0, 9, (45, 21)).astype(np.uint64),
+    }
+    mats["f32"][rng.random((97, 61)) < 0.03] = np.nan
+    mats["f64"][rng.random((70, 40)) < 0.03] = np.nan
+    for elem, a in mats.items():
+        g[f"{elem}_x"] = a
+        m = M(a)
+        for name, op in (("gt", ">"), ("lt", "<"), ("ge", ">="), ("le", "<=")):
+            for ti, thr in enumerate((0.5, 2, -0.25)):
+                rel = {">": m > thr, "<": m < thr, ">=": m >= thr, "<=": m <= thr}[op]
+                g[f"{elem}_find_{name}_{ti}"] = dm.find(rel).to_numpy().reshape(-1)
+                g[f"{elem}_all_{name}_{ti}"] = np.array(dm.all(rel))
+                g[f"{elem}_any_{name}_{ti}"] = np.array(dm.any(rel))
+        g[f"{elem}_find_nonzero"] = dm.find(m).to_numpy().reshape(-1)
+        g[f"{elem}_all_nonzero"] = np.array(dm.all(m))
+        g[f"{elem}_any_nonzero"] = np.array(dm.any(m))
+    g["eye_find"] = dm.find(dm.Matrix(3, 3, fill="eye")).to_numpy().reshape(-1)
+    g["expr_find"] = dm.find(M(mats["f32"]) * 2 - 1 > 0.25).to_numpy().reshape(-1)
+    np.savez_compressed(OUT / "pred.npz", **g)
     dm.shutdown()
     print("golden fixtures written to", OUT)
 

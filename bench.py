@@ -283,6 +283,17 @@ def secondary_suite(dm, torch) -> dict:
         nbytes = 2 * 4 * nrow * ncol
         out["logistic_step_1Mx1024_f32"] = {"ms": t, "GB/s": nbytes / t / 1e6, "frac": nbytes / t / 1e6 / peak_hbm,
                                             "note": "z=X@w, r=1/(1+exp(-z))-y, g=X.t()@r, accu(r); X read twice"}
+        r_e = 1 / (1 + dm.exp(0 - X @ w)) - y
+
+        def timed_fused():
+            r, g = dm.evaluate_many(r_e, X.t() @ r_e)
+            dm.accu(r)
+
+        t = best_ms(timed_fused, reps=3)
+        nbytes = 4 * nrow * ncol
+        out["logistic_step_fused_1Mx1024_f32"] = {
+            "ms": t, "GB/s": nbytes / t / 1e6, "frac": nbytes / t / 1e6 / peak_hbm,
+            "note": "r, g = evaluate_many(r, X.t() @ r) with r = 1/(1+exp(-X@w))-y; accu(r); X read once"}
         del X
     except Exception as e:  # pragma: no cover
         out["logistic_error"] = repr(e)[:200]

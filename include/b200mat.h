@@ -77,16 +77,16 @@ extern "C" {
 #define BM_K_LOGISTIC_GRAD  13   /* fused single-pass logistic step             */
 #define BM_K_PRED_COUNT     14   /* pred_count / pred_all_any: matches of an element-vs-scalar test
                                     (ops.py:202-262, kernels.py:643-699); result u64 via
-                                    bm_execute_reduce; iparams[0] = BM_P_*, threshold in scalars[0] */
+                                    bm_execute_reduce; iparams[0] = BM_CMP_*, threshold in scalars[0] */
 #define BM_K_PRED_FIND      15   /* pred_find_build: ascending u64 linear indices of the matches   */
 
 /* comparison of a predicate (kernels.py:643-657 _predicate_mask) */
-#define BM_P_GT 0
-#define BM_P_LT 1
-#define BM_P_GE 2
-#define BM_P_LE 3
-#define BM_P_EQ 4
-#define BM_P_NE 5
+#define BM_CMP_GT 0
+#define BM_CMP_LT 1
+#define BM_CMP_GE 2
+#define BM_CMP_LE 3
+#define BM_CMP_EQ 4
+#define BM_CMP_NE 5
 
 /* program tags for BM_K_EWISE / BM_K_REDUCE (post-order, expr.py:611-657) */
 #define BM_P_LOAD   0   /* push input[arg]                            */

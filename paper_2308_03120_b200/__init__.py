@@ -13,7 +13,7 @@ The public names mirror reference/pkg/src/devmat/__init__.py.
 from .errors import (BackendError, BoundsError, BufferError_, DevmatError, DimensionError, ElemTypeError,
                      KernelCacheWarning, NotPositiveDefiniteError, NotSymmetricError, PrecisionUnsupportedError,
                      SingularMatrixError)
-from .expr import (EvalPlan, ExprNode, Relational, Shape, build_node, census, evaluate, plan, plan_reduce,
+from .expr import (EvalPlan, ExprNode, Relational, Shape, build_node, census, evaluate, evaluate_many, plan, plan_reduce,
                    rewrite_trans, shape_of)
 from .linalg import as_scalar, gemm, gemv, norm, trace
 from .matrix import Col, HostMatrix, Mat, Matrix, Row, Subview, conv_to, to_device, to_host

@@ -23,8 +23,8 @@ DTYPE_CODE = {"f32": BM_F32, "f64": BM_F64, "i32": BM_I32, "u64": BM_U64}
 (BM_K_EWISE, BM_K_REDUCE, BM_K_RDIM, BM_K_GEMM, BM_K_COPY, BM_K_TRANSPOSE, BM_K_FILL, BM_K_EYE,
  BM_K_LINSPACE, BM_K_RANDU, BM_K_RANDN, BM_K_STRIDED_COPY, BM_K_LOGISTIC_GRAD, BM_K_PRED_COUNT,
  BM_K_PRED_FIND) = range(1, 16)
-BM_P_GT, BM_P_LT, BM_P_GE, BM_P_LE, BM_P_EQ, BM_P_NE = range(6)
-PRED_CODE = {">": BM_P_GT, "<": BM_P_LT, ">=": BM_P_GE, "<=": BM_P_LE, "==": BM_P_EQ, "!=": BM_P_NE}
+BM_CMP_GT, BM_CMP_LT, BM_CMP_GE, BM_CMP_LE, BM_CMP_EQ, BM_CMP_NE = range(6)
+PRED_CODE = {">": BM_CMP_GT, "<": BM_CMP_LT, ">=": BM_CMP_GE, "<=": BM_CMP_LE, "==": BM_CMP_EQ, "!=": BM_CMP_NE}
 
 BM_P_LOAD, BM_P_UNARY, BM_P_SCALAR, BM_P_GLUE = range(4)
 UNARY_CODE = {"eop_exp": 0, "eop_log": 1, "eop_log10": 2, "eop_sqrt": 3, "eop_square": 4, "eop_pow": 5,

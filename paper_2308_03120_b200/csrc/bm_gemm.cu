@@ -233,6 +233,16 @@ __global__ void __launch_bounds__(256) gemv_t_vec_kernel(const T* __restrict__ A
     if (lane == 0) part[(i64)blockIdx.y * ncols + j] = acc;
 }
 
+// fold of the fused logistic step's per-CTA gradient partials, in CTA order
+__global__ void __launch_bounds__(256) lgrad_finish_kernel(const double* __restrict__ part, int grid, i64 k,
+                                                           float* __restrict__ g) {
+    const i64 c = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= k) return;
+    double s = 0.0;
+    for (int b = 0; b < grid; ++b) s += part[(i64)b * k + c];
+    g[c] = (float)s;
+}
+
 }  // namespace bm
 
 namespace bmi {
@@ -375,6 +385,13 @@ int launch_gemm(const bm_invocation* inv) {
         case BM_U64: return gemm_simt<unsigned long long>(ta, tb, m, n, k, A, a.lda, B, b.lda, C, c.lda);
     }
     return set_error(BM_ERR_ARG, "gemm: bad dtype");
+}
+
+int launch_lgrad_finish(const double* gpart, int grid, int64_t k, float* g) {
+    bm::lgrad_finish_kernel<<<(unsigned)((k + 255) / 256), 256, 0, st().stream>>>(gpart, grid, k, g);
+    BM_CUDA(cudaGetLastError());
+    st().launches++;
+    return BM_OK;
 }
 
 }  // namespace bmi

@@ -64,6 +64,7 @@ struct Driver {
     PFN_cuModuleGetFunction_v2000 moduleGetFunction = nullptr;
     PFN_cuLaunchKernel_v4000 launchKernel = nullptr;
     PFN_cuLaunchKernelEx_v11060 launchKernelEx = nullptr;
+    PFN_cuOccupancyMaxActiveClusters_v11070 occupancyMaxActiveClusters = nullptr;
     PFN_cuFuncSetAttribute_v9000 funcSetAttribute = nullptr;
     PFN_cuFuncGetAttribute_v2020 funcGetAttribute = nullptr;
     PFN_cuTensorMapEncodeTiled_v12000 tensorMapEncodeTiled = nullptr;
@@ -79,6 +80,7 @@ int launch_gemm(const bm_invocation* inv);
 int launch_misc(const bm_invocation* inv);
 int launch_pred_count(const bm_invocation* inv, void* dev_result);
 int launch_pred_find(const bm_invocation* inv);
+int launch_logistic_grad(const bm_invocation* inv);
 int combine_partials(const void* dev_partials, int64_t count, int dtype, int op, void* dev_out);
 int launch_fold(int dtype, int op, const void* partials, int64_t nitems, int64_t nfull, bool unit_mode, int chunk,
                 int nchunks, void* result);

@@ -1,0 +1,264 @@
+// bm_lgrad.cuh -- single-pass fused logistic-regression gradient (SURVEY 8f
+// rank 1, config 5): g = X^T F(X w, ...) reading X from HBM once, and the
+// element-wise result r = F(X w, ...) as a side output.
+//
+// The reference runs this as three kernels and reads X twice: z = X@w
+// (sgemv per panel), r = 1/(1+exp(0-z)) - y (fused chain), g = X.t()@r
+// (mov_transpose + gemm), kernels.py:584-586,704-708.
+//
+// Layout.  X is column-major (m x k, lda).  Work is cut into slabs of 64 rows
+// x all k columns.  TMA moves 2-D boxes of 64 rows (256 B, the inner extent
+// that streams at full HBM rate; 64-B rows stream at a third of it,
+// tools/tma2d_probe.cu) x 128 columns.  A slab of 64 x 1024 f32 is 256 KB --
+// more than one SM holds -- so a cluster of 4 CTAs shares it: CTA q of the
+// cluster owns columns [256q, 256q + 256) and keeps its 64 KB quarter in a
+// 3-stage TMA ring.  Per slab:
+//   phase 1  each CTA computes partial z over its columns (f32 chains as in
+//            the reference's sgemv, partials added in f64; fixed order),
+//            publishes them in shared memory, and after one cluster barrier
+//            every CTA sums the four partials in rank order from distributed
+//            shared memory (identical z in all four CTAs);
+//   chain    r_i = F(round_f32(z_i), y_i, ...) -- the fused element-wise
+//            program, every stage rounded to f32 like the unfused plan;
+//   phase 2  each CTA adds sum_i X_ic r_i for its columns from its resident
+//            quarter: lanes over rows, then a butterfly transpose-reduce
+//            (31 shuffles for 16 columns) so each (warp, lane < 16) owns one
+//            column's f64 accumulator for the whole kernel.
+// The loop is software-pipelined: while the cluster barrier of slab j + 1
+// settles, the CTA runs phase 2 of slab j (split barrier arrive / wait).
+// Slabs are dealt round-robin to clusters; every cluster writes its k
+// partials and lgrad_finish folds them in cluster order: deterministic.
+// Compiled by NVRTC with the program's functor E.
+#pragma once
+#include "bm_reduce.cuh"
+
+namespace bm {
+
+#define LG_RB 64            // rows per slab (256 B of f32: full-rate TMA rows)
+#define LG_BOXC 128         // columns per TMA box (32 KB)
+#ifndef LG_CLUSTER
+#define LG_CLUSTER 4        // CTAs per slab (clusters of 8 fit only 15 x 8 SMs at once)
+#endif
+#define LG_COLS (1024 / LG_CLUSTER)   // columns per CTA (LG_CLUSTER * LG_COLS = 1024 = k max)
+#define LG_KMAX (LG_CLUSTER * LG_COLS)
+#define LG_STAGES ((192 * 1024) / (LG_RB * LG_COLS * 4))
+#define LG_THREADS (LG_COLS * 2)      // warps of 16 columns each
+#define LG_STAGE_BYTES (LG_RB * LG_COLS * 4)
+
+struct alignas(64) LgTmap {
+    unsigned long long v[16];   // CUtensorMap (128 B, opaque)
+};
+
+struct LgArgs {
+    Args a;                     // program inputs 1.. (input 0 of the program is z), scalars
+    LgTmap tmx;                 // X: dim0 = rows (contiguous), dim1 = columns
+    const float* w;             // k
+    float* r;                   // m (side output)
+    double* gpart;              // clusters x k partials
+    i64 m, k;
+    i64 nslabs;
+};
+
+__device__ __forceinline__ unsigned lg_smem(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void lg_bar_init(unsigned long long* b, unsigned cnt) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(lg_smem(b)), "r"(cnt));
+}
+__device__ __forceinline__ void lg_expect_tx(unsigned long long* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(lg_smem(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void lg_arrive(unsigned long long* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(lg_smem(b)) : "memory");
+}
+__device__ __forceinline__ void lg_wait(unsigned long long* b, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "LG_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra LG_WAIT_%=;\n"
+        "}\n" ::"r"(lg_smem(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void lg_tma_2d(void* dst, const LgTmap* tm, int c0, int c1, unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            lg_smem(dst)),
+        "l"(tm), "r"(c0), "r"(c1), "r"(lg_smem(bar))
+        : "memory");
+}
+__device__ __forceinline__ unsigned lg_cluster_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void lg_cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// f64 at the same shared-memory offset in CTA `rank` of the cluster (no
+// memory clobber: the loads of all ranks can be in flight together; ordering
+// against the peers' writes comes from the cluster barrier before them)
+__device__ __forceinline__ double lg_ld_peer(const double* p, unsigned rank) {
+    unsigned remote;
+    asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(lg_smem(p)), "r"(rank));
+    double v;
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(remote));
+    return v;
+}
+
+template <class E>
+__device__ void logistic_grad(const LgArgs& L) {
+    extern __shared__ __align__(1024) char lg_raw[];
+    char* ring = lg_raw + ((1024 - (lg_smem(lg_raw) & 1023)) & 1023);
+    __shared__ unsigned long long full[LG_STAGES], empty[LG_STAGES];
+    __shared__ double zpart[2][LG_THREADS / 32][LG_RB];   // by slab parity
+    __shared__ double zq[2][LG_RB];          // this CTA's partial z, by slab parity (read by the cluster)
+    __shared__ float rs[2][LG_RB];
+    __shared__ float ws[LG_COLS];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const unsigned q = lg_cluster_rank();
+    const i64 cluster = blockIdx.x / LG_CLUSTER, nclusters = gridDim.x / LG_CLUSTER;
+    const i64 nmine = L.nslabs > cluster ? (L.nslabs - cluster + nclusters - 1) / nclusters : 0;
+    const int col0 = (int)q * LG_COLS;                  // this CTA's first column
+    for (int c = tid; c < LG_COLS; c += LG_THREADS) ws[c] = (col0 + c < L.k) ? L.w[col0 + c] : 0.f;
+    if (tid == 0) {
+        for (int s = 0; s < LG_STAGES; ++s) {
+            lg_bar_init(&full[s], 1);
+            lg_bar_init(&empty[s], LG_THREADS / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&L.tmx) : "memory");
+    }
+    __syncthreads();
+    auto issue = [&](i64 j) {   // this CTA's quarter of slab j into stage j % STAGES
+        const int s = (int)(j % LG_STAGES);
+        const i64 slab = cluster + j * nclusters;
+        lg_expect_tx(&full[s], LG_STAGE_BYTES);
+#pragma unroll
+        for (int b = 0; b < (LG_COLS + LG_BOXC - 1) / LG_BOXC; ++b)
+            lg_tma_2d(ring + s * LG_STAGE_BYTES + b * (LG_BOXC * LG_RB * 4), &L.tmx, (int)(slab * LG_RB),
+                      col0 + b * LG_BOXC, &full[s]);
+    };
+    if (tid == 0)
+        for (i64 j = 0; j < LG_STAGES - 1 && j < nmine; ++j) issue(j);
+
+    double gacc = 0.0;                         // column col0 + 16 * warp + lane (lanes < 16)
+    const int wc = 16 * warp;                  // this warp's 16 columns within the CTA's 256
+    // column c (0..255) of stage s: 64 rows = 256 B at (c/128)*32KB + (c%128)*256
+    auto colp = [&](int s, int c) -> const float2* {
+        return reinterpret_cast<const float2*>(ring + s * LG_STAGE_BYTES + (c >> 7) * (LG_BOXC * LG_RB * 4) +
+                                               (c & 127) * (LG_RB * 4)) + lane;
+    };
+    // phase 1 of slab j: lane holds rows 2*lane, 2*lane+1; two f32 chains per
+    // row over the warp's 16 columns (the reference's z is an f32 sgemv); the
+    // 16 warp partials and the 4 CTA partials are added in f64
+    auto phase1 = [&](i64 j) {
+        const int s = (int)(j % LG_STAGES);
+        lg_wait(&full[s], (unsigned)((j / LG_STAGES) & 1));
+        float a0 = 0.f, a1 = 0.f, b0 = 0.f, b1 = 0.f;
+#pragma unroll
+        for (int u = 0; u < 16; u += 2) {
+            const float2 x = *colp(s, wc + u), y = *colp(s, wc + u + 1);
+            const float w0 = ws[wc + u], w1 = ws[wc + u + 1];
+            a0 = __fmaf_rn(x.x, w0, a0);
+            a1 = __fmaf_rn(x.y, w0, a1);
+            b0 = __fmaf_rn(y.x, w1, b0);
+            b1 = __fmaf_rn(y.y, w1, b1);
+        }
+        const int par = (int)(j & 1);
+        zpart[par][warp][2 * lane] = (double)a0 + (double)b0;
+        zpart[par][warp][2 * lane + 1] = (double)a1 + (double)b1;
+    };
+    // publish this CTA's partial z of slab j and arrive on the cluster barrier
+    // (zpart of slab j complete: the caller synchronised)
+    auto publish = [&](i64 j) {
+        const int par = (int)(j & 1);
+        if (tid < LG_RB) {
+            // balanced tree over the warp partials (fixed order, 4 levels deep)
+            double t[LG_THREADS / 32];
+#pragma unroll
+            for (int w = 0; w < LG_THREADS / 32; ++w) t[w] = zpart[par][w][tid];
+#pragma unroll
+            for (int h = 1; h < LG_THREADS / 32; h <<= 1)
+#pragma unroll
+                for (int w = 0; w + h < LG_THREADS / 32; w += 2 * h) t[w] = t[w] + t[w + h];
+            zq[par][tid] = t[0];
+            asm volatile("fence.acq_rel.cluster;" ::: "memory");   // only the writers pay for the release
+        }
+        asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+    };
+    // after the cluster barrier of slab j: z (four partials in rank order) and r
+    auto chain = [&](i64 j) {
+        asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+        const int par = (int)(j & 1);
+        if (tid < LG_RB) {
+            double zp[LG_CLUSTER];
+#pragma unroll
+            for (unsigned p = 0; p < LG_CLUSTER; ++p) zp[p] = lg_ld_peer(&zq[par][tid], p);
+            double z = zp[0];
+#pragma unroll
+            for (unsigned p = 1; p < LG_CLUSTER; ++p) z = z + zp[p];
+            const i64 row = (cluster + j * nclusters) * LG_RB + tid;
+            float r = 0.f;
+            if (row < L.m) {
+                r = E::at(L.a, row, (float)z);
+                if (q == 0) L.r[row] = r;
+            }
+            rs[par][tid] = r;
+        }
+    };
+    // phase 2 of slab j: partial sums over this lane's two rows for the warp's
+    // 16 columns, a transpose-reduce across the 32 lanes, then the stage is free
+    auto phase2 = [&](i64 j) {
+        const int s = (int)(j % LG_STAGES), par = (int)(j & 1);
+        const float r0 = rs[par][2 * lane], r1 = rs[par][2 * lane + 1];
+        float v[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+            const float2 x = *colp(s, wc + c);
+            v[c] = __fmaf_rn(x.y, r1, x.x * r0);
+        }
+#pragma unroll
+        for (int c = 0; c < 16; ++c) v[c] = v[c] + __shfl_xor_sync(0xffffffffu, v[c], 16);
+#pragma unroll
+        for (int off = 8; off >= 1; off >>= 1) {
+            const bool upper = (lane & off) != 0;
+#pragma unroll
+            for (int c = 0; c < off; ++c) {
+                const float send = upper ? v[c] : v[c + off];
+                const float keep = upper ? v[c + off] : v[c];
+                v[c] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+            }
+        }
+        gacc += (double)v[0];                  // lane l (and l ^ 16) now holds column wc + (l & 15)
+        __syncwarp();
+        if (lane == 0) lg_arrive(&empty[s]);
+    };
+
+    // Software pipeline: the cluster exchange of slab j + 1 is in flight while
+    // this CTA runs phase 2 of slab j.
+    if (nmine > 0) {
+        phase1(0);
+        __syncthreads();
+        publish(0);
+    }
+    for (i64 j = 0; j < nmine; ++j) {
+        if (tid == 0 && j + LG_STAGES - 1 < nmine) {
+            const i64 jn = j + LG_STAGES - 1;
+            if (jn >= LG_STAGES) lg_wait(&empty[jn % LG_STAGES], (unsigned)(((jn / LG_STAGES) - 1) & 1));
+            issue(jn);
+        }
+        chain(j);
+        if (j + 1 < nmine) phase1(j + 1);
+        __syncthreads();                       // r of slab j and the z partials of slab j + 1
+        if (j + 1 < nmine) publish(j + 1);
+        phase2(j);
+    }
+    if (lane < 16) {
+        const i64 c = col0 + wc + lane;
+        if (c < L.k) L.gpart[cluster * L.k + c] = gacc;
+    }
+    lg_cluster_sync();                             // no CTA exits while a peer may still read its zq
+}
+
+}  // namespace bm

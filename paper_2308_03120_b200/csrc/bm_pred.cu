@@ -23,11 +23,11 @@ namespace bm {
 template <typename T>
 __device__ __forceinline__ bool pred_eval(T x, int op, T k) {
     switch (op) {
-        case BM_P_GT: return x > k;
-        case BM_P_LT: return x < k;
-        case BM_P_GE: return x >= k;
-        case BM_P_LE: return x <= k;
-        case BM_P_EQ: return x == k;
+        case BM_CMP_GT: return x > k;
+        case BM_CMP_LT: return x < k;
+        case BM_CMP_GE: return x >= k;
+        case BM_CMP_LE: return x <= k;
+        case BM_CMP_EQ: return x == k;
         default: return x != k;
     }
 }
@@ -166,7 +166,7 @@ int launch_pred_count(const bm_invocation* inv, void* dev_result) {
     const bm_view& v = inv->inputs[0];
     const int64_t n = v.count;
     const int op = (int)inv->iparams[0];
-    if (op < BM_P_GT || op > BM_P_NE) return set_error(BM_ERR_ARG, "predicate: bad comparison");
+    if (op < BM_CMP_GT || op > BM_CMP_NE) return set_error(BM_ERR_ARG, "predicate: bad comparison");
     BM_CUDA(cudaMemsetAsync(dev_result, 0, 8, st().stream));
     if (n == 0) return BM_OK;
     return pred_typed(v.dtype, [&](auto t) {
@@ -191,7 +191,7 @@ int launch_pred_find(const bm_invocation* inv) {
     if (o.dtype != BM_U64 || o.stride != 1) return set_error(BM_ERR_ARG, "find: output must be a contiguous u64 view");
     const int64_t n = v.count;
     const int op = (int)inv->iparams[0];
-    if (op < BM_P_GT || op > BM_P_NE) return set_error(BM_ERR_ARG, "predicate: bad comparison");
+    if (op < BM_CMP_GT || op > BM_CMP_NE) return set_error(BM_ERR_ARG, "predicate: bad comparison");
     if (n == 0 || o.count == 0) return BM_OK;
     const int64_t nchunks = (n + PRED_CHUNK - 1) / PRED_CHUNK;
     if (nchunks > 0x7fffffff) return set_error(BM_ERR_NOTIMPL, "find: input too large");

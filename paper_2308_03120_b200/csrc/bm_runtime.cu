@@ -60,6 +60,7 @@ int load_driver() {
     BM_GET(cuModuleGetFunction, moduleGetFunction);
     BM_GET(cuLaunchKernel, launchKernel);
     BM_GET(cuLaunchKernelEx, launchKernelEx);
+    BM_GET(cuOccupancyMaxActiveClusters, occupancyMaxActiveClusters);
     BM_GET(cuFuncSetAttribute, funcSetAttribute);
     BM_GET(cuFuncGetAttribute, funcGetAttribute);
     BM_GET(cuTensorMapEncodeTiled, tensorMapEncodeTiled);
@@ -320,6 +321,8 @@ int bm_enqueue(const bm_invocation* inv) {
             return launch_gemm(inv);
         case BM_K_PRED_FIND:
             return launch_pred_find(inv);
+        case BM_K_LOGISTIC_GRAD:
+            return launch_logistic_grad(inv);
         default:
             return launch_misc(inv);
     }

@@ -359,6 +359,7 @@ class EvalPlan:
     result: tuple
     absorbed: list
     reduce: PlanStep | None = None   # trailing fused reduction (plan_reduce)
+    extra: tuple = ()                # further result refs (evaluate_many)
 
     @property
     def n_invocations(self) -> int:
@@ -367,14 +368,22 @@ class EvalPlan:
     @property
     def temp_schedule(self) -> dict:
         """slot -> (producing step, last consuming step); the result slot has none."""
-        final = self.result[1] if self.result and self.result[0] == "slot" else None
+        final = self.final_slots
         span = {s.out_slot: [i, None] for i, s in enumerate(self.steps)}
+        for i, st in enumerate(self.steps):    # side outputs written by the step (logistic_grad's r)
+            for a in st.params.get("alloc_slots", ()):
+                span[a] = [i, None]
         consumers = list(self.steps) + ([self.reduce] if self.reduce is not None else [])
         for i, s in enumerate(consumers):
             for ref in s.inputs:
-                if ref[0] == "slot" and ref[1] != final:
+                if ref[0] == "slot" and ref[1] not in final:
                     span[ref[1]][1] = i
         return {k: tuple(v) for k, v in span.items()}
+
+    @property
+    def final_slots(self) -> set:
+        refs = ((self.result,) if self.result else ()) + tuple(self.extra)
+        return {r[1] for r in refs if r and r[0] == "slot"}
 
     def leaf_buffer_ids(self) -> set[int]:
         ids = {ref[1].mem.buffer_id for s in self.steps for ref in s.inputs if ref[0] == "leaf"}
@@ -418,6 +427,7 @@ class _Lowerer:
         self.steps: list[PlanStep] = []
         self.slots: list[SlotInfo] = []
         self.absorbed: list[tuple] = []
+        self.memo: dict = {}          # (id(node), type) -> ref of a value a fused step already produced
 
     def emit(self, kernel, inputs, in_modes, shape, out_type, out_mode, scalars=(), params=None,
              absorbed_from=None) -> tuple:
@@ -431,6 +441,9 @@ class _Lowerer:
 
     # -- recursion ------------------------------------------------------------------------
     def lower(self, node: ExprNode, want: str):
+        hit = self.memo.get((id(node), want))
+        if hit is not None:
+            return hit
         k = node.kind
         if k == "leaf":
             m = node.operands[0]
@@ -487,6 +500,10 @@ class _Lowerer:
                 ref = self.emit("mov_copy", [ref], ["flat"], shape_of(node), want, "flat")
             return ref
         if k == "glue_times":
+            if self.fuse:
+                ref = self._logistic(node, want)
+                if ref is not None:
+                    return ref
             a, b = node.operands
             ta = tb = 0
             if a.kind == "op_htrans":     # fold the transpose into the GEMM
@@ -501,6 +518,81 @@ class _Lowerer:
                 ref = self.emit("mov_copy", [ref], ["flat"], shape_of(node), want, "flat")
             return ref
         raise ValueError(f"cannot lower node kind {k!r}")
+
+    # -- fused single-pass logistic step ---------------------------------------
+    def _logistic(self, node: ExprNode, want: str):
+        """X.t() @ F(X @ w, leaves...) -> one logistic_grad step that reads X
+        once and also produces F(...) (memoised, so evaluate_many can return
+        it).  Only the config-5 shape class: f32, X a leaf with k <= 1024
+        columns and m % 4 == 0 rows, F element-wise over the one product X @ w
+        and m x 1 f32 leaves.  Anything else lowers as GEMV + chain + GEMV."""
+        a, b = node.operands
+        if a.kind != "op_htrans" or a.operands[0].kind != "leaf" or b.kind not in ELEMENTWISE_KINDS:
+            return None
+        X = a.operands[0].operands[0]
+        m, k = X.n_rows, X.n_cols
+        sb = shape_of(b)
+        if X.elem_type != "f32" or b.elem_type != "f32" or sb.rows != m or sb.cols != 1:
+            return None
+        if not 1 <= k <= 1024 or m % 4 or m < 16:
+            return None
+        found: list = []
+
+        def scan(n: ExprNode) -> bool:
+            if n.kind in ELEMENTWISE_KINDS:
+                return all(scan(o) for o in n.operands)
+            if n.kind == "glue_times" and n.operands[0].kind == "leaf" and n.operands[0].operands[0] is X:
+                if found and found[0] is not n:
+                    return False
+                found[:] = [n]
+                return True
+            if n.kind == "leaf":
+                s_ = shape_of(n)
+                return n.elem_type == "f32" and s_.rows == m and s_.cols == 1
+            return False
+
+        if not scan(b) or not found:
+            return None
+        gnode = found[0]
+        w = gnode.operands[1]
+        sw = shape_of(w)
+        if w.elem_type != "f32" or sw.rows != k or sw.cols != 1:
+            return None
+        prog = _Program()
+        prog.inputs.append(("z", None))       # program input 0: X @ w, computed in the kernel
+
+        def walk(n: ExprNode) -> None:
+            if n is gnode:
+                prog.stages.append(("load", 0))
+            elif n.kind == "leaf":
+                prog.load(("leaf", n.operands[0]))
+            elif n.kind in EGLUE_KINDS:
+                walk(n.operands[0])
+                walk(n.operands[1])
+                prog.stages.append(("glue", n.kind))
+            elif n.kind in EOP_SCALAR_KINDS:
+                walk(n.operands[0])
+                prog.stages.append(("scalar", n.kind, n.aux[0]))
+            else:
+                walk(n.operands[0])
+                prog.stages.append(("unary", n.kind, n.aux[0] if n.aux else None))
+
+        walk(b)
+        walk = None  # noqa: F841  (break the closure's self-reference, see program())
+        if len(prog.stages) > 64 or len(prog.inputs) + 2 > 16:
+            return None
+        wref = self.lower(w, "f32")
+        self.slots.append(SlotInfo(m, 1, "f32"))
+        r_slot = len(self.slots) - 1
+        inputs = [("leaf", X), wref, ("slot", r_slot)] + list(prog.inputs[1:])
+        modes = ["2d", "flat", "flat"] + ["flat"] * (len(prog.inputs) - 1)
+        ref = self.emit("logistic_grad", inputs, modes, shape_of(node), "f32", "flat",
+                        params={"program": tuple(prog.stages), "compute_dtype": NP_DTYPE["f32"].str,
+                                "alloc_slots": (r_slot,)})
+        self.memo[(id(b), "f32")] = ("slot", r_slot)
+        if want != "f32":
+            ref = self.emit("mov_copy", [ref], ["flat"], shape_of(node), want, "flat")
+        return ref
 
     # -- element-wise programs -----------------------------------------------------------------
     def program(self, root: ExprNode, elem: str, budget: int) -> _Program:
@@ -684,9 +776,10 @@ def execute_plan(plan_obj: EvalPlan, target_buf=None):
     an empty plan).  When the plan carries a fused reduction it is executed
     last and its value is returned instead."""
     rt = runtime.get_runtime()
-    if plan_obj.result is not None and plan_obj.result[0] == "leaf" and plan_obj.reduce is None:
+    if plan_obj.result is not None and plan_obj.result[0] == "leaf" and plan_obj.reduce is None and not plan_obj.extra:
         return plan_obj.result[1]
     final_slot = plan_obj.result[1] if plan_obj.result is not None else None
+    finals = plan_obj.final_slots
     release_after = {s: span[1] for s, span in plan_obj.temp_schedule.items()}
     slot_bufs: dict[int, object] = {}
 
@@ -694,11 +787,14 @@ def execute_plan(plan_obj: EvalPlan, target_buf=None):
         done = set()
         for ref in step.inputs:
             s = ref[1]
-            if ref[0] == "slot" and s != final_slot and release_after.get(s) == i and s not in done:
+            if ref[0] == "slot" and s not in finals and release_after.get(s) == i and s not in done:
                 done.add(s)
                 rt.release_deferred(slot_bufs.pop(s))
 
     for i, step in enumerate(plan_obj.steps):
+        for a in step.params.get("alloc_slots", ()):     # side outputs the step writes
+            ai = plan_obj.slots[a]
+            slot_bufs[a] = rt.acquire_memory(ai.rows * ai.cols, ai.elem_type)
         views = _step_views(plan_obj, step, slot_bufs)
         info = plan_obj.slots[step.out_slot]
         if step.out_slot == final_slot and target_buf is not None:
@@ -722,6 +818,8 @@ def execute_plan(plan_obj: EvalPlan, target_buf=None):
         finally:
             release_inputs(step, len(plan_obj.steps))
         return value
+    if plan_obj.extra:
+        return [slot_bufs[r[1]] if r[0] == "slot" else r[1] for r in (plan_obj.result,) + tuple(plan_obj.extra)]
     return slot_bufs[final_slot]
 
 
@@ -758,6 +856,51 @@ def evaluate(x, out=None, fuse: bool = True):
     out._reshape_storage(shape.rows, shape.cols)
     execute_plan(p, target_buf=out.mem)
     return out
+
+
+def evaluate_many(*xs, fuse: bool = True) -> list:
+    """Evaluate several expressions in one plan and return one fresh matrix
+    per expression (an extension of the reference's evaluate).  Values a
+    fused step produces on the way are shared: with r = F(X @ w, y) and
+    g = X.t() @ r, ``r, g = evaluate_many(r, g)`` reads X once (the fused
+    logistic step) instead of twice."""
+    from .matrix import Matrix
+    nodes = [as_expr(x) for x in xs]
+    if not nodes:
+        return []
+    low = _Lowerer(fuse)
+    # products first, so that side outputs of fused steps are memoised
+    # before the expressions that name them are lowered
+    order = sorted(range(len(nodes)), key=lambda i: 0 if nodes[i].kind == "glue_times" else 1)
+    refs: list = [None] * len(nodes)
+    for i in order:
+        refs[i] = low.lower(nodes[i], nodes[i].elem_type)
+    seen: set = set()
+    out_refs = []
+    for r in refs:                 # a value asked for twice is copied for the second matrix
+        if r[0] == "slot" and r[1] in seen:
+            r = ("dup", r[1])
+        elif r[0] == "slot":
+            seen.add(r[1])
+        out_refs.append(r)
+    slot_refs = [r if r[0] != "dup" else ("slot", r[1]) for r in out_refs]
+    p = EvalPlan(low.steps, low.slots, slot_refs[0], low.absorbed, extra=tuple(slot_refs[1:]))
+    rt = runtime.get_runtime()
+    if not p.steps:
+        bufs = [r[1] for r in slot_refs]
+    else:
+        bufs = execute_plan(p)
+    result = []
+    for node, r, b in zip(nodes, out_refs, bufs):
+        shape = shape_of(node)
+        if r[0] == "slot":
+            result.append(Matrix._adopt(b, shape.rows, shape.cols, node.elem_type))
+        else:   # a leaf or a duplicate: a copy, like evaluate(leaf)
+            src = b.mem if r[0] == "leaf" else b
+            m = Matrix._uninitialised(shape.rows, shape.cols, node.elem_type)
+            rt.copy_d2d(src, m.mem, shape.n_elem)
+            result.append(m)
+    return result
 
 
 def reduce_value(op: str, *xs):

@@ -334,6 +334,17 @@ def build_invocation(inv: KernelInvocation) -> _clib.Invocation:
         c.compute_dtype = _clib.DTYPE_CODE[p["gen_type"]]
         c.iparams[0] = rng_key(int(p["seed"]), int(p["stream"]))
         return c
+    if kind == "logistic_grad":
+        # fused g = X^T F(X w, ...) with r = F(...) (bm_lgrad.cuh): inputs X, w, r
+        # (written), then the program's inputs 1..; program input 0 is X w
+        c.kind = _clib.BM_K_LOGISTIC_GRAD
+        elem = _NPSTR_TO_ELEM[np.dtype(p["compute_dtype"]).str]
+        c.compute_dtype = _clib.DTYPE_CODE[elem]
+        pb = _ProgramBuilder(c, elem)
+        for st in p["program"]:
+            pb.stage(st)
+        pb.finish()
+        return c
     if kind in ("pred_count", "pred_all_any", "pred_find_build"):
         # element-vs-scalar predicates (kernels.py:643-699): the threshold is
         # cast to the element type first (_scalar), the count is u64

@@ -421,3 +421,44 @@ def test_find_large_vs_oracle(dm, n):
             from paper_2308_03120_b200.expr import Relational
             rel = Relational(op, m, thr)
         same(dm.find(rel).to_numpy().reshape(-1), O.find_indices(v, op, thr))
+
+
+# ---- fused single-pass logistic step (bm_lgrad.cuh) -------------------------------------------------
+
+def test_fused_logistic_step_vs_reference(dm):
+    """r, g = evaluate_many(F(X@w, y), X.t() @ F(...)) is one fused kernel
+    reading X once; same tolerances as the unfused reference step."""
+    g = golden("misc")
+    X, w, y = (dm.Matrix.from_numpy(g[k]) for k in ("lr_X", "lr_w", "lr_y"))
+    r_e = 1 / (1 + dm.exp(0 - X @ w)) - y
+    p = dm.plan(X.t() @ r_e)
+    assert [s.kernel for s in p.steps] == ["logistic_grad"]
+    r, gr = dm.evaluate_many(r_e, X.t() @ r_e)
+    ulp_close(r.to_numpy(), g["lr_r"], 1e-5)
+    np.testing.assert_allclose(gr.to_numpy(), g["lr_g"], rtol=1e-4, atol=1e-5)
+    assert rel_err(dm.accu(r), g["lr_s"]) <= 1e-4
+    # the single-expression form (no r returned)
+    np.testing.assert_allclose(dm.evaluate(X.t() @ r_e).to_numpy(), g["lr_g"], rtol=1e-4, atol=1e-5)
+
+
+@pytest.mark.parametrize("m,k", [(1 << 16, 1024), (4100, 300), (4096 * 3 + 16, 1000)])
+def test_fused_logistic_step_large(dm, m, k):
+    rng = np.random.default_rng(m + k)
+    X = rng.standard_normal((m, k), dtype=np.float32)
+    w = (0.03 * rng.standard_normal((k, 1))).astype(np.float32)
+    y = (rng.random((m, 1)) < 0.5).astype(np.float32)
+    mX, mw, my = dm.Matrix.from_numpy(X), dm.Matrix.from_numpy(w), dm.Matrix.from_numpy(y)
+    r_e = 1 / (1 + dm.exp(0 - mX @ mw)) - my
+    r, gr = dm.evaluate_many(r_e, mX.t() @ r_e)
+    # unfused device path (GEMV + chain + GEMV) and an f64 host reference
+    r2 = dm.evaluate(1 / (1 + dm.exp(0 - dm.evaluate(mX @ mw))) - my)
+    g2 = dm.evaluate(mX.t() @ r2)
+    rf = 1 / (1 + np.exp(-(X.astype(np.float64) @ w))) - y
+    gf = X.T.astype(np.float64) @ rf
+    normwise(r.to_numpy(), rf, 1e-5)
+    normwise(gr.to_numpy(), gf, 1e-5)
+    normwise(gr.to_numpy(), g2.to_numpy(), 1e-5)
+    # deterministic: a second run is bit-identical
+    r3, g3 = dm.evaluate_many(r_e, mX.t() @ r_e)
+    same(g3.to_numpy(), gr.to_numpy())
+    same(r3.to_numpy(), r.to_numpy())

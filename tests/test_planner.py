@@ -212,3 +212,48 @@ def test_planning_leaves_no_reference_cycles():
     finally:
         gc.set_debug(0)
         gc.garbage.clear()
+
+
+# ---- fused single-pass logistic step ------------------------------------------
+
+def _logistic_parts(m=4096, k=1024):
+    X, w, y = FakeMatrix(m, k), FakeMatrix(k, 1), FakeMatrix(m, 1)
+    xn, wn, yn = X._as_expr_node(), w._as_expr_node(), y._as_expr_node()
+    r = 1 / (1 + dm.exp(0 - xn @ wn)) - yn
+    return X, w, y, xn, r
+
+
+def test_logistic_gradient_is_one_fused_step():
+    X, w, y, xn, r = _logistic_parts()
+    p = expr.plan(xn.t() @ r)
+    assert [s.kernel for s in p.steps] == ["logistic_grad"]
+    st = p.steps[0]
+    assert st.inputs[0] == ("leaf", X) and st.inputs[1] == ("leaf", w) and st.inputs[3] == ("leaf", y)
+    assert st.params["program"][0] == ("load", 0)            # X @ w is program input 0
+    r_slot = st.inputs[2][1]
+    assert st.params["alloc_slots"] == (r_slot,)
+    assert p.temp_schedule[r_slot] == (0, 0)                   # r is released after the step
+
+
+def test_logistic_fusion_declines_other_shapes():
+    X, w, y, xn, r = _logistic_parts(m=4098)                   # rows not a multiple of 4
+    assert [s.kernel for s in expr.plan(xn.t() @ r).steps] != ["logistic_grad"]
+    X, w, y, xn, r = _logistic_parts(k=2048)                   # too many columns
+    assert "logistic_grad" not in [s.kernel for s in expr.plan(xn.t() @ r).steps]
+    X2 = FakeMatrix(4096, 1024)._as_expr_node()                # a different X in the product
+    w = FakeMatrix(1024, 1)._as_expr_node()
+    r2 = 1 / (1 + dm.exp(0 - X2 @ w))
+    assert "logistic_grad" not in [s.kernel for s in expr.plan(xn.t() @ r2).steps]
+
+
+def test_logistic_kernel_compiles():
+    X, w, y, xn, r = _logistic_parts()
+    p = expr.plan(xn.t() @ r)
+    st = p.steps[0]
+    fake_r = FakeMatrix(4096, 1)
+    views = [expr._make_view(X.mem, 4096, 1024, "2d"), expr._make_view(w.mem, 1024, 1, "flat"),
+             expr._make_view(fake_r.mem, 4096, 1, "flat"), expr._make_view(y.mem, 4096, 1, "flat")]
+    g = FakeMatrix(1024, 1)
+    inv = build_invocation(KernelInvocation("logistic_grad", tuple(views), _flat(g), (), st.params))
+    rc = _clib.lib().bm_jit_compile_only(ctypes.byref(inv))
+    assert rc == 0, _clib.last_error()

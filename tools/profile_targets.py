@@ -1,5 +1,5 @@
 """Run one hot-path workload a few times so ncu can capture its kernel.
-Usage: python tools/profile_targets.py cfg1|accu1|logistic|gemm_f32|gemm_f64|rdim0|rdim1|dot"""
+Usage: python tools/profile_targets.py cfg1|accu1|logistic|logistic_fused|gemm_f32|gemm_f64|rdim0|rdim1|dot"""
 import pathlib
 import sys
 
@@ -33,6 +33,14 @@ def main(which: str) -> None:
             r = dm.evaluate(1 / (1 + dm.exp(0 - z)) - y)
             g = dm.evaluate(X.t() @ r)
             dm.accu(r)
+    elif which == "logistic_fused":
+        nrow, ncol = 1 << 20, 1024
+        X = dm.Matrix(nrow, ncol, fill="randn")
+        w = dm.evaluate(0.03 * dm.Matrix(ncol, 1, fill="randn"))
+        y = dm.evaluate(dm.conv_to(dm.conv_to(2 * dm.Matrix(nrow, 1, fill="randu"), "i32"), "f32"))
+        r_e = 1 / (1 + dm.exp(0 - X @ w)) - y
+        for _ in range(3):
+            r, g = dm.evaluate_many(r_e, X.t() @ r_e)
     elif which in ("gemm_f32", "gemm_f64"):
         elem = which[-3:]
         n = 8192

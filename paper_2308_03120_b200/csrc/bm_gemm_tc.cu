@@ -265,52 +265,65 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-#define DM_BM 128
+// CTA tile BM x 128 (BM = 64: 4 warps in a 2 x 2 grid of 32 x 64 warp tiles,
+// two CTAs per SM so one CTA's barrier and refill overlap the other's DMMAs;
+// BM = 128: 8 warps of 64 x 32).  Each warp tile is 32 8x8 DMMA tiles (64 f64
+// accumulators per lane) fed by 12 8-byte shared loads per k4 step.
 #define DM_BN 128
 #define DM_BK 16
 #define DM_ST 3
-#define DM_LD (DM_BM + 8)
-#define DM_SMEM (DM_ST * 2 * DM_BK * DM_LD * 8)
 
-template <bool TA, bool TB>
-__global__ void __launch_bounds__(256, 1) gemm_dmma_kernel(const double* __restrict__ A, i64 lda,
-                                                           const double* __restrict__ B, i64 ldb,
-                                                           double* __restrict__ C, i64 ldc, i64 m, i64 n, i64 k) {
+template <int BM>
+struct DmCfg {
+    static constexpr int NW = BM == 64 ? 4 : 8;           // warps
+    static constexpr int WGN = BM == 64 ? 2 : 4;          // warps along N
+    static constexpr int MI = BM == 64 ? 4 : 8;           // 8-row DMMA tiles per warp (M)
+    static constexpr int NJ = BM == 64 ? 8 : 4;           // 8-col DMMA tiles per warp (N)
+    static constexpr int LDA = BM + 8, LDB = DM_BN + 8;   // padded smem rows (doubles)
+    static constexpr int SMEM = DM_ST * DM_BK * (LDA + LDB) * 8;
+};
+
+template <bool TA, bool TB, int BM>
+__global__ void __launch_bounds__(DmCfg<BM>::NW * 32, BM == 64 ? 2 : 1)
+    gemm_dmma_kernel(const double* __restrict__ A, i64 lda, const double* __restrict__ B, i64 ldb,
+                     double* __restrict__ C, i64 ldc, i64 m, i64 n, i64 k) {
+    typedef DmCfg<BM> G;
+    constexpr int NT = G::NW * 32;
     extern __shared__ __align__(16) double dsm[];
-    double* As = dsm;                                  // [ST][BK][LD]
-    double* Bs = dsm + DM_ST * DM_BK * DM_LD;          // [ST][BK][LD]
+    double* As = dsm;                                     // [ST][BK][LDA]
+    double* Bs = dsm + DM_ST * DM_BK * G::LDA;            // [ST][BK][LDB]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int gid = lane >> 2, tig = lane & 3;
-    const i64 m0 = (i64)blockIdx.y * DM_BM, n0 = (i64)blockIdx.x * DM_BN;
-    const int wm = (warp >> 2) * 64, wn = (warp & 3) * 32;
-    double acc[8][4][2];
+    const i64 m0 = (i64)blockIdx.y * BM, n0 = (i64)blockIdx.x * DM_BN;
+    const int wm = (warp / G::WGN) * (8 * G::MI), wn = (warp % G::WGN) * (8 * G::NJ);
+    double acc[G::MI][G::NJ][2];
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < G::MI; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int j = 0; j < G::NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
     auto load = [&](int st, i64 k0) {
-        double* as = As + st * DM_BK * DM_LD;
-        double* bs = Bs + st * DM_BK * DM_LD;
+        double* as = As + st * DM_BK * G::LDA;
+        double* bs = Bs + st * DM_BK * G::LDB;
 #pragma unroll
-        for (int t = 0; t < (DM_BK * DM_BM) / 256; ++t) {
-            const int idx = threadIdx.x + t * 256;
+        for (int t = 0; t < (DM_BK * BM) / NT; ++t) {
+            const int idx = threadIdx.x + t * NT;
             int kk, mm;
-            if (TA) { mm = idx / DM_BK; kk = idx % DM_BK; } else { kk = idx / DM_BM; mm = idx % DM_BM; }
+            if (TA) { mm = idx / DM_BK; kk = idx % DM_BK; } else { kk = idx / BM; mm = idx % BM; }
             const i64 gi = m0 + mm, gl = k0 + kk;
             const bool ok = gi < m && gl < k;
             const double* src = ok ? (TA ? A + gl + gi * lda : A + gi + gl * lda) : A;
-            cp_async8(as + kk * DM_LD + mm, src, ok);
+            cp_async8(as + kk * G::LDA + mm, src, ok);
         }
 #pragma unroll
-        for (int t = 0; t < (DM_BK * DM_BN) / 256; ++t) {
-            const int idx = threadIdx.x + t * 256;
+        for (int t = 0; t < (DM_BK * DM_BN) / NT; ++t) {
+            const int idx = threadIdx.x + t * NT;
             int kk, nn;
             if (TB) { kk = idx / DM_BN; nn = idx % DM_BN; } else { nn = idx / DM_BK; kk = idx % DM_BK; }
             const i64 gj = n0 + nn, gl = k0 + kk;
             const bool ok = gj < n && gl < k;
             const double* src = ok ? (TB ? B + gj + gl * ldb : B + gl + gj * ldb) : B;
-            cp_async8(bs + kk * DM_LD + nn, src, ok);
+            cp_async8(bs + kk * G::LDB + nn, src, ok);
         }
     };
     const i64 nk = (k + DM_BK - 1) / DM_BK;
@@ -326,26 +339,26 @@ __global__ void __launch_bounds__(256, 1) gemm_dmma_kernel(const double* __restr
         const i64 nxt = kb + DM_ST - 1;
         if (nxt < nk) load((int)(nxt % DM_ST), nxt * DM_BK);
         cp_async_commit();
-        const double* as = As + (kb % DM_ST) * DM_BK * DM_LD;
-        const double* bs = Bs + (kb % DM_ST) * DM_BK * DM_LD;
+        const double* as = As + (kb % DM_ST) * DM_BK * G::LDA;
+        const double* bs = Bs + (kb % DM_ST) * DM_BK * G::LDB;
 #pragma unroll
         for (int ks = 0; ks < DM_BK; ks += 4) {
-            double af[8], bf[4];
+            double af[G::MI], bf[G::NJ];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) af[i] = as[(ks + tig) * DM_LD + wm + 8 * i + gid];
+            for (int i = 0; i < G::MI; ++i) af[i] = as[(ks + tig) * G::LDA + wm + 8 * i + gid];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) bf[j] = bs[(ks + tig) * DM_LD + wn + 8 * j + gid];
+            for (int j = 0; j < G::NJ; ++j) bf[j] = bs[(ks + tig) * G::LDB + wn + 8 * j + gid];
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
+            for (int i = 0; i < G::MI; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j], af[i], bf[j]);
+                for (int j = 0; j < G::NJ; ++j) dmma_8x8x4(acc[i][j], af[i], bf[j]);
         }
     }
     cp_async_wait<0>();
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < G::MI; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < G::NJ; ++j)
 #pragma unroll
             for (int t = 0; t < 2; ++t) {
                 const i64 r = m0 + wm + 8 * i + gid, c = n0 + wn + 8 * j + 2 * tig + t;
@@ -426,32 +439,43 @@ int gemm_tc_f32(int ta, int tb, int64_t m, int64_t n, int64_t k, const float* A,
     return rc;
 }
 
+template <int BM>
+static int dmma_launch(int ta, int tb, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
+                       const double* B, int64_t ldb, double* C, int64_t ldc) {
+    typedef bm::DmCfg<BM> G;
+    dim3 grid((unsigned)((n + DM_BN - 1) / DM_BN), (unsigned)((m + BM - 1) / BM));
+    if (grid.y > 65535) return set_error(BM_ERR_NOTIMPL, "gemm: too many row tiles");
+    cudaStream_t s = st().stream;
+    static bool attr = false;
+    if (!attr) {
+        BM_CUDA(cudaFuncSetAttribute(bm::gemm_dmma_kernel<true, true, BM>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
+        BM_CUDA(cudaFuncSetAttribute(bm::gemm_dmma_kernel<true, false, BM>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
+        BM_CUDA(cudaFuncSetAttribute(bm::gemm_dmma_kernel<false, true, BM>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
+        BM_CUDA(cudaFuncSetAttribute(bm::gemm_dmma_kernel<false, false, BM>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
+        attr = true;
+    }
+    const int nt = G::NW * 32;
+    if (ta) {
+        if (tb) bm::gemm_dmma_kernel<true, true, BM><<<grid, nt, G::SMEM, s>>>(A, lda, B, ldb, C, ldc, m, n, k);
+        else bm::gemm_dmma_kernel<true, false, BM><<<grid, nt, G::SMEM, s>>>(A, lda, B, ldb, C, ldc, m, n, k);
+    } else {
+        if (tb) bm::gemm_dmma_kernel<false, true, BM><<<grid, nt, G::SMEM, s>>>(A, lda, B, ldb, C, ldc, m, n, k);
+        else bm::gemm_dmma_kernel<false, false, BM><<<grid, nt, G::SMEM, s>>>(A, lda, B, ldb, C, ldc, m, n, k);
+    }
+    BM_CUDA(cudaGetLastError());
+    st().launches++;
+    return BM_OK;
+}
+
 int gemm_dmma_f64(int ta, int tb, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B,
                   int64_t ldb, double* C, int64_t ldc, bool* handled) {
     *handled = false;
     if (m * n * k < (int64_t)1 << 18) return BM_OK;
-    dim3 grid((unsigned)((n + DM_BN - 1) / DM_BN), (unsigned)((m + DM_BM - 1) / DM_BM));
-    if (grid.y > 65535) return BM_OK;
-    cudaStream_t s = st().stream;
-    static bool attr = false;
-    if (!attr) {
-        BM_CUDA(cudaFuncSetAttribute(bm::gemm_dmma_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, DM_SMEM));
-        BM_CUDA(cudaFuncSetAttribute(bm::gemm_dmma_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, DM_SMEM));
-        BM_CUDA(cudaFuncSetAttribute(bm::gemm_dmma_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, DM_SMEM));
-        BM_CUDA(cudaFuncSetAttribute(bm::gemm_dmma_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, DM_SMEM));
-        attr = true;
-    }
-    if (ta) {
-        if (tb) bm::gemm_dmma_kernel<true, true><<<grid, 256, DM_SMEM, s>>>(A, lda, B, ldb, C, ldc, m, n, k);
-        else bm::gemm_dmma_kernel<true, false><<<grid, 256, DM_SMEM, s>>>(A, lda, B, ldb, C, ldc, m, n, k);
-    } else {
-        if (tb) bm::gemm_dmma_kernel<false, true><<<grid, 256, DM_SMEM, s>>>(A, lda, B, ldb, C, ldc, m, n, k);
-        else bm::gemm_dmma_kernel<false, false><<<grid, 256, DM_SMEM, s>>>(A, lda, B, ldb, C, ldc, m, n, k);
-    }
-    BM_CUDA(cudaGetLastError());
-    st().launches++;
-    *handled = true;
-    return BM_OK;
+    static const int bm = (std::getenv("BM_DMMA_BM") && std::atoi(std::getenv("BM_DMMA_BM")) == 128) ? 128 : 64;
+    const int rc = bm == 128 ? dmma_launch<128>(ta, tb, m, n, k, A, lda, B, ldb, C, ldc)
+                             : dmma_launch<64>(ta, tb, m, n, k, A, lda, B, ldb, C, ldc);
+    if (!rc) *handled = true;
+    return rc;
 }
 
 }  // namespace bmi

@@ -225,20 +225,74 @@ __device__ __forceinline__ T pw_half(const S& s, i64 off, char* tile) {
     return res;
 }
 
-// balanced pairwise tree over `count` = 2^k consecutive half-units
+// rows of one half-unit, loaded (program evaluated) but not yet reduced
+template <typename T> struct HalfRows { T v[8][16 / sizeof(T)]; };
+
+template <typename T, class S>
+__device__ __forceinline__ void half_load(const S& s, i64 off, HalfRows<T>& h) {
+    constexpr int V = 16 / sizeof(T);
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) s.template vec<V>(off + r * 32 * V + lane * V, h.v[r]);
+}
+
+template <typename T>
+__device__ __forceinline__ T half_reduce(const HalfRows<T>& h, char* tile) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+        *reinterpret_cast<uint4*>(tile + r * BM_TILE_PITCH + lane * 16) = *reinterpret_cast<const uint4*>(h.v[r]);
+    __syncwarp();
+    const T res = pw_half_tile<T>(tile);
+    __syncwarp();
+    return res;
+}
+
+// balanced pairwise tree over `count` = 2^k consecutive half-units.  The
+// binary-counter stack lives in registers (levels unrolled) and, on the
+// vector path, the rows of half-unit u + 1 are loaded while half-unit u is
+// reduced, so every warp keeps a half-unit of loads in flight.
 template <typename T, class S>
 __device__ T pw_balanced(const S& s, i64 off, i64 count, char* tile, bool vec_ok) {
     constexpr i64 U = PwHalf<T>::value;
-    T stk[24];
-    int lvl[24];
-    int sp = 0;
-    for (i64 u = 0; u < count; ++u) {
-        T v = vec_ok ? pw_half<T, true>(s, off + u * U, tile) : pw_half<T, false>(s, off + u * U, tile);
-        int l = 0;
-        while (sp > 0 && lvl[sp - 1] == l) { v = stk[sp - 1] + v; --sp; ++l; }
-        stk[sp] = v; lvl[sp] = l; ++sp;
+    constexpr int LV = 12;                        // register levels: count <= 4096
+    if (count > (1 << LV) || !vec_ok) {
+        T stk[24];
+        int lvl[24];
+        int sp = 0;
+        for (i64 u = 0; u < count; ++u) {
+            T v = vec_ok ? pw_half<T, true>(s, off + u * U, tile) : pw_half<T, false>(s, off + u * U, tile);
+            int l = 0;
+            while (sp > 0 && lvl[sp - 1] == l) { v = stk[sp - 1] + v; --sp; ++l; }
+            stk[sp] = v; lvl[sp] = l; ++sp;
+        }
+        return stk[0];
     }
-    return stk[0];
+    T stk[LV + 1];
+    HalfRows<T> cur, nxt;
+    half_load<T>(s, off, cur);
+    for (i64 u = 0; u < count; ++u) {
+        if (u + 1 < count) half_load<T>(s, off + (u + 1) * U, nxt);
+        T v = half_reduce<T>(cur, tile);
+        // u's trailing one bits are the pending left subtrees v merges with
+#pragma unroll
+        for (int l = 0; l <= LV; ++l) {
+            if (l < LV && ((u >> l) & 1)) {
+                v = stk[l] + v;
+            } else {
+                stk[l] = v;
+                break;
+            }
+        }
+        cur = nxt;
+    }
+    int top = 0;
+    while ((1ll << top) < count) ++top;
+    T res = stk[0];
+#pragma unroll
+    for (int l = 1; l <= LV; ++l)
+        if (l == top) res = stk[l];
+    return res;
 }
 
 // numpy leaf: n < 8 sequential from 0; n <= 128 eight interleaved accumulators

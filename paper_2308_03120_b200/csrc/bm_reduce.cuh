@@ -251,9 +251,11 @@ __device__ __forceinline__ T half_reduce(const HalfRows<T>& h, char* tile) {
 // balanced pairwise tree over `count` = 2^k consecutive half-units.  The
 // binary-counter stack lives in registers (levels unrolled) and, on the
 // vector path, the rows of half-unit u + 1 are loaded while half-unit u is
-// reduced, so every warp keeps a half-unit of loads in flight.
+// reduced, so every warp keeps a half-unit of loads in flight.  Not inlined:
+// its double-buffered rows must not raise the register budget of the
+// reduction kernels' hot half-unit loop.
 template <typename T, class S>
-__device__ T pw_balanced(const S& s, i64 off, i64 count, char* tile, bool vec_ok) {
+__device__ __noinline__ T pw_balanced(const S& s, i64 off, i64 count, char* tile, bool vec_ok) {
     constexpr i64 U = PwHalf<T>::value;
     constexpr int LV = 12;                        // register levels: count <= 4096
     if (count > (1 << LV) || !vec_ok) {

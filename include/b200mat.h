@@ -79,6 +79,12 @@ extern "C" {
                                     (ops.py:202-262, kernels.py:643-699); result u64 via
                                     bm_execute_reduce; iparams[0] = BM_CMP_*, threshold in scalars[0] */
 #define BM_K_PRED_FIND      15   /* pred_find_build: ascending u64 linear indices of the matches   */
+#define BM_K_GEMM_FUSED     16   /* glue_times over element-wise operands (f32, 3xTF32): each operand's
+                                    program is evaluated inside the split pre-pass (expr.py:596-605
+                                    lowers them to separate chains).  inputs: A's program inputs
+                                    (iparams[0] of them), then B's; prog: A's stages (iparams[1]),
+                                    then B's (loads relative to B's inputs); iparams[2], [3] = stored
+                                    rows of A and B; [4..6] = m, n, k; output C (m x n)            */
 
 /* comparison of a predicate (kernels.py:643-657 _predicate_mask) */
 #define BM_CMP_GT 0

@@ -24,45 +24,18 @@ namespace bm {
 // ---------------------------------------------------------------------------
 // 3xTF32 split pre-pass: out[r * kp + c] for r < rp (M or N), c < kp (K)
 
-__device__ __forceinline__ float tf32_rna(float x) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return __uint_as_float(r);
-}
-
-// src_kmajor: op(src)(r, c) = src[c + r*ld]; otherwise src[r + c*ld]
+// the split kernel (split_tf32_body) lives in bm_reduce.cuh so that NVRTC can
+// instantiate it over a fused element-wise operand (GEMM prologue fusion)
+struct PlainSrc {
+    const float* src;
+    i64 ld;
+    __device__ __forceinline__ float at(i64 idx) const { return src[idx]; }
+};
 template <bool SRC_KMAJOR>
 __global__ void __launch_bounds__(256) split_tf32_kernel(const float* __restrict__ src, i64 ld, i64 rows, i64 k,
                                                          float* __restrict__ hi, float* __restrict__ lo, i64 kp,
                                                          i64 rp) {
-    __shared__ float tile[32][33];
-    const i64 r0 = (i64)blockIdx.y * 32, c0 = (i64)blockIdx.x * 32;
-    if (SRC_KMAJOR) {
-        for (int j = threadIdx.y; j < 32; j += blockDim.y) {
-            const i64 r = r0 + j, c = c0 + threadIdx.x;
-            float v = 0.f;
-            if (r < rows && c < k) v = src[c + r * ld];
-            tile[j][threadIdx.x] = v;
-        }
-    } else {
-        // read with threadIdx.x along r (contiguous), park transposed
-        for (int j = threadIdx.y; j < 32; j += blockDim.y) {
-            const i64 r = r0 + threadIdx.x, c = c0 + j;
-            float v = 0.f;
-            if (r < rows && c < k) v = src[r + c * ld];
-            tile[threadIdx.x][j] = v;
-        }
-    }
-    __syncthreads();
-    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
-        const i64 r = r0 + j, c = c0 + threadIdx.x;
-        if (r < rp && c < kp) {
-            const float x = tile[j][threadIdx.x];
-            const float h = tf32_rna(x);
-            hi[r * kp + c] = h;
-            lo[r * kp + c] = tf32_rna(x - h);
-        }
-    }
+    split_tf32_body<SRC_KMAJOR>(PlainSrc{src, ld}, ld, rows, k, hi, lo, kp, rp);
 }
 
 // ---------------------------------------------------------------------------
@@ -394,10 +367,11 @@ static int split_operand(const float* src, int64_t ld, bool kmajor, int64_t rows
     return BM_OK;
 }
 
-int gemm_tc_f32(int ta, int tb, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const float* B,
-                int64_t ldb, float* C, int64_t ldc, bool* handled) {
+// C = op(A) op(B) on the 3xTF32 tcgen05 path; split_a / split_b fill the
+// K-major hi/lo copies of op(A) (m x k) and op(B)^T (n x k).
+int gemm_tc_f32_core(int64_t m, int64_t n, int64_t k, const SplitFn& split_a, const SplitFn& split_b, float* C,
+                     int64_t ldc, bool* handled) {
     *handled = false;
-    if (m * n * k < (int64_t)1 << 21) return BM_OK;   // tiny: the SIMT kernel is cheaper than the split pass
     const int64_t mp = (m + TC_BM - 1) / TC_BM * TC_BM;
     const int64_t np = (n + TC_BN - 1) / TC_BN * TC_BN;
     const int64_t kp = (k + 31) / 32 * 32;   // split kernel tiles K by 32
@@ -407,10 +381,8 @@ int gemm_tc_f32(int ta, int tb, int64_t m, int64_t n, int64_t k, const float* A,
     const int64_t a_elems = mp * kp, b_elems = np * kp;
     BM_CUDA(cudaMallocAsync((void**)&buf, (size_t)(2 * (a_elems + b_elems) * 4), s));
     float *ahi = buf, *alo = buf + a_elems, *bhi = buf + 2 * a_elems, *blo = buf + 2 * a_elems + b_elems;
-    // op(A) is m x k; K-major iff A is stored transposed.  op(B) is k x n and we
-    // need its N x K K-major form: K-major iff B is NOT transposed.
-    int rc = split_operand(A, lda, ta != 0, m, k, ahi, alo, kp, mp);
-    if (!rc) rc = split_operand(B, ldb, tb == 0, n, k, bhi, blo, kp, np);
+    int rc = split_a(ahi, alo, kp, mp);
+    if (!rc) rc = split_b(bhi, blo, kp, np);
     CUtensorMap tm[4];
     if (!rc) rc = encode_kmajor(&tm[0], ahi, kp, mp, TC_BM);
     if (!rc) rc = encode_kmajor(&tm[1], alo, kp, mp, TC_BM);
@@ -437,6 +409,19 @@ int gemm_tc_f32(int ta, int tb, int64_t m, int64_t n, int64_t k, const float* A,
     cudaFreeAsync(buf, s);
     if (!rc) *handled = true;
     return rc;
+}
+
+int gemm_tc_f32(int ta, int tb, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const float* B,
+                int64_t ldb, float* C, int64_t ldc, bool* handled) {
+    *handled = false;
+    if (m * n * k < (int64_t)1 << 21) return BM_OK;   // tiny: the SIMT kernel is cheaper than the split pass
+    // op(A) is m x k; K-major iff A is stored transposed.  op(B) is k x n and we
+    // need its N x K K-major form: K-major iff B is NOT transposed.
+    return gemm_tc_f32_core(
+        m, n, k,
+        [&](float* hi, float* lo, int64_t kp, int64_t rp) { return split_operand(A, lda, ta != 0, m, k, hi, lo, kp, rp); },
+        [&](float* hi, float* lo, int64_t kp, int64_t rp) { return split_operand(B, ldb, tb == 0, n, k, hi, lo, kp, rp); },
+        C, ldc, handled);
 }
 
 template <int BM>

@@ -781,6 +781,53 @@ __device__ void reduce_flat(const Args& a, const S& s) {
 }
 
 // ---------------------------------------------------------------------------
+// 3xTF32 split pre-pass (bm_gemm_tc.cu): hi = rna_tf32(x), lo = rna_tf32(x -
+// hi), written K-major as out[r * kp + c] for r < rp (M or N), c < kp (K),
+// zero-padded.  The source is read through `src.at(linear index)`: a plain
+// matrix, or (GEMM prologue fusion) the JIT-compiled element-wise program of
+// the operand, evaluated on the fly so the operand is never materialised.
+// SRC_KMAJOR: op(X)(r, c) = X[c + r*ld]; otherwise X[r + c*ld].
+
+__device__ __forceinline__ float tf32_rna(float x) {
+    unsigned r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+template <bool SRC_KMAJOR, class SRC>
+__device__ __forceinline__ void split_tf32_body(const SRC& src, i64 ld, i64 rows, i64 k, float* __restrict__ hi,
+                                                float* __restrict__ lo, i64 kp, i64 rp) {
+    __shared__ float tile[32][33];
+    const i64 r0 = (i64)blockIdx.y * 32, c0 = (i64)blockIdx.x * 32;
+    if (SRC_KMAJOR) {
+        for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+            const i64 r = r0 + j, c = c0 + threadIdx.x;
+            float v = 0.f;
+            if (r < rows && c < k) v = src.at(c + r * ld);
+            tile[j][threadIdx.x] = v;
+        }
+    } else {
+        // read with threadIdx.x along r (contiguous), park transposed
+        for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+            const i64 r = r0 + threadIdx.x, c = c0 + j;
+            float v = 0.f;
+            if (r < rows && c < k) v = src.at(r + c * ld);
+            tile[threadIdx.x][j] = v;
+        }
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        const i64 r = r0 + j, c = c0 + threadIdx.x;
+        if (r < rp && c < kp) {
+            const float x = tile[j][threadIdx.x];
+            const float h = tf32_rna(x);
+            hi[r * kp + c] = h;
+            lo[r * kp + c] = tf32_rna(x - h);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // External fold for large reductions: CTA k folds the aligned chunk k of
 // block partials (combine_pairwise in shared memory), then one CTA folds the
 // chunk results.  Equal to one combine_pairwise over all blocks (aligned

@@ -323,6 +323,8 @@ int bm_enqueue(const bm_invocation* inv) {
             return launch_pred_find(inv);
         case BM_K_LOGISTIC_GRAD:
             return launch_logistic_grad(inv);
+        case BM_K_GEMM_FUSED:
+            return launch_gemm_fused(inv);
         default:
             return launch_misc(inv);
     }

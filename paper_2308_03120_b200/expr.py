@@ -502,6 +502,8 @@ class _Lowerer:
         if k == "glue_times":
             if self.fuse:
                 ref = self._logistic(node, want)
+                if ref is None:
+                    ref = self._gemm_prologue(node, want)
                 if ref is not None:
                     return ref
             a, b = node.operands
@@ -592,6 +594,46 @@ class _Lowerer:
         self.memo[(id(b), "f32")] = ("slot", r_slot)
         if want != "f32":
             ref = self.emit("mov_copy", [ref], ["flat"], shape_of(node), want, "flat")
+        return ref
+
+    # -- GEMM prologue fusion ------------------------------------------------
+    def _gemm_prologue(self, node: ExprNode, want: str):
+        """glue_times with an element-wise operand, f32, on the tensor-core
+        path: the operands' programs run inside the 3xTF32 split pre-pass
+        (gemm_fused) instead of materialising `2*A + 1` first.  Vector and
+        small shapes keep the reference's lowering (GEMV / SIMT)."""
+        a, b = node.operands
+        ta = tb = 0
+        if a.kind == "op_htrans":
+            a, ta = a.operands[0], 1
+        if b.kind == "op_htrans":
+            b, tb = b.operands[0], 1
+        if node.elem_type != "f32" or a.elem_type != "f32" or b.elem_type != "f32":
+            return None
+        if a.kind not in ELEMENTWISE_KINDS and b.kind not in ELEMENTWISE_KINDS:
+            return None
+        s = shape_of(node)
+        sa, sb = shape_of(a), shape_of(b)
+        k = sa.rows if ta else sa.cols
+        if s.rows < 2 or s.cols < 2 or s.rows * s.cols * k < (1 << 21):
+            return None
+        progs = []
+        for x in (a, b):
+            if x.kind in ELEMENTWISE_KINDS:
+                pr = self._fit_program(x, "f32")
+            else:
+                pr = _Program()
+                pr.load(self.lower(x, "f32"))
+            progs.append(pr)
+        if len(progs[0].inputs) + len(progs[1].inputs) > 16 or len(progs[0].stages) + len(progs[1].stages) > 64:
+            return None
+        inputs = list(progs[0].inputs) + list(progs[1].inputs)
+        ref = self.emit("gemm_fused", inputs, ["flat"] * len(inputs), s, "f32", "2d",
+                        params={"a_prog": tuple(progs[0].stages), "b_prog": tuple(progs[1].stages),
+                                "na": len(progs[0].inputs), "trans_a": ta, "trans_b": tb,
+                                "a_rows": sa.rows, "b_rows": sb.rows, "m": s.rows, "n": s.cols, "k": k})
+        if want != "f32":
+            ref = self.emit("mov_copy", [ref], ["flat"], s, want, "flat")
         return ref
 
     # -- element-wise programs -----------------------------------------------------------------

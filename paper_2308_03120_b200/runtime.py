@@ -334,6 +334,23 @@ def build_invocation(inv: KernelInvocation) -> _clib.Invocation:
         c.compute_dtype = _clib.DTYPE_CODE[p["gen_type"]]
         c.iparams[0] = rng_key(int(p["seed"]), int(p["stream"]))
         return c
+    if kind == "gemm_fused":
+        # GEMM prologue fusion: A's program (over inputs [0, na)), then B's
+        # (loads relative to B's inputs), evaluated inside the split pre-pass
+        c.kind = _clib.BM_K_GEMM_FUSED
+        c.compute_dtype = _clib.BM_F32
+        pb = _ProgramBuilder(c, "f32")
+        for st in p["a_prog"]:
+            pb.stage(st)
+        npa = pb.n
+        for st in p["b_prog"]:
+            pb.stage(st)
+        pb.finish()
+        c.trans_a, c.trans_b = int(p["trans_a"]), int(p["trans_b"])
+        c.iparams[0], c.iparams[1] = int(p["na"]), npa
+        c.iparams[2], c.iparams[3] = int(p["a_rows"]), int(p["b_rows"])
+        c.iparams[4], c.iparams[5], c.iparams[6] = int(p["m"]), int(p["n"]), int(p["k"])
+        return c
     if kind == "logistic_grad":
         # fused g = X^T F(X w, ...) with r = F(...) (bm_lgrad.cuh): inputs X, w, r
         # (written), then the program's inputs 1..; program input 0 is X w

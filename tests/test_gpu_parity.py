@@ -462,3 +462,31 @@ def test_fused_logistic_step_large(dm, m, k):
     r3, g3 = dm.evaluate_many(r_e, mX.t() @ r_e)
     same(g3.to_numpy(), gr.to_numpy())
     same(r3.to_numpy(), r.to_numpy())
+
+
+# ---- GEMM prologue fusion ------------------------------------------------------------------------
+
+@pytest.mark.parametrize("m,n,k,tb", [(512, 384, 256, 1), (1000, 700, 300, 0), (2048, 2048, 1024, 1)])
+def test_gemm_fused_operand_chains(dm, m, n, k, tb):
+    """(2A + 1) @ op(exp(B/4) - 3) with the operand programs inside the split
+    pre-pass: same numbers as materialising the operands first."""
+    rng = np.random.default_rng(m + n + k)
+    a = rng.random((m, k), dtype=np.float32)
+    b = rng.random((n, k) if tb else (k, n), dtype=np.float32)
+    mA, mB = dm.Matrix.from_numpy(a), dm.Matrix.from_numpy(b)
+    eb = dm.exp(mB / 4) - 3
+    expr = (2 * mA + 1) @ (eb.t() if tb else eb)
+    assert [s.kernel for s in dm.plan(expr).steps] == ["gemm_fused"]
+    dm.synchronise()
+    before = dm.counters()
+    got = dm.evaluate(expr).to_numpy()
+    assert (dm.counters() - before).launches == 1
+    # unfused device path and an f64 host reference of the same operand values
+    ua = dm.evaluate(2 * mA + 1)
+    ub = dm.evaluate(eb)
+    ref_dev = dm.evaluate(ua @ (ub.t() if tb else ub)).to_numpy()
+    oa = ua.to_numpy().astype(np.float64)
+    ob = ub.to_numpy().astype(np.float64)
+    ref = oa @ (ob.T if tb else ob)
+    normwise(got, ref, 1e-5)
+    same(got, ref_dev)          # identical operand values and the same 3xTF32 kernel: bit-identical

@@ -257,3 +257,32 @@ def test_logistic_kernel_compiles():
     inv = build_invocation(KernelInvocation("logistic_grad", tuple(views), _flat(g), (), st.params))
     rc = _clib.lib().bm_jit_compile_only(ctypes.byref(inv))
     assert rc == 0, _clib.last_error()
+
+
+# ---- GEMM prologue fusion ------------------------------------------------------
+
+def test_gemm_operand_chains_fuse_into_the_split_pass():
+    a, b = leaf(256, 256), leaf(256, 256)
+    p = dm.plan((2 * a + 1) @ (b - 3).t())
+    assert [s.kernel for s in p.steps] == ["gemm_fused"]
+    st = p.steps[0]
+    assert st.params["na"] == 1 and st.params["trans_b"] == 1
+    assert st.params["a_prog"][0] == ("load", 0) and st.params["b_prog"][0] == ("load", 0)
+    # one chained operand and one plain leaf
+    p = dm.plan((2 * a + 1) @ b)
+    assert [s.kernel for s in p.steps] == ["gemm_fused"]
+    # small and vector shapes keep the reference's lowering
+    assert dm.plan((2 * leaf(4, 4) + 1) @ (leaf(4, 4) - 3)).n_invocations == 3
+    v = leaf(256, 1)
+    assert "gemm_fused" not in [s.kernel for s in dm.plan((2 * a + 1) @ v).steps]
+
+
+def test_gemm_split_kernel_compiles():
+    A, B, C = FakeMatrix(256, 256), FakeMatrix(256, 256), FakeMatrix(256, 256)
+    an, bn = A._as_expr_node(), B._as_expr_node()
+    p = dm.plan(dm.exp(an) * 0.5 @ (bn - 3))
+    st = p.steps[0]
+    views = [expr._make_view(A.mem, 256, 256, "flat"), expr._make_view(B.mem, 256, 256, "flat")]
+    inv = build_invocation(KernelInvocation("gemm_fused", tuple(views), expr._make_view(C.mem, 256, 256, "2d"), (),
+                                            st.params))
+    assert inv.kind == _clib.BM_K_GEMM_FUSED and inv.iparams[0] == 1

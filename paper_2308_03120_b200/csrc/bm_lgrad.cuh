@@ -69,16 +69,23 @@ __device__ __forceinline__ void lg_expect_tx(unsigned long long* b, unsigned byt
 __device__ __forceinline__ void lg_arrive(unsigned long long* b) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(lg_smem(b)) : "memory");
 }
+// try_wait polled from a C++ loop: a branch loop inside inline asm hides the
+// loop from the compiler's reconvergence analysis, which deadlocked a
+// warp-specialised variant of this kernel (divergent producer lane + named
+// barriers)
 __device__ __forceinline__ void lg_wait(unsigned long long* b, unsigned parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "LG_WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra LG_WAIT_%=;\n"
-        "}\n" ::"r"(lg_smem(b)),
-        "r"(parity)
-        : "memory");
+    unsigned ok;
+    do {
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n"
+            "}\n"
+            : "=r"(ok)
+            : "r"(lg_smem(b)), "r"(parity)
+            : "memory");
+    } while (!ok);
 }
 __device__ __forceinline__ void lg_tma_2d(void* dst, const LgTmap* tm, int c0, int c1, unsigned long long* bar) {
     asm volatile(

@@ -30,8 +30,6 @@ namespace bm {
 #define BM_REDUCE_BLOCK 8192
 #define BM_TILE_PITCH 544
 #define BM_TILE_BYTES (8 * BM_TILE_PITCH)   // one half-unit (8 rows of 512 B)
-#define BM_RWARPS 16                     // default warps per (persistent) reduction CTA
-#define BM_REDUCE_SMEM (BM_RWARPS * BM_TILE_BYTES)
 #ifndef BM_UNIT_UNROLL
 #define BM_UNIT_UNROLL 4                 // rows of a pairwise unit loaded per batch
 #endif
@@ -481,15 +479,16 @@ __device__ A cta_combine_pairwise(A* v, A* w, int cnt) {
 // ---------------------------------------------------------------------------
 // flat reduction kernel body.
 //
-// Work items are either the 2048/1024-element pairwise units of every full
-// REDUCE_BLOCK block ("unit mode", used when there are few blocks per SM, so
-// the work balances across all 148 SMs) or whole blocks ("block mode"); the
-// ragged tail block is one extra item.  Items are dealt to CTAs round-robin
-// (one persistent CTA per SM), every item writes one partial to global
-// scratch, and the last CTA to finish folds them: units -> block partials
-// with numpy's balanced tree, then blocks with combine_pairwise -- streamed by
-// each thread over an aligned power-of-two run of blocks with a binary-counter
-// stack (identical to combine_pairwise's level order), then across threads.
+// Work items are either the 1024/512-element pairwise half-units of every
+// full REDUCE_BLOCK block ("unit mode": always for the float accu, and for the
+// other ops when blocks are scarce) or whole blocks ("block mode"); the
+// ragged tail block is one extra item.  One persistent CTA per SM; warps take
+// runs of items from a global counter (reduce_flat).  Every item writes one
+// partial to global scratch, and the last CTA to finish folds them (ticket):
+// half-unit partials -> block values with numpy's balanced tree
+// (stage_block_values), then the blocks with combine_pairwise
+// (cta_fold_pairwise: balanced 256-groups per warp, the ragged rest and the
+// group values level by level), chunk results streamed in order.
 // No float atomics: the result is the reference's bits.
 
 template <typename A, int OP>

@@ -14,10 +14,11 @@
 // cluster owns columns [256q, 256q + 256) and keeps its 64 KB quarter in a
 // 3-stage TMA ring.  Per slab:
 //   phase 1  each CTA computes partial z over its columns (f32 chains as in
-//            the reference's sgemv, partials added in f64; fixed order),
-//            publishes them in shared memory, and after one cluster barrier
-//            every CTA sums the four partials in rank order from distributed
-//            shared memory (identical z in all four CTAs);
+//            the reference's sgemv, partials added in f64; fixed order) and
+//            pushes them into all four CTAs' shared memory (distributed
+//            shared memory stores); after one cluster barrier every CTA sums
+//            the four partials in rank order (identical z in all four CTAs);
+//            the program inputs of the next slab are prefetched into L2;
 //   chain    r_i = F(round_f32(z_i), y_i, ...) -- the fused element-wise
 //            program, every stage rounded to f32 like the unfused plan;
 //   phase 2  each CTA adds sum_i X_ic r_i for its columns from its resident
@@ -34,7 +35,10 @@
 
 namespace bm {
 
+#ifndef LG_RB
 #define LG_RB 64            // rows per slab (256 B of f32: full-rate TMA rows)
+#endif
+#define LG_RPL (LG_RB / 32) // rows per lane
 #define LG_BOXC 128         // columns per TMA box (32 KB)
 #ifndef LG_CLUSTER
 #define LG_CLUSTER 4        // CTAs per slab (clusters of 8 fit only 15 x 8 SMs at once)
@@ -102,24 +106,13 @@ __device__ __forceinline__ unsigned lg_cluster_rank() {
 __device__ __forceinline__ void lg_cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-// f64 at the same shared-memory offset in CTA `rank` of the cluster (no
-// memory clobber: the loads of all ranks can be in flight together; ordering
-// against the peers' writes comes from the cluster barrier before them)
-__device__ __forceinline__ double lg_ld_peer(const double* p, unsigned rank) {
-    unsigned remote;
-    asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(lg_smem(p)), "r"(rank));
-    double v;
-    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(remote));
-    return v;
-}
-
 template <class E>
 __device__ void logistic_grad(const LgArgs& L) {
     extern __shared__ __align__(1024) char lg_raw[];
     char* ring = lg_raw + ((1024 - (lg_smem(lg_raw) & 1023)) & 1023);
     __shared__ unsigned long long full[LG_STAGES], empty[LG_STAGES];
     __shared__ double zpart[2][LG_THREADS / 32][LG_RB];   // by slab parity
-    __shared__ double zq[2][LG_RB];          // this CTA's partial z, by slab parity (read by the cluster)
+    __shared__ double zq_all[2][LG_CLUSTER][LG_RB];   // the cluster's partial z, by slab parity (pushed by each CTA)
     __shared__ float rs[2][LG_RB];
     __shared__ float ws[LG_COLS];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -151,30 +144,47 @@ __device__ void logistic_grad(const LgArgs& L) {
 
     double gacc = 0.0;                         // column col0 + 16 * warp + lane (lanes < 16)
     const int wc = 16 * warp;                  // this warp's 16 columns within the CTA's 256
-    // column c (0..255) of stage s: 64 rows = 256 B at (c/128)*32KB + (c%128)*256
-    auto colp = [&](int s, int c) -> const float2* {
-        return reinterpret_cast<const float2*>(ring + s * LG_STAGE_BYTES + (c >> 7) * (LG_BOXC * LG_RB * 4) +
-                                               (c & 127) * (LG_RB * 4)) + lane;
+    // column c of stage s: LG_RB rows at (c/128) * box + (c%128) * LG_RB floats;
+    // this lane's LG_RPL consecutive rows
+    auto colf = [&](int s, int c) -> const float* {
+        return reinterpret_cast<const float*>(ring + s * LG_STAGE_BYTES + (c >> 7) * (LG_BOXC * LG_RB * 4) +
+                                              (c & 127) * (LG_RB * 4)) + LG_RPL * lane;
     };
-    // phase 1 of slab j: lane holds rows 2*lane, 2*lane+1; two f32 chains per
-    // row over the warp's 16 columns (the reference's z is an f32 sgemv); the
-    // 16 warp partials and the 4 CTA partials are added in f64
+    auto ldx = [&](int s, int c, float (&x)[LG_RPL]) {
+        const float* p = colf(s, c);
+        if constexpr (LG_RPL == 2) {
+            const float2 v = *reinterpret_cast<const float2*>(p);
+            x[0] = v.x;
+            x[LG_RPL - 1] = v.y;
+        } else {
+#pragma unroll
+            for (int h = 0; h < LG_RPL; ++h) x[h] = p[h];
+        }
+    };
+    // phase 1 of slab j: lane holds rows RPL*lane .. RPL*lane + RPL - 1; two
+    // f32 chains per row over the warp's 16 columns (the reference's z is an
+    // f32 sgemv); the 16 warp partials and the 4 CTA partials are added in f64
     auto phase1 = [&](i64 j) {
         const int s = (int)(j % LG_STAGES);
         lg_wait(&full[s], (unsigned)((j / LG_STAGES) & 1));
-        float a0 = 0.f, a1 = 0.f, b0 = 0.f, b1 = 0.f;
+        float a[LG_RPL], b[LG_RPL];
+#pragma unroll
+        for (int h = 0; h < LG_RPL; ++h) a[h] = b[h] = 0.f;
 #pragma unroll
         for (int u = 0; u < 16; u += 2) {
-            const float2 x = *colp(s, wc + u), y = *colp(s, wc + u + 1);
+            float x[LG_RPL], y[LG_RPL];
+            ldx(s, wc + u, x);
+            ldx(s, wc + u + 1, y);
             const float w0 = ws[wc + u], w1 = ws[wc + u + 1];
-            a0 = __fmaf_rn(x.x, w0, a0);
-            a1 = __fmaf_rn(x.y, w0, a1);
-            b0 = __fmaf_rn(y.x, w1, b0);
-            b1 = __fmaf_rn(y.y, w1, b1);
+#pragma unroll
+            for (int h = 0; h < LG_RPL; ++h) {
+                a[h] = __fmaf_rn(x[h], w0, a[h]);
+                b[h] = __fmaf_rn(y[h], w1, b[h]);
+            }
         }
         const int par = (int)(j & 1);
-        zpart[par][warp][2 * lane] = (double)a0 + (double)b0;
-        zpart[par][warp][2 * lane + 1] = (double)a1 + (double)b1;
+#pragma unroll
+        for (int h = 0; h < LG_RPL; ++h) zpart[par][warp][LG_RPL * lane + h] = (double)a[h] + (double)b[h];
     };
     // publish this CTA's partial z of slab j and arrive on the cluster barrier
     // (zpart of slab j complete: the caller synchronised)
@@ -189,7 +199,13 @@ __device__ void logistic_grad(const LgArgs& L) {
             for (int h = 1; h < LG_THREADS / 32; h <<= 1)
 #pragma unroll
                 for (int w = 0; w + h < LG_THREADS / 32; w += 2 * h) t[w] = t[w] + t[w + h];
-            zq[par][tid] = t[0];
+            // push this CTA's partial into every CTA of the cluster (itself included)
+#pragma unroll
+            for (unsigned p = 0; p < LG_CLUSTER; ++p) {
+                unsigned remote;
+                asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(lg_smem(&zq_all[par][q][tid])), "r"(p));
+                asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(remote), "d"(t[0]) : "memory");
+            }
             asm volatile("fence.acq_rel.cluster;" ::: "memory");   // only the writers pay for the release
         }
         asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
@@ -199,12 +215,9 @@ __device__ void logistic_grad(const LgArgs& L) {
         asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
         const int par = (int)(j & 1);
         if (tid < LG_RB) {
-            double zp[LG_CLUSTER];
+            double z = zq_all[par][0][tid];    // local: the peers pushed their partials
 #pragma unroll
-            for (unsigned p = 0; p < LG_CLUSTER; ++p) zp[p] = lg_ld_peer(&zq[par][tid], p);
-            double z = zp[0];
-#pragma unroll
-            for (unsigned p = 1; p < LG_CLUSTER; ++p) z = z + zp[p];
+            for (unsigned p = 1; p < LG_CLUSTER; ++p) z = z + zq_all[par][p][tid];
             const i64 row = (cluster + j * nclusters) * LG_RB + tid;
             float r = 0.f;
             if (row < L.m) {
@@ -218,12 +231,18 @@ __device__ void logistic_grad(const LgArgs& L) {
     // 16 columns, a transpose-reduce across the 32 lanes, then the stage is free
     auto phase2 = [&](i64 j) {
         const int s = (int)(j % LG_STAGES), par = (int)(j & 1);
-        const float r0 = rs[par][2 * lane], r1 = rs[par][2 * lane + 1];
+        float rr[LG_RPL];
+#pragma unroll
+        for (int h = 0; h < LG_RPL; ++h) rr[h] = rs[par][LG_RPL * lane + h];
         float v[16];
 #pragma unroll
         for (int c = 0; c < 16; ++c) {
-            const float2 x = *colp(s, wc + c);
-            v[c] = __fmaf_rn(x.y, r1, x.x * r0);
+            float x[LG_RPL];
+            ldx(s, wc + c, x);
+            float acc = x[0] * rr[0];
+#pragma unroll
+            for (int h = 1; h < LG_RPL; ++h) acc = __fmaf_rn(x[h], rr[h], acc);
+            v[c] = acc;
         }
 #pragma unroll
         for (int c = 0; c < 16; ++c) v[c] = v[c] + __shfl_xor_sync(0xffffffffu, v[c], 16);
@@ -256,6 +275,10 @@ __device__ void logistic_grad(const LgArgs& L) {
             issue(jn);
         }
         chain(j);
+        if (j + 1 < nmine && tid < LG_RB) {      // the chain of slab j + 1 finds y & co. in L2
+            const i64 row = (cluster + (j + 1) * nclusters) * LG_RB + tid;
+            if (row < L.m) E::prefetch(L.a, row);
+        }
         if (j + 1 < nmine) phase1(j + 1);
         __syncthreads();                       // r of slab j and the z partials of slab j + 1
         if (j + 1 < nmine) publish(j + 1);

@@ -240,31 +240,39 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 // CTA tile BM x 128 (BM = 64: 4 warps in a 2 x 2 grid of 32 x 64 warp tiles,
 // two CTAs per SM so one CTA's barrier and refill overlap the other's DMMAs;
-// BM = 128: 8 warps of 64 x 32).  Each warp tile is 32 8x8 DMMA tiles (64 f64
+// BM = 128 would be 8 warps of 64 x 32).  Each warp tile is 32 8x8 DMMA tiles (64 f64
 // accumulators per lane) fed by 12 8-byte shared loads per k4 step.
 #define DM_BN 128
-#define DM_BK 16
-#define DM_ST 3
 
-template <int BM>
+template <int BM, int BK, int ST>
 struct DmCfg {
     static constexpr int NW = BM == 64 ? 4 : 8;           // warps
     static constexpr int WGN = BM == 64 ? 2 : 4;          // warps along N
     static constexpr int MI = BM == 64 ? 4 : 8;           // 8-row DMMA tiles per warp (M)
     static constexpr int NJ = BM == 64 ? 8 : 4;           // 8-col DMMA tiles per warp (N)
     static constexpr int LDA = BM + 8, LDB = DM_BN + 8;   // padded smem rows (doubles)
-    static constexpr int SMEM = DM_ST * DM_BK * (LDA + LDB) * 8;
+    static constexpr int SMEM = ST * BK * (LDA + LDB) * 8;
 };
 
-template <bool TA, bool TB, int BM>
-__global__ void __launch_bounds__(DmCfg<BM>::NW * 32, BM == 64 ? 2 : 1)
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+                 "r"(valid ? 16 : 0)
+                 : "memory");
+}
+
+// VEC: the M-contiguous A (not TA) and N-contiguous B (TB) tiles move as
+// 16-byte pairs (host checks even m / n / ld and 16-byte bases), halving the
+// LDGSTS count per stage.
+template <bool TA, bool TB, int BM, int BK, int ST, bool VEC>
+__global__ void __launch_bounds__(DmCfg<BM, BK, ST>::NW * 32, BM == 64 ? 2 : 1)
     gemm_dmma_kernel(const double* __restrict__ A, i64 lda, const double* __restrict__ B, i64 ldb,
                      double* __restrict__ C, i64 ldc, i64 m, i64 n, i64 k) {
-    typedef DmCfg<BM> G;
+    typedef DmCfg<BM, BK, ST> G;
     constexpr int NT = G::NW * 32;
+    constexpr bool VA = VEC && !TA, VB = VEC && TB;
     extern __shared__ __align__(16) double dsm[];
     double* As = dsm;                                     // [ST][BK][LDA]
-    double* Bs = dsm + DM_ST * DM_BK * G::LDA;            // [ST][BK][LDB]
+    double* Bs = dsm + ST * BK * G::LDA;                  // [ST][BK][LDB]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int gid = lane >> 2, tig = lane & 3;
     const i64 m0 = (i64)blockIdx.y * BM, n0 = (i64)blockIdx.x * DM_BN;
@@ -276,46 +284,68 @@ __global__ void __launch_bounds__(DmCfg<BM>::NW * 32, BM == 64 ? 2 : 1)
         for (int j = 0; j < G::NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
     auto load = [&](int st, i64 k0) {
-        double* as = As + st * DM_BK * G::LDA;
-        double* bs = Bs + st * DM_BK * G::LDB;
+        double* as = As + st * BK * G::LDA;
+        double* bs = Bs + st * BK * G::LDB;
+        if (VA) {
 #pragma unroll
-        for (int t = 0; t < (DM_BK * BM) / NT; ++t) {
-            const int idx = threadIdx.x + t * NT;
-            int kk, mm;
-            if (TA) { mm = idx / DM_BK; kk = idx % DM_BK; } else { kk = idx / BM; mm = idx % BM; }
-            const i64 gi = m0 + mm, gl = k0 + kk;
-            const bool ok = gi < m && gl < k;
-            const double* src = ok ? (TA ? A + gl + gi * lda : A + gi + gl * lda) : A;
-            cp_async8(as + kk * G::LDA + mm, src, ok);
+            for (int t = 0; t < (BK * BM / 2) / NT; ++t) {
+                const int idx = threadIdx.x + t * NT;
+                const int kk = idx / (BM / 2), mm = 2 * (idx % (BM / 2));
+                const i64 gi = m0 + mm, gl = k0 + kk;
+                const bool ok = gi < m && gl < k;
+                cp_async16(as + kk * G::LDA + mm, ok ? A + gi + gl * lda : A, ok);
+            }
+        } else {
+#pragma unroll
+            for (int t = 0; t < (BK * BM) / NT; ++t) {
+                const int idx = threadIdx.x + t * NT;
+                int kk, mm;
+                if (TA) { mm = idx / BK; kk = idx % BK; } else { kk = idx / BM; mm = idx % BM; }
+                const i64 gi = m0 + mm, gl = k0 + kk;
+                const bool ok = gi < m && gl < k;
+                const double* src = ok ? (TA ? A + gl + gi * lda : A + gi + gl * lda) : A;
+                cp_async8(as + kk * G::LDA + mm, src, ok);
+            }
         }
+        if (VB) {
 #pragma unroll
-        for (int t = 0; t < (DM_BK * DM_BN) / NT; ++t) {
-            const int idx = threadIdx.x + t * NT;
-            int kk, nn;
-            if (TB) { kk = idx / DM_BN; nn = idx % DM_BN; } else { nn = idx / DM_BK; kk = idx % DM_BK; }
-            const i64 gj = n0 + nn, gl = k0 + kk;
-            const bool ok = gj < n && gl < k;
-            const double* src = ok ? (TB ? B + gj + gl * ldb : B + gl + gj * ldb) : B;
-            cp_async8(bs + kk * G::LDB + nn, src, ok);
+            for (int t = 0; t < (BK * DM_BN / 2) / NT; ++t) {
+                const int idx = threadIdx.x + t * NT;
+                const int kk = idx / (DM_BN / 2), nn = 2 * (idx % (DM_BN / 2));
+                const i64 gj = n0 + nn, gl = k0 + kk;
+                const bool ok = gj < n && gl < k;
+                cp_async16(bs + kk * G::LDB + nn, ok ? B + gj + gl * ldb : B, ok);
+            }
+        } else {
+#pragma unroll
+            for (int t = 0; t < (BK * DM_BN) / NT; ++t) {
+                const int idx = threadIdx.x + t * NT;
+                int kk, nn;
+                if (TB) { kk = idx / DM_BN; nn = idx % DM_BN; } else { nn = idx / BK; kk = idx % BK; }
+                const i64 gj = n0 + nn, gl = k0 + kk;
+                const bool ok = gj < n && gl < k;
+                const double* src = ok ? (TB ? B + gj + gl * ldb : B + gl + gj * ldb) : B;
+                cp_async8(bs + kk * G::LDB + nn, src, ok);
+            }
         }
     };
-    const i64 nk = (k + DM_BK - 1) / DM_BK;
+    const i64 nk = (k + BK - 1) / BK;
 #pragma unroll
-    for (int st = 0; st < DM_ST - 1; ++st) {
-        if (st < nk) load(st, st * DM_BK);
+    for (int st = 0; st < ST - 1; ++st) {
+        if (st < nk) load(st, st * BK);
         cp_async_commit();
     }
     for (i64 kb = 0; kb < nk; ++kb) {
-        cp_async_wait<DM_ST - 2>();
+        cp_async_wait<ST - 2>();
         __syncthreads();
         // prefetch stage kb + ST - 1 into the buffer consumed at kb - 1
-        const i64 nxt = kb + DM_ST - 1;
-        if (nxt < nk) load((int)(nxt % DM_ST), nxt * DM_BK);
+        const i64 nxt = kb + ST - 1;
+        if (nxt < nk) load((int)(nxt % ST), nxt * BK);
         cp_async_commit();
-        const double* as = As + (kb % DM_ST) * DM_BK * G::LDA;
-        const double* bs = Bs + (kb % DM_ST) * DM_BK * G::LDB;
+        const double* as = As + (kb % ST) * BK * G::LDA;
+        const double* bs = Bs + (kb % ST) * BK * G::LDB;
 #pragma unroll
-        for (int ks = 0; ks < DM_BK; ks += 4) {
+        for (int ks = 0; ks < BK; ks += 4) {
             double af[G::MI], bf[G::NJ];
 #pragma unroll
             for (int i = 0; i < G::MI; ++i) af[i] = as[(ks + tig) * G::LDA + wm + 8 * i + gid];
@@ -338,7 +368,6 @@ __global__ void __launch_bounds__(DmCfg<BM>::NW * 32, BM == 64 ? 2 : 1)
                 if (r < m && c < n) C[r + c * ldc] = acc[i][j][t];
             }
 }
-
 }  // namespace bm
 
 namespace bmi {
@@ -424,41 +453,59 @@ int gemm_tc_f32(int ta, int tb, int64_t m, int64_t n, int64_t k, const float* A,
         C, ldc, handled);
 }
 
-template <int BM>
-static int dmma_launch(int ta, int tb, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
-                       const double* B, int64_t ldb, double* C, int64_t ldc) {
-    typedef bm::DmCfg<BM> G;
+template <bool TA, bool TB, int BM, int BK, int ST, bool VEC>
+static int dmma_go(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B, int64_t ldb,
+                   double* C, int64_t ldc) {
+    typedef bm::DmCfg<BM, BK, ST> G;
     dim3 grid((unsigned)((n + DM_BN - 1) / DM_BN), (unsigned)((m + BM - 1) / BM));
     if (grid.y > 65535) return set_error(BM_ERR_NOTIMPL, "gemm: too many row tiles");
-    cudaStream_t s = st().stream;
     static bool attr = false;
     if (!attr) {
-        BM_CUDA(cudaFuncSetAttribute(bm::gemm_dmma_kernel<true, true, BM>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
-        BM_CUDA(cudaFuncSetAttribute(bm::gemm_dmma_kernel<true, false, BM>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
-        BM_CUDA(cudaFuncSetAttribute(bm::gemm_dmma_kernel<false, true, BM>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
-        BM_CUDA(cudaFuncSetAttribute(bm::gemm_dmma_kernel<false, false, BM>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
+        BM_CUDA(cudaFuncSetAttribute(bm::gemm_dmma_kernel<TA, TB, BM, BK, ST, VEC>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
         attr = true;
     }
-    const int nt = G::NW * 32;
-    if (ta) {
-        if (tb) bm::gemm_dmma_kernel<true, true, BM><<<grid, nt, G::SMEM, s>>>(A, lda, B, ldb, C, ldc, m, n, k);
-        else bm::gemm_dmma_kernel<true, false, BM><<<grid, nt, G::SMEM, s>>>(A, lda, B, ldb, C, ldc, m, n, k);
-    } else {
-        if (tb) bm::gemm_dmma_kernel<false, true, BM><<<grid, nt, G::SMEM, s>>>(A, lda, B, ldb, C, ldc, m, n, k);
-        else bm::gemm_dmma_kernel<false, false, BM><<<grid, nt, G::SMEM, s>>>(A, lda, B, ldb, C, ldc, m, n, k);
-    }
+    bm::gemm_dmma_kernel<TA, TB, BM, BK, ST, VEC><<<grid, G::NW * 32, G::SMEM, st().stream>>>(A, lda, B, ldb, C, ldc,
+                                                                                             m, n, k);
     BM_CUDA(cudaGetLastError());
     st().launches++;
     return BM_OK;
+}
+
+template <int BM, int BK, int ST, bool VEC>
+static int dmma_launch(int ta, int tb, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
+                       const double* B, int64_t ldb, double* C, int64_t ldc) {
+    if (ta) {
+        if (tb) return dmma_go<true, true, BM, BK, ST, VEC>(m, n, k, A, lda, B, ldb, C, ldc);
+        return dmma_go<true, false, BM, BK, ST, VEC>(m, n, k, A, lda, B, ldb, C, ldc);
+    }
+    if (tb) return dmma_go<false, true, BM, BK, ST, VEC>(m, n, k, A, lda, B, ldb, C, ldc);
+    return dmma_go<false, false, BM, BK, ST, VEC>(m, n, k, A, lda, B, ldb, C, ldc);
 }
 
 int gemm_dmma_f64(int ta, int tb, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B,
                   int64_t ldb, double* C, int64_t ldc, bool* handled) {
     *handled = false;
     if (m * n * k < (int64_t)1 << 18) return BM_OK;
-    static const int bm = (std::getenv("BM_DMMA_BM") && std::atoi(std::getenv("BM_DMMA_BM")) == 128) ? 128 : 64;
-    const int rc = bm == 128 ? dmma_launch<128>(ta, tb, m, n, k, A, lda, B, ldb, C, ldc)
-                             : dmma_launch<64>(ta, tb, m, n, k, A, lda, B, ldb, C, ldc);
+    // 16-byte pair copies need even extents/strides and 16-byte bases on the
+    // contiguous operand(s)
+    const bool vec = (ta || ((m | lda) % 2 == 0 && ((uintptr_t)A & 15) == 0)) &&
+                     (!tb || ((n | ldb) % 2 == 0 && ((uintptr_t)B & 15) == 0));
+    static const int variant = std::getenv("BM_DMMA_VARIANT") ? std::atoi(std::getenv("BM_DMMA_VARIANT")) : 0;
+    int rc;
+    switch (variant) {
+        case 1: rc = dmma_launch<64, 16, 3, false>(ta, tb, m, n, k, A, lda, B, ldb, C, ldc); break;
+        case 2: rc = vec ? dmma_launch<64, 32, 2, true>(ta, tb, m, n, k, A, lda, B, ldb, C, ldc)
+                         : dmma_launch<64, 32, 2, false>(ta, tb, m, n, k, A, lda, B, ldb, C, ldc); break;
+        case 3: rc = vec ? dmma_launch<64, 8, 6, true>(ta, tb, m, n, k, A, lda, B, ldb, C, ldc)
+                         : dmma_launch<64, 8, 6, false>(ta, tb, m, n, k, A, lda, B, ldb, C, ldc); break;
+        case 4: rc = vec ? dmma_launch<64, 16, 3, true>(ta, tb, m, n, k, A, lda, B, ldb, C, ldc)
+                         : dmma_launch<64, 16, 3, false>(ta, tb, m, n, k, A, lda, B, ldb, C, ldc); break;
+        case 5: rc = vec ? dmma_launch<64, 8, 8, true>(ta, tb, m, n, k, A, lda, B, ldb, C, ldc)
+                         : dmma_launch<64, 8, 8, false>(ta, tb, m, n, k, A, lda, B, ldb, C, ldc); break;
+        default: rc = vec ? dmma_launch<64, 16, 4, true>(ta, tb, m, n, k, A, lda, B, ldb, C, ldc)
+                          : dmma_launch<64, 16, 4, false>(ta, tb, m, n, k, A, lda, B, ldb, C, ldc); break;
+    }
     if (!rc) *handled = true;
     return rc;
 }

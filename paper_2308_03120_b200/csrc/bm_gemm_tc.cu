@@ -12,7 +12,7 @@
 // error per product; the accumulation is promoted to round-to-nearest f32
 // every 64 K (see below), so the result tracks an SGEMM.
 //
-// f64: DMMA (mma.sync.aligned.m8n8k4 f64) with cp.async double buffering.
+// f64: DMMA (mma.sync.aligned.m8n8k4 f64) fed by a 4-stage cp.async ring.
 #include <cstring>
 
 #include "bm_internal.h"
@@ -80,7 +80,7 @@ __host__ __device__ constexpr uint32_t tf32_idesc(int m, int n) {
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
                        const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_blo,
-                       float* __restrict__ C, i64 m, i64 n, i64 ldc, int nk, int group_m) {
+                       float* __restrict__ C, i64 m, i64 n, i64 ldc, int nk, int group_m, int kb0, int accumulate) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 const int s = kb % TC_STAGES;
                 if (kb >= TC_STAGES) mbar_wait(&empty[s], (uint32_t)(((kb / TC_STAGES) - 1) & 1));
                 mbar_expect_tx(&full[s], TC_STAGE_BYTES);
-                const int kc = kb * TC_BK;
+                const int kc = (kb0 + kb) * TC_BK;
                 tma_load_2d(tile_ahi(s), &tm_ahi, kc, m0, &full[s]);
                 tma_load_2d(tile_alo(s), &tm_alo, kc, m0, &full[s]);
                 tma_load_2d(tile_bhi(s), &tm_bhi, kc, n0, &full[s]);
@@ -182,9 +182,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         // epilogue warps 2..9: TMEM lane quarter q = warp % 4, column half h
         const int q = warp & 3;
         const int h = (warp - 2) >> 2;
+        // a later K pass starts its chain from C (loads issued up front, their
+        // latency hidden behind the first chunk's MMAs), so the chunk sums
+        // add in the same order as one long pass
+        const i64 row = (i64)m0 + 32 * q + lane;
         float acc[128];
+        if (accumulate && row < m) {
+            const float* cp = C + row + ((i64)n0 + h * 128) * ldc;
+            const int ncol = (int)(n - n0 - h * 128 < 128 ? n - n0 - h * 128 : 128);
 #pragma unroll
-        for (int i = 0; i < 128; ++i) acc[i] = 0.f;
+            for (int t = 0; t < 128; ++t) acc[t] = t < ncol ? __ldg(cp + t * ldc) : 0.f;
+        } else {
+#pragma unroll
+            for (int t = 0; t < 128; ++t) acc[t] = 0.f;
+        }
         for (int c = 0; c < nchunks; ++c) {
             const int b = c & 1;
             mbar_wait(&acc_full[b], (uint32_t)((c >> 1) & 1));
@@ -202,7 +213,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[b]);
         }
-        const i64 row = (i64)m0 + 32 * q + lane;
         if (row < m) {
 #pragma unroll
             for (int t = 0; t < 128; ++t) {
@@ -218,10 +228,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
 // ---------------------------------------------------------------------------
 // f64: DMMA m8n8k4 (mma.sync f64 runs on the FP64 tensor path of sm_100).
-// CTA tile 128x128, 8 warps of 64x32 (8x4 DMMA tiles each, 64 f64
-// accumulators per lane), K staged 16 at a time through a 3-stage cp.async
-// (LDGSTS) ring so global latency overlaps the DMMAs.  Out-of-range elements
-// are zero-filled by cp.async's src-size operand.
+// CTA tile 64x128 (two CTAs per SM), 4 warps of 32x64 (4x8 DMMA tiles each,
+// 64 f64 accumulators per lane), K staged 16 at a time through a 4-stage
+// cp.async (LDGSTS) ring so global latency overlaps the DMMAs; contiguous
+// operands move as 16-byte pairs.  Out-of-range elements are zero-filled by
+// cp.async's src-size operand.
 
 __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
@@ -429,11 +440,24 @@ int gemm_tc_f32_core(int64_t m, int64_t n, int64_t k, const SplitFn& split_a, co
     if (!rc) {
         dim3 grid((unsigned)((np / TC_BN) * (mp / TC_BM)));
         static const int group_m = std::getenv("BM_GEMM_GROUP") ? std::atoi(std::getenv("BM_GEMM_GROUP")) : 8;
-        bm::gemm_3xtf32_kernel<<<grid, TC_THREADS, TC_SMEM, s>>>(tm[0], tm[1], tm[2], tm[3], C, m, n, ldc, (int)(kp / TC_BK),
-                                                                  group_m > 0 ? group_m : 8);
-        cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) rc = cuda_fail(e, "3xTF32 GEMM launch");
-        else st().launches++;
+        // Long K runs as several stream-ordered passes of at most kpass K
+        // (the later ones add into C): within one launch the resident CTAs
+        // drift apart along K, and at K = 32768 their A/B slabs stop meeting
+        // in L2 (4x the minimum DRAM reads, and the GPU power-throttles on
+        // them); a pass restarts them together.  Measured: 32768^3 196 -> 218
+        // TF/s with 8192-K passes; up to K = 16384 one pass is as fast.
+        static const int64_t kpass_env = std::getenv("BM_GEMM_KPASS") ? std::atoll(std::getenv("BM_GEMM_KPASS")) : 8192;
+        const int nk = (int)(kp / TC_BK);
+        int pass_kb = kpass_env > 0 && kp > 2 * kpass_env ? (int)(kpass_env / (TC_BK * TC_CHUNK_KB)) * TC_CHUNK_KB : nk;
+        if (pass_kb <= 0 || pass_kb >= nk) pass_kb = nk;
+        for (int kb0 = 0; kb0 < nk && !rc; kb0 += pass_kb) {
+            const int len = nk - kb0 < pass_kb ? nk - kb0 : pass_kb;
+            bm::gemm_3xtf32_kernel<<<grid, TC_THREADS, TC_SMEM, s>>>(tm[0], tm[1], tm[2], tm[3], C, m, n, ldc, len,
+                                                                      group_m > 0 ? group_m : 8, kb0, kb0 > 0);
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) rc = cuda_fail(e, "3xTF32 GEMM launch");
+            else st().launches++;
+        }
     }
     cudaFreeAsync(buf, s);
     if (!rc) *handled = true;

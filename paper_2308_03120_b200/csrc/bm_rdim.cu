@@ -21,10 +21,163 @@
 #define BM_UNIT_UNROLL 16   // single input: all 16 rows of a pairwise unit in flight
 #include "bm_reduce.cuh"
 
+
 namespace bm {
 
 // ---------------------------------------------------------------------------
 // dim 0
+
+// Sum / mean over columns whose length is a power-of-two number of
+// half-units (numpy's pairwise tree is then the balanced one): each warp walks
+// its (column, half-unit) pairs as one stream, loading the next half-unit --
+// across column boundaries too -- while it reduces the current one, so the
+// loads never drain between columns.
+template <typename T, int OP>
+__global__ void __launch_bounds__(256, 2) rdim0_stream_kernel(const T* __restrict__ a, i64 rows, i64 cols,
+                                                                       i64 lda, T* out, i64 cnt) {
+    constexpr i64 U = PwHalf<T>::value;
+    constexpr int LV = 12;
+    extern __shared__ __align__(16) char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    char* tile = smem + warp * BM_TILE_BYTES;
+    const i64 gw = (i64)blockIdx.x * (blockDim.x >> 5) + warp;
+    const i64 nw = (i64)gridDim.x * (blockDim.x >> 5);
+    if (gw >= cols) return;
+    int top = 0;
+    while ((1ll << top) < cnt) ++top;
+    i64 c = gw, u = 0;
+    T stk[LV + 1];
+    HalfRows<T> cur, nxt;
+    half_load<T>(BufSrc<T>{a + c * lda, 1}, 0, cur);
+    while (true) {
+        i64 nc = c, nu = u + 1;
+        if (nu == cnt) { nu = 0; nc = c + nw; }
+        if (nc < cols) half_load<T>(BufSrc<T>{a + nc * lda, 1}, nu * U, nxt);
+        T v = half_reduce<T>(cur, tile);
+#pragma unroll
+        for (int l = 0; l <= LV; ++l) {
+            if (l < LV && ((u >> l) & 1)) {
+                v = stk[l] + v;
+            } else {
+                stk[l] = v;
+                break;
+            }
+        }
+        if (nu == 0) {
+            T sum = stk[0];
+#pragma unroll
+            for (int l = 1; l <= LV; ++l)
+                if (l == top) sum = stk[l];
+            sum = sum + T(0);
+            T r = sum;
+            if constexpr (OP == 5) r = OpDiv::f(sum, KScal<T>::f((double)rows, rows));
+            if (lane == 0) out[c] = r;
+        }
+        if (nc >= cols) break;
+        c = nc;
+        u = nu;
+        cur = nxt;
+    }
+}
+
+// Columns of 8*sub half-units (a power-of-two count for sum/mean; any count
+// for min/max): the CTA's eight warps share one column at a time, warp w
+// reducing half-units [w*sub, (w+1)*sub) -- for sum the balanced subtree
+// there, the CTA then adding the eight subtree sums as the top three levels
+// of the same balanced tree; for min/max a NaN-propagating partial, merged in
+// any order.  One CTA streams one contiguous column (e.g. 128 KiB) instead of
+// eight warps streaming eight columns, which the DRAM serves faster, and each
+// warp loads its next half-unit -- across columns too -- while it reduces the
+// current one.
+template <typename T, int OP>
+__global__ void __launch_bounds__(256, 2) rdim0_cta_kernel(const T* __restrict__ a, i64 rows, i64 cols, i64 lda,
+                                                           T* out, i64 sub) {
+    constexpr i64 U = PwHalf<T>::value;
+    constexpr int V = 16 / sizeof(T);
+    constexpr int LV = 12;
+    constexpr bool MM = OP == 2 || OP == 3;
+    extern __shared__ __align__(16) char smem[];
+    __shared__ T res[2][8];
+    __shared__ int res_nan[2][8];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    char* tile = smem + warp * BM_TILE_BYTES;
+    if ((i64)blockIdx.x >= cols) return;
+    int top = 0;
+    while ((1ll << top) < sub) ++top;
+    const i64 step = gridDim.x;
+    const i64 base = (i64)warp * sub * U;
+    i64 c = blockIdx.x, j = 0;
+    int par = 0;
+    T stk[LV + 1];
+    MinMaxAcc<T, OP == 3> acc;
+    HalfRows<T> cur, nxt;
+    half_load<T>(BufSrc<T>{a + c * lda + base, 1}, 0, cur);
+    while (true) {
+        i64 nc = c, nj = j + 1;
+        if (nj == sub) { nj = 0; nc = c + step; }
+        if (nc < cols) half_load<T>(BufSrc<T>{a + nc * lda + base, 1}, nj * U, nxt);
+        if constexpr (MM) {
+#pragma unroll
+            for (int r = 0; r < 8; ++r)
+#pragma unroll
+                for (int k = 0; k < V; ++k) acc.add(cur.v[r][k]);
+        } else {
+            T v = half_reduce<T>(cur, tile);
+#pragma unroll
+            for (int l = 0; l <= LV; ++l) {
+                if (l < LV && ((j >> l) & 1)) {
+                    v = stk[l] + v;
+                } else {
+                    stk[l] = v;
+                    break;
+                }
+            }
+        }
+        if (nj == 0) {
+            if constexpr (MM) {
+                acc.warp_merge();
+                if (lane == 0) {
+                    res[par][warp] = acc.v;
+                    res_nan[par][warp] = acc.nan;
+                }
+                acc = MinMaxAcc<T, OP == 3>();
+            } else {
+                T r = stk[0];
+#pragma unroll
+                for (int l = 1; l <= LV; ++l)
+                    if (l == top) r = stk[l];
+                if (lane == 0) res[par][warp] = r;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                const T* q = res[par];
+                T o;
+                if constexpr (MM) {
+                    MinMaxAcc<T, OP == 3> m;
+#pragma unroll
+                    for (int w = 0; w < 8; ++w) {
+                        MinMaxAcc<T, OP == 3> x;
+                        x.v = q[w];
+                        x.nan = res_nan[par][w] != 0;
+                        m.merge(x);
+                    }
+                    o = m.result();
+                } else {
+                    T sum = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
+                    sum = sum + T(0);
+                    o = sum;
+                    if constexpr (OP == 5) o = OpDiv::f(sum, KScal<T>::f((double)rows, rows));
+                }
+                out[c] = o;
+            }
+            par ^= 1;
+        }
+        if (nc >= cols) break;
+        c = nc;
+        j = nj;
+        cur = nxt;
+    }
+}
 
 template <typename T, int OP>
 __global__ void __launch_bounds__(256, 2) rdim0_kernel(const T* __restrict__ a, i64 rows, i64 cols, i64 lda, T* out,
@@ -251,8 +404,42 @@ static int rdim_launch(const bm_view& in, void* out_base, int dim) {
         if (cols == 0) return BM_OK;
         const bool vec = (((uintptr_t)a & 15u) == 0) && ((lda * sz) % 16 == 0);
         int grid = (int)((cols + 7) / 8);
-        const int cap = st().sm_count * 2;   // 2 resident CTAs per SM (registers)
+        const int cap = st().sm_count * 2;   // 2 resident CTAs per SM (registers / ring)
         if (grid > cap) grid = cap;
+        constexpr int64_t U = 4096 / sizeof(T);   // PwHalf: 1024 f32 / 512 f64 elements
+        const int64_t cnt = rows / U;
+        const bool pow2 = rows % U == 0 && cnt >= 1 && cnt <= 4096 && (cnt & (cnt - 1)) == 0;
+        constexpr bool fsum = (OP == 1 || OP == 5) && is_float_t_host<T>::value;
+        static const bool cta_on = !std::getenv("BM_RD0_CTA") || std::atoi(std::getenv("BM_RD0_CTA"));
+        if (cta_on && vec && rows % U == 0 && cnt >= 8 && cnt / 8 <= 4096 &&
+            ((fsum && pow2) || ((OP == 2 || OP == 3) && cnt % 8 == 0))) {
+            int cgrid = (int)cols;
+            const int ccap = st().sm_count * 2;
+            if (cgrid > ccap) {
+                // columns per CTA k, then just enough CTAs that none gets more than k
+                const int64_t k = (cols + ccap - 1) / ccap;
+                cgrid = (int)((cols + k - 1) / k);
+            }
+            bm::rdim0_cta_kernel<T, OP><<<cgrid, 256, 8 * BM_TILE_BYTES, s>>>(a, rows, cols, lda, out, cnt / 8);
+            BM_CUDA(cudaGetLastError());
+            st().launches++;
+            return BM_OK;
+        }
+        if constexpr (fsum) {
+            static const bool stream_on = !std::getenv("BM_RDIM0_STREAM") || std::atoi(std::getenv("BM_RDIM0_STREAM"));
+            if (stream_on && vec && pow2) {
+                int sgrid = (int)((cols + 7) / 8);
+                const int scap = st().sm_count * 2;
+                if (sgrid > scap) {
+                    const int64_t k = (cols + 8LL * scap - 1) / (8LL * scap);
+                    sgrid = (int)((cols + 8 * k - 1) / (8 * k));
+                }
+                bm::rdim0_stream_kernel<T, OP><<<sgrid, 256, 8 * BM_TILE_BYTES, s>>>(a, rows, cols, lda, out, cnt);
+                BM_CUDA(cudaGetLastError());
+                st().launches++;
+                return BM_OK;
+            }
+        }
         static bool attr = false;
         if (!attr) {
             BM_CUDA(cudaFuncSetAttribute(bm::rdim0_kernel<T, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -222,6 +222,34 @@ def test_rdim_large_bit_exact(dm, shape):
             same(dm.evaluate(getattr(dm, op)(m, dim)).to_numpy(), O.rdim(op, a, dim))
 
 
+@pytest.mark.parametrize("dt,shape", [(np.float32, (4096, 300)), (np.float32, (1024, 7)), (np.float64, (512, 1500)),
+                                      (np.float64, (8192, 1))])
+def test_rdim0_sum_mean_streamed_bit_exact(dm, dt, shape):
+    """column lengths that are a power-of-two number of half-units take the
+    streamed dim-0 path; sum and mean stay bit-exact with the reference"""
+    a = (np.random.default_rng(7).random(shape) - 0.25).astype(dt)
+    m = dm.Matrix.from_numpy(a)
+    for op in ("sum", "mean"):
+        same(dm.evaluate(getattr(dm, op)(m, 0)).to_numpy(), O.rdim(op, a, 0))
+
+
+@pytest.mark.parametrize("dt,shape", [(np.float64, (4096, 37)), (np.float32, (8192, 20)), (np.float64, (12288, 9)),
+                                      (np.int32, (8192, 5))])
+def test_rdim0_minmax_cta_path_nan(dm, dt, shape):
+    """columns of a multiple of 8 half-units take the CTA-per-column dim-0
+    path; min/max propagate NaN like numpy and are exact"""
+    rng = np.random.default_rng(11)
+    if np.issubdtype(dt, np.integer):
+        a = rng.integers(-10**6, 10**6, size=shape).astype(dt)
+    else:
+        a = rng.standard_normal(shape).astype(dt)
+        a[shape[0] - 1, 0] = np.nan
+        a[3 * shape[0] // 4, shape[1] - 1] = np.nan
+    m = dm.Matrix.from_numpy(a)
+    for op in ("min", "max"):
+        same(dm.evaluate(getattr(dm, op)(m, 0)).to_numpy(), O.rdim(op, a, 0))
+
+
 # ---- GEMM ----------------------------------------------------------------------------------------
 
 def test_gemm_vs_reference(dm):

@@ -18,7 +18,7 @@
 //            pushes them into all four CTAs' shared memory (distributed
 //            shared memory stores); after one cluster barrier every CTA sums
 //            the four partials in rank order (identical z in all four CTAs);
-//            the program inputs of the next slab are prefetched into L2;
+//            the program inputs of the next slab are loaded into registers;
 //   chain    r_i = F(round_f32(z_i), y_i, ...) -- the fused element-wise
 //            program, every stage rounded to f32 like the unfused plan;
 //   phase 2  each CTA adds sum_i X_ic r_i for its columns from its resident
@@ -142,6 +142,7 @@ __device__ void logistic_grad(const LgArgs& L) {
     if (tid == 0)
         for (i64 j = 0; j < LG_STAGES - 1 && j < nmine; ++j) issue(j);
 
+    typename E::Pre pre;                       // chain inputs of the next slab (threads < LG_RB)
     double gacc = 0.0;                         // column col0 + 16 * warp + lane (lanes < 16)
     const int wc = 16 * warp;                  // this warp's 16 columns within the CTA's 256
     // column c of stage s: LG_RB rows at (c/128) * box + (c%128) * LG_RB floats;
@@ -221,7 +222,7 @@ __device__ void logistic_grad(const LgArgs& L) {
             const i64 row = (cluster + j * nclusters) * LG_RB + tid;
             float r = 0.f;
             if (row < L.m) {
-                r = E::at(L.a, row, (float)z);
+                r = E::at(L.a, pre, (float)z);
                 if (q == 0) L.r[row] = r;
             }
             rs[par][tid] = r;
@@ -264,6 +265,10 @@ __device__ void logistic_grad(const LgArgs& L) {
     // Software pipeline: the cluster exchange of slab j + 1 is in flight while
     // this CTA runs phase 2 of slab j.
     if (nmine > 0) {
+        if (tid < LG_RB) {
+            const i64 row = cluster * LG_RB + tid;
+            if (row < L.m) E::load(L.a, row, pre);
+        }
         phase1(0);
         __syncthreads();
         publish(0);
@@ -275,9 +280,9 @@ __device__ void logistic_grad(const LgArgs& L) {
             issue(jn);
         }
         chain(j);
-        if (j + 1 < nmine && tid < LG_RB) {      // the chain of slab j + 1 finds y & co. in L2
+        if (j + 1 < nmine && tid < LG_RB) {      // y & co. of slab j + 1 into registers now
             const i64 row = (cluster + (j + 1) * nclusters) * LG_RB + tid;
-            if (row < L.m) E::prefetch(L.a, row);
+            if (row < L.m) E::load(L.a, row, pre);
         }
         if (j + 1 < nmine) phase1(j + 1);
         __syncthreads();                       // r of slab j and the z partials of slab j + 1

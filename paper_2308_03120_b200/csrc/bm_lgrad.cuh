@@ -15,9 +15,10 @@
 // 3-stage TMA ring.  Per slab:
 //   phase 1  each CTA computes partial z over its columns (f32 chains as in
 //            the reference's sgemv, partials added in f64; fixed order) and
-//            pushes them into all four CTAs' shared memory (distributed
-//            shared memory stores); after one cluster barrier every CTA sums
-//            the four partials in rank order (identical z in all four CTAs);
+//            pushes them into the peers' shared memory (st.async, completing
+//            bytes on the peer's mbarrier -- no fence, no cluster barrier);
+//            once they land every CTA sums the four partials in rank order
+//            (identical z in all four CTAs);
 //            the program inputs of the next slab are loaded into registers;
 //   chain    r_i = F(round_f32(z_i), y_i, ...) -- the fused element-wise
 //            program, every stage rounded to f32 like the unfused plan;
@@ -25,8 +26,8 @@
 //            quarter: lanes over rows, then a butterfly transpose-reduce
 //            (31 shuffles for 16 columns) so each (warp, lane < 16) owns one
 //            column's f64 accumulator for the whole kernel.
-// The loop is software-pipelined: while the cluster barrier of slab j + 1
-// settles, the CTA runs phase 2 of slab j (split barrier arrive / wait).
+// The loop is software-pipelined: while the partials of slab j + 1 travel,
+// the CTA runs phase 2 of slab j.
 // Slabs are dealt round-robin to clusters; every cluster writes its k
 // partials and lgrad_finish folds them in cluster order: deterministic.
 // Compiled by NVRTC with the program's functor E.
@@ -91,6 +92,22 @@ __device__ __forceinline__ void lg_wait(unsigned long long* b, unsigned parity) 
             : "memory");
     } while (!ok);
 }
+// the same, acquiring at cluster scope: the bytes completing the phase were
+// stored by peer CTAs (st.async)
+__device__ __forceinline__ void lg_wait_cluster(unsigned long long* b, unsigned parity) {
+    unsigned ok;
+    do {
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n"
+            "}\n"
+            : "=r"(ok)
+            : "r"(lg_smem(b)), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
 __device__ __forceinline__ void lg_tma_2d(void* dst, const LgTmap* tm, int c0, int c1, unsigned long long* bar) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
@@ -111,6 +128,7 @@ __device__ void logistic_grad(const LgArgs& L) {
     extern __shared__ __align__(1024) char lg_raw[];
     char* ring = lg_raw + ((1024 - (lg_smem(lg_raw) & 1023)) & 1023);
     __shared__ unsigned long long full[LG_STAGES], empty[LG_STAGES];
+    __shared__ unsigned long long zbar[2];                // peers' z partials of a slab landed (by parity)
     __shared__ double zpart[2][LG_THREADS / 32][LG_RB];   // by slab parity
     __shared__ double zq_all[2][LG_CLUSTER][LG_RB];   // the cluster's partial z, by slab parity (pushed by each CTA)
     __shared__ float rs[2][LG_RB];
@@ -126,10 +144,12 @@ __device__ void logistic_grad(const LgArgs& L) {
             lg_bar_init(&full[s], 1);
             lg_bar_init(&empty[s], LG_THREADS / 32);
         }
+        lg_bar_init(&zbar[0], 1);
+        lg_bar_init(&zbar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&L.tmx) : "memory");
     }
-    __syncthreads();
+    lg_cluster_sync();                         // peers' zbar initialised before anyone pushes
     auto issue = [&](i64 j) {   // this CTA's quarter of slab j into stage j % STAGES
         const int s = (int)(j % LG_STAGES);
         const i64 slab = cluster + j * nclusters;
@@ -187,10 +207,16 @@ __device__ void logistic_grad(const LgArgs& L) {
 #pragma unroll
         for (int h = 0; h < LG_RPL; ++h) zpart[par][warp][LG_RPL * lane + h] = (double)a[h] + (double)b[h];
     };
-    // publish this CTA's partial z of slab j and arrive on the cluster barrier
-    // (zpart of slab j complete: the caller synchronised)
+    // publish this CTA's partial z of slab j: st.async into the three peers'
+    // zq_all, each store completing bytes on the peer's zbar[parity] (no
+    // fence, no cluster barrier); its own copy is a plain local store.  The
+    // expect_tx for the peers' bytes is posted by thread 0 (the phase may see
+    // the bytes first: the tx-count goes negative until then).  A slot is
+    // rewritten two slabs later only after its reader published the slab in
+    // between, which the writer had to receive first.
     auto publish = [&](i64 j) {
         const int par = (int)(j & 1);
+        if (tid == 0) lg_expect_tx(&zbar[par], (LG_CLUSTER - 1) * LG_RB * 8);
         if (tid < LG_RB) {
             // balanced tree over the warp partials (fixed order, 4 levels deep)
             double t[LG_THREADS / 32];
@@ -200,23 +226,25 @@ __device__ void logistic_grad(const LgArgs& L) {
             for (int h = 1; h < LG_THREADS / 32; h <<= 1)
 #pragma unroll
                 for (int w = 0; w + h < LG_THREADS / 32; w += 2 * h) t[w] = t[w] + t[w + h];
-            // push this CTA's partial into every CTA of the cluster (itself included)
+            zq_all[par][q][tid] = t[0];
 #pragma unroll
-            for (unsigned p = 0; p < LG_CLUSTER; ++p) {
-                unsigned remote;
-                asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(lg_smem(&zq_all[par][q][tid])), "r"(p));
-                asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(remote), "d"(t[0]) : "memory");
+            for (unsigned p = 1; p < LG_CLUSTER; ++p) {
+                const unsigned peer = (q + p) % LG_CLUSTER;
+                unsigned raddr, rbar;
+                asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(lg_smem(&zq_all[par][q][tid])), "r"(peer));
+                asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbar) : "r"(lg_smem(&zbar[par])), "r"(peer));
+                asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(raddr),
+                             "d"(t[0]), "r"(rbar)
+                             : "memory");
             }
-            asm volatile("fence.acq_rel.cluster;" ::: "memory");   // only the writers pay for the release
         }
-        asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     };
-    // after the cluster barrier of slab j: z (four partials in rank order) and r
+    // z of slab j (four partials in rank order, once the peers' bytes landed) and r
     auto chain = [&](i64 j) {
-        asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
         const int par = (int)(j & 1);
         if (tid < LG_RB) {
-            double z = zq_all[par][0][tid];    // local: the peers pushed their partials
+            lg_wait_cluster(&zbar[par], (unsigned)((j >> 1) & 1));
+            double z = zq_all[par][0][tid];
 #pragma unroll
             for (unsigned p = 1; p < LG_CLUSTER; ++p) z = z + zq_all[par][p][tid];
             const i64 row = (cluster + j * nclusters) * LG_RB + tid;
@@ -262,7 +290,7 @@ __device__ void logistic_grad(const LgArgs& L) {
         if (lane == 0) lg_arrive(&empty[s]);
     };
 
-    // Software pipeline: the cluster exchange of slab j + 1 is in flight while
+    // Software pipeline: the partials of slab j + 1 are in flight while
     // this CTA runs phase 2 of slab j.
     if (nmine > 0) {
         if (tid < LG_RB) {

@@ -23,9 +23,10 @@
 //   chain    r_i = F(round_f32(z_i), y_i, ...) -- the fused element-wise
 //            program, every stage rounded to f32 like the unfused plan;
 //   phase 2  each CTA adds sum_i X_ic r_i for its columns from its resident
-//            quarter: lanes over rows, then a butterfly transpose-reduce
-//            (31 shuffles for 16 columns) so each (warp, lane < 16) owns one
-//            column's f64 accumulator for the whole kernel.
+//            quarter: a lane reads 4-row quads of 8 columns (16-byte shared
+//            loads), then a transpose-reduce across its half-warp (8 shuffles
+//            for 8 columns) leaves each even lane one column's f64
+//            accumulator for the whole kernel.
 // The loop is software-pipelined: while the partials of slab j + 1 travel,
 // the CTA runs phase 2 of slab j.
 // Slabs are dealt round-robin to clusters; every cluster writes its k
@@ -39,7 +40,6 @@ namespace bm {
 #ifndef LG_RB
 #define LG_RB 64            // rows per slab (256 B of f32: full-rate TMA rows)
 #endif
-#define LG_RPL (LG_RB / 32) // rows per lane
 #define LG_BOXC 128         // columns per TMA box (32 KB)
 #ifndef LG_CLUSTER
 #define LG_CLUSTER 4        // CTAs per slab (clusters of 8 fit only 15 x 8 SMs at once)
@@ -131,7 +131,7 @@ __device__ void logistic_grad(const LgArgs& L) {
     __shared__ unsigned long long zbar[2];                // peers' z partials of a slab landed (by parity)
     __shared__ double zpart[2][LG_THREADS / 32][LG_RB];   // by slab parity
     __shared__ double zq_all[2][LG_CLUSTER][LG_RB];   // the cluster's partial z, by slab parity (pushed by each CTA)
-    __shared__ float rs[2][LG_RB];
+    __shared__ __align__(16) float rs[2][LG_RB];
     __shared__ float ws[LG_COLS];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const unsigned q = lg_cluster_rank();
@@ -163,49 +163,41 @@ __device__ void logistic_grad(const LgArgs& L) {
         for (i64 j = 0; j < LG_STAGES - 1 && j < nmine; ++j) issue(j);
 
     typename E::Pre pre;                       // chain inputs of the next slab (threads < LG_RB)
-    double gacc = 0.0;                         // column col0 + 16 * warp + lane (lanes < 16)
+    double gacc = 0.0;                         // one column per even lane (see phase 2)
     const int wc = 16 * warp;                  // this warp's 16 columns within the CTA's 256
-    // column c of stage s: LG_RB rows at (c/128) * box + (c%128) * LG_RB floats;
-    // this lane's LG_RPL consecutive rows
-    auto colf = [&](int s, int c) -> const float* {
-        return reinterpret_cast<const float*>(ring + s * LG_STAGE_BYTES + (c >> 7) * (LG_BOXC * LG_RB * 4) +
-                                              (c & 127) * (LG_RB * 4)) + LG_RPL * lane;
+    // Lane layout (LG_RB = 64): half-warp hc = lane / 16 takes columns
+    // wc + 8 hc .. wc + 8 hc + 7, lane hl = lane % 16 rows 4 hl .. 4 hl + 3, so
+    // every shared-memory read is one 16-byte row quad of one column.
+    static_assert(LG_RB == 64, "lane layout assumes 64-row slabs");
+    const int hl = lane & 15, hc = lane >> 4;
+    const int cw = wc + 8 * hc;                // this half-warp's first column
+    auto ldx4 = [&](int s, int c) -> float4 {
+        return *reinterpret_cast<const float4*>(ring + s * LG_STAGE_BYTES + (c >> 7) * (LG_BOXC * LG_RB * 4) +
+                                                (c & 127) * (LG_RB * 4) + 16 * hl);
     };
-    auto ldx = [&](int s, int c, float (&x)[LG_RPL]) {
-        const float* p = colf(s, c);
-        if constexpr (LG_RPL == 2) {
-            const float2 v = *reinterpret_cast<const float2*>(p);
-            x[0] = v.x;
-            x[LG_RPL - 1] = v.y;
-        } else {
-#pragma unroll
-            for (int h = 0; h < LG_RPL; ++h) x[h] = p[h];
-        }
-    };
-    // phase 1 of slab j: lane holds rows RPL*lane .. RPL*lane + RPL - 1; two
-    // f32 chains per row over the warp's 16 columns (the reference's z is an
-    // f32 sgemv); the 16 warp partials and the 4 CTA partials are added in f64
+    // phase 1 of slab j: an f32 chain per row over the half-warp's 8 columns
+    // (the reference's z is an f32 sgemv); the two halves, the 16 warp
+    // partials and the 4 CTA partials are added in f64 in a fixed order
     auto phase1 = [&](i64 j) {
         const int s = (int)(j % LG_STAGES);
         lg_wait(&full[s], (unsigned)((j / LG_STAGES) & 1));
-        float a[LG_RPL], b[LG_RPL];
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
 #pragma unroll
-        for (int h = 0; h < LG_RPL; ++h) a[h] = b[h] = 0.f;
-#pragma unroll
-        for (int u = 0; u < 16; u += 2) {
-            float x[LG_RPL], y[LG_RPL];
-            ldx(s, wc + u, x);
-            ldx(s, wc + u + 1, y);
-            const float w0 = ws[wc + u], w1 = ws[wc + u + 1];
-#pragma unroll
-            for (int h = 0; h < LG_RPL; ++h) {
-                a[h] = __fmaf_rn(x[h], w0, a[h]);
-                b[h] = __fmaf_rn(y[h], w1, b[h]);
-            }
+        for (int u = 0; u < 8; ++u) {
+            const float4 x = ldx4(s, cw + u);
+            const float w = ws[cw + u];
+            a0 = __fmaf_rn(x.x, w, a0);
+            a1 = __fmaf_rn(x.y, w, a1);
+            a2 = __fmaf_rn(x.z, w, a2);
+            a3 = __fmaf_rn(x.w, w, a3);
         }
         const int par = (int)(j & 1);
+        double d[4] = {(double)a0, (double)a1, (double)a2, (double)a3};
 #pragma unroll
-        for (int h = 0; h < LG_RPL; ++h) zpart[par][warp][LG_RPL * lane + h] = (double)a[h] + (double)b[h];
+        for (int h = 0; h < 4; ++h) {
+            const double o = __shfl_xor_sync(0xffffffffu, d[h], 16);
+            if (hc == 0) zpart[par][warp][4 * hl + h] = d[h] + o;   // low half + high half
+        }
     };
     // publish this CTA's partial z of slab j: st.async into the three peers'
     // zq_all, each store completing bytes on the peer's zbar[parity] (no
@@ -256,36 +248,34 @@ __device__ void logistic_grad(const LgArgs& L) {
             rs[par][tid] = r;
         }
     };
-    // phase 2 of slab j: partial sums over this lane's two rows for the warp's
-    // 16 columns, a transpose-reduce across the 32 lanes, then the stage is free
+    // phase 2 of slab j: each lane's 4-row partial sums for its 8 columns, a
+    // transpose-reduce across the 16 lanes of the half-warp (7 shuffles for 8
+    // columns, then one across the lane pair), after which even lanes own
+    // column cw + 4 b3 + 2 b2 + b1 (b = lane bits) for the whole kernel
     auto phase2 = [&](i64 j) {
         const int s = (int)(j % LG_STAGES), par = (int)(j & 1);
-        float rr[LG_RPL];
+        const float4 rr = *reinterpret_cast<const float4*>(&rs[par][4 * hl]);
+        float v[8];
 #pragma unroll
-        for (int h = 0; h < LG_RPL; ++h) rr[h] = rs[par][LG_RPL * lane + h];
-        float v[16];
-#pragma unroll
-        for (int c = 0; c < 16; ++c) {
-            float x[LG_RPL];
-            ldx(s, wc + c, x);
-            float acc = x[0] * rr[0];
-#pragma unroll
-            for (int h = 1; h < LG_RPL; ++h) acc = __fmaf_rn(x[h], rr[h], acc);
-            v[c] = acc;
+        for (int c = 0; c < 8; ++c) {
+            const float4 x = ldx4(s, cw + c);
+            float acc = x.x * rr.x;
+            acc = __fmaf_rn(x.y, rr.y, acc);
+            acc = __fmaf_rn(x.z, rr.z, acc);
+            v[c] = __fmaf_rn(x.w, rr.w, acc);
         }
 #pragma unroll
-        for (int c = 0; c < 16; ++c) v[c] = v[c] + __shfl_xor_sync(0xffffffffu, v[c], 16);
-#pragma unroll
-        for (int off = 8; off >= 1; off >>= 1) {
+        for (int off = 8, n = 4; off >= 2; off >>= 1, n >>= 1) {
             const bool upper = (lane & off) != 0;
 #pragma unroll
-            for (int c = 0; c < off; ++c) {
-                const float send = upper ? v[c] : v[c + off];
-                const float keep = upper ? v[c + off] : v[c];
+            for (int c = 0; c < n; ++c) {
+                const float send = upper ? v[c] : v[c + n];
+                const float keep = upper ? v[c + n] : v[c];
                 v[c] = keep + __shfl_xor_sync(0xffffffffu, send, off);
             }
         }
-        gacc += (double)v[0];                  // lane l (and l ^ 16) now holds column wc + (l & 15)
+        v[0] = v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+        gacc += (double)v[0];
         __syncwarp();
         if (lane == 0) lg_arrive(&empty[s]);
     };
@@ -317,8 +307,8 @@ __device__ void logistic_grad(const LgArgs& L) {
         if (j + 1 < nmine) publish(j + 1);
         phase2(j);
     }
-    if (lane < 16) {
-        const i64 c = col0 + wc + lane;
+    if ((lane & 1) == 0) {
+        const i64 c = col0 + cw + 4 * ((lane >> 3) & 1) + 2 * ((lane >> 2) & 1) + ((lane >> 1) & 1);
         if (c < L.k) L.gpart[cluster * L.k + c] = gacc;
     }
     lg_cluster_sync();                             // no CTA exits while a peer may still read its zq

@@ -192,6 +192,18 @@ def run_reference_arm(args, rank: int) -> None:
 # ---------------------------------------------------------------------------
 # B200 arm
 
+def _ncu_traffic(key: str):
+    """DRAM bytes per launch of a bench kernel from the committed ncu capture
+    (profiles/ncu_traffic.json); None when absent."""
+    import json
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)[key]["bytes"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def _event_time_ms(torch, fn, steps: int) -> float:
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record()
@@ -429,7 +441,9 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
                        "parallelism": f"column-block shards x{world}; rank partials all-gathered (NCCL) and folded "
                                       "deterministically on device" if world > 1 else "single GPU"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak_hbm, "unit": "GB/s",
-                         "frac": achieved / peak_hbm, "traffic": None, "peak_source": peak_src,
+                         "frac": achieved / peak_hbm, "traffic": _ncu_traffic("cfg1_bm_reduce"),
+                         "traffic_unit": "DRAM bytes per launch (ncu capture, profiles/ncu_traffic.json)",
+                         "algorithmic_bytes_per_launch": BYTES_PER_STEP, "peak_source": peak_src,
                          "kernel": "bm_reduce (fused program + numpy-order pairwise accu)",
                          "kernel_ms": kern_avg, "kernel_ms_isolated_launch": kern},
             "e2e": {"value": world * BYTES_PER_STEP / e2e_s / 1e9, "unit": "GB/s",

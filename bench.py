@@ -340,6 +340,7 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
     # correctness of the measured thing (cheap): device result vs single-shard oracle-free self-check
     for _ in range(args.warmup):
         red.launch()
+    red.join()
     barrier()
     c0 = _clib.Counters()
     lib.bm_get_counters(c0)
@@ -349,6 +350,7 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
         start.record()
         for _ in range(args.steps):
             red.launch()
+        red.join()                             # the last steps' collectives run on a side stream
         end.record()
         end.synchronize()
         barrier()

@@ -14,6 +14,7 @@ size.  No float atomics, no NCCL sum whose order NCCL chooses.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 
@@ -52,49 +53,113 @@ def partial_dtype(op: str, elem: str) -> str:
 class ShardedReduction:
     """A scalar reduction over column-block shards, reusable across steps.
 
-    ``prepare`` plans the fused kernel once; ``launch`` enqueues this rank's
-    partial, the all-gather and the device-side fold without any host
+    The constructor plans the fused kernel once; ``launch`` enqueues this
+    rank's partial, the all-gather and the device-side fold without any host
     synchronisation; ``value`` reads the folded result back.
+
+    With more than one rank, consecutive steps are software-pipelined: the
+    partial of step k goes to a side stream that runs the all-gather and the
+    fold, while the compute stream goes on with step k + 1.  Partials,
+    gathered vectors and results are double-buffered by step parity, and step
+    k + 2 waits for the gather that read its partial buffer, so a step costs
+    max(kernel, collective) instead of their sum.  ``join`` orders the current
+    stream after every collective issued so far (timing, value).
+    ``collective="allreduce"`` gathers by summing rank-slotted vectors (for
+    backends without all-gather of device tensors, e.g. gloo in tests).
     """
 
-    def __init__(self, op: str, *local_exprs, group=None):
+    def __init__(self, op: str, *local_exprs, group=None, pipeline=None, collective="all_gather"):
         import torch
         import torch.distributed as dist
         self.op = op
         self.dist = dist
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.plan = _expr.plan_reduce(op, *local_exprs)
         if self.plan.steps:
             raise ValueError("sharded reduction expects a purely element-wise local program")
+        if collective not in ("all_gather", "allreduce"):
+            raise ValueError(f"unknown collective {collective!r}")
+        self.collective = collective
         node = _expr.as_expr(local_exprs[0])
         self.elem = node.elem_type
         self.pdt = partial_dtype(op, self.elem)
         tdt = getattr(torch, _TORCH_DTYPE[self.pdt])
-        self.partial = torch.zeros(1, dtype=tdt, device="cuda")
-        self.gathered = torch.zeros(self.world, dtype=tdt, device="cuda")
-        self.result = torch.zeros(1, dtype=tdt, device="cuda")
+        if pipeline is None:
+            pipeline = os.environ.get("BM_SHARD_PIPELINE", "1") != "0"
+        self.pipeline = bool(pipeline) and self.world > 1
+        nbuf = 2 if self.pipeline else 1
+        self.partials = [torch.zeros(1, dtype=tdt, device="cuda") for _ in range(nbuf)]
+        self.gathered = [torch.zeros(self.world, dtype=tdt, device="cuda") for _ in range(nbuf)]
+        self.results = [torch.zeros(1, dtype=tdt, device="cuda") for _ in range(nbuf)]
+        self.partial = self.partials[0]
+        self.result = self.results[0]
         views = _expr._step_views(self.plan, self.plan.reduce, {})
         self.inv = _rt.build_invocation(_rt.KernelInvocation("fused_reduce", tuple(views), None, (),
                                                              dict(self.plan.reduce.params)))
         self._lib = _clib.lib()
         self._op_code = {"accu": _clib.BM_R_ACCU, "min": _clib.BM_R_MIN, "max": _clib.BM_R_MAX,
                          "dot": _clib.BM_R_DOT}[op]
+        self._step = 0
+        self._last = 0
+        if self.pipeline:
+            self._comm = torch.cuda.Stream()
+            self._reduced = [torch.cuda.Event() for _ in range(nbuf)]
+            self._gathered = [None] * nbuf    # event after the gather + fold of the buffer's last step
+
+    def _gather_and_fold(self, slot: int) -> None:
+        part, gath = self.partials[slot], self.gathered[slot]
+        if self.collective == "all_gather":
+            self.dist.all_gather_into_tensor(gath, part, group=self.group)
+        else:
+            gath.zero_()
+            gath[self.rank:self.rank + 1].copy_(part)
+            self.dist.all_reduce(gath, group=self.group)
+        _clib.check(self._lib.bm_combine_partials_to_device(
+            ctypes.c_void_p(gath.data_ptr()), self.world, _clib.DTYPE_CODE[self.elem], self._op_code,
+            ctypes.c_void_p(self.results[slot].data_ptr())), "combine partials")
 
     def launch(self) -> None:
-        _clib.check(self._lib.bm_reduce_to_device(ctypes.byref(self.inv), ctypes.c_void_p(self.partial.data_ptr())),
+        import torch
+        slot = self._step % len(self.partials)
+        self._step += 1
+        self._last = slot
+        compute = torch.cuda.current_stream()
+        if self.pipeline and self._gathered[slot] is not None:
+            compute.wait_event(self._gathered[slot])   # the gather that read this partial is done
+        _clib.check(self._lib.bm_reduce_to_device(ctypes.byref(self.inv),
+                                                  ctypes.c_void_p(self.partials[slot].data_ptr())),
                     "sharded reduce")
         if self.world == 1:
             return
-        self.dist.all_gather_into_tensor(self.gathered, self.partial, group=self.group)
-        _clib.check(self._lib.bm_combine_partials_to_device(
-            ctypes.c_void_p(self.gathered.data_ptr()), self.world, _clib.DTYPE_CODE[self.elem], self._op_code,
-            ctypes.c_void_p(self.result.data_ptr())), "combine partials")
+        if not self.pipeline:
+            self._gather_and_fold(slot)
+            return
+        self._reduced[slot].record(compute)
+        lib_stream = self._lib.bm_get_stream()
+        with torch.cuda.stream(self._comm):
+            self._comm.wait_event(self._reduced[slot])
+            _clib.check(self._lib.bm_set_stream(ctypes.c_void_p(self._comm.cuda_stream)), "comm stream")
+            try:
+                self._gather_and_fold(slot)
+            finally:
+                _clib.check(self._lib.bm_set_stream(ctypes.c_void_p(lib_stream)), "compute stream")
+            ev = torch.cuda.Event()
+            ev.record(self._comm)
+            self._gathered[slot] = ev
+
+    def join(self) -> None:
+        """Order the current stream after every collective issued so far."""
+        import torch
+        if self.pipeline:
+            torch.cuda.current_stream().wait_stream(self._comm)
 
     def value(self):
         import torch
+        self.join()
         torch.cuda.synchronize()
-        src = self.partial if self.world == 1 else self.result
+        src = self.partials[self._last] if self.world == 1 else self.results[self._last]
         v = src.cpu().numpy()[0]
         dt = kernels.NP_DTYPE[self.elem]
         if self.op == "dot" and dt.kind == "f":

@@ -189,3 +189,53 @@ def _logistic_worker(rank, world, port, q, nrow, ncol):
 def test_sharded_logistic_step_matches_single_device():
     gerr, serr = _spawn(_logistic_worker, 2, 1000, 64)
     assert gerr < 1e-6 and serr < 1e-6
+
+
+# ---- the pipelined device path: two ranks sharing one GPU over gloo ----------------------------
+
+def _pipeline_worker(rank, world, port, q, rows, cols, pipeline):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2308_03120_b200 as dm
+        from paper_2308_03120_b200 import dist as D
+        torch.cuda.set_device(0)
+        dm.init("b200", device_id=0)
+        D.bind_torch_stream()
+        full = np.random.default_rng(9).random((rows, cols), dtype=np.float32)
+        start, count = column_block(cols, rank, world)
+        m = dm.Matrix.from_numpy(np.asfortranarray(full[:, start:start + count]))
+        red = D.ShardedReduction("accu", m, pipeline=pipeline, collective="allreduce")
+        view = D.torch_view(m)
+        # three back-to-back steps, the input doubled on the compute stream in between:
+        # step k reduces 2^k * X (exact), step 2 reuses step 0's buffers
+        red.launch()
+        view.mul_(2)
+        red.launch()
+        view.mul_(2)
+        red.launch()
+        red.join()
+        torch.cuda.synchronize()
+        res = [np.float32(r.cpu().numpy()[0]).tobytes() for r in red.results]
+        last = np.float32(red.value()).tobytes()
+        if rank == 0:
+            q.put((res, last, red.pipeline))
+        dm.shutdown()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("pipeline", [True, False])
+def test_pipelined_sharded_reduction_two_ranks_one_gpu(pipeline):
+    rows, cols = 1024, 256                     # 16 REDUCE_BLOCK blocks per rank: bit-exact
+    res, last, piped = _spawn(_pipeline_worker, 2, rows, cols, pipeline)
+    full = np.random.default_rng(9).random((rows, cols), dtype=np.float32)
+    want = [np.float32(O.reduce_accu((np.float32(2 ** k) * full).reshape(-1, order="F"))).tobytes()
+            for k in range(3)]
+    assert piped == pipeline
+    assert last == want[2]
+    if pipeline:
+        assert res == [want[2], want[1]]       # buffers by step parity
+    else:
+        assert res == [want[2]]

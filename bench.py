@@ -482,8 +482,16 @@ def main() -> None:
     if world > 1:
         import torch
         import torch.distributed as tdist
-        torch.cuda.set_device(local_rank)
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if os.environ.get("BM_BENCH_SHARE_GPU") == "1":
+            # test mode only: every rank on GPU 0 over gloo (NCCL refuses two ranks
+            # on one device); a rank-slotted all-reduce stands in for the all-gather
+            local_rank = 0
+            os.environ["BM_SHARD_COLLECTIVE"] = "allreduce"
+            torch.cuda.set_device(0)
+            tdist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local_rank)
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         run_b200(args, rank, world, local_rank)
     finally:

@@ -68,7 +68,7 @@ class ShardedReduction:
     backends without all-gather of device tensors, e.g. gloo in tests).
     """
 
-    def __init__(self, op: str, *local_exprs, group=None, pipeline=None, collective="all_gather"):
+    def __init__(self, op: str, *local_exprs, group=None, pipeline=None, collective=None):
         import torch
         import torch.distributed as dist
         self.op = op
@@ -79,6 +79,8 @@ class ShardedReduction:
         self.plan = _expr.plan_reduce(op, *local_exprs)
         if self.plan.steps:
             raise ValueError("sharded reduction expects a purely element-wise local program")
+        if collective is None:
+            collective = os.environ.get("BM_SHARD_COLLECTIVE", "all_gather")
         if collective not in ("all_gather", "allreduce"):
             raise ValueError(f"unknown collective {collective!r}")
         self.collective = collective

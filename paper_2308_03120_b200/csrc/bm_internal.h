@@ -83,6 +83,7 @@ int launch_pred_count(const bm_invocation* inv, void* dev_result);
 int launch_pred_find(const bm_invocation* inv);
 int launch_logistic_grad(const bm_invocation* inv);
 int launch_gemm_fused(const bm_invocation* inv);
+int launch_rdim_fused(const bm_invocation* inv);
 // fills the K-major tf32 hi/lo copies (rp x kp) of one GEMM operand
 typedef std::function<int(float* hi, float* lo, int64_t kp, int64_t rp)> SplitFn;
 int gemm_tc_f32_core(int64_t m, int64_t n, int64_t k, const SplitFn& split_a, const SplitFn& split_b, float* C,

@@ -20,6 +20,7 @@
 #include "bm_ptx.cuh"
 #define BM_UNIT_UNROLL 16   // single input: all 16 rows of a pairwise unit in flight
 #include "bm_reduce.cuh"
+#include "bm_rdim0.cuh"
 
 
 namespace bm {
@@ -80,103 +81,12 @@ __global__ void __launch_bounds__(256, 2) rdim0_stream_kernel(const T* __restric
     }
 }
 
-// Columns of 8*sub half-units (a power-of-two count for sum/mean; any count
-// for min/max): the CTA's eight warps share one column at a time, warp w
-// reducing half-units [w*sub, (w+1)*sub) -- for sum the balanced subtree
-// there, the CTA then adding the eight subtree sums as the top three levels
-// of the same balanced tree; for min/max a NaN-propagating partial, merged in
-// any order.  One CTA streams one contiguous column (e.g. 128 KiB) instead of
-// eight warps streaming eight columns, which the DRAM serves faster, and each
-// warp loads its next half-unit -- across columns too -- while it reduces the
-// current one.
+// Columns of 8*sub half-units: one CTA per column at a time (bm_rdim0.cuh)
 template <typename T, int OP>
 __global__ void __launch_bounds__(256, 2) rdim0_cta_kernel(const T* __restrict__ a, i64 rows, i64 cols, i64 lda,
                                                            T* out, i64 sub) {
-    constexpr i64 U = PwHalf<T>::value;
-    constexpr int V = 16 / sizeof(T);
-    constexpr int LV = 12;
-    constexpr bool MM = OP == 2 || OP == 3;
     extern __shared__ __align__(16) char smem[];
-    __shared__ T res[2][8];
-    __shared__ int res_nan[2][8];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    char* tile = smem + warp * BM_TILE_BYTES;
-    if ((i64)blockIdx.x >= cols) return;
-    int top = 0;
-    while ((1ll << top) < sub) ++top;
-    const i64 step = gridDim.x;
-    const i64 base = (i64)warp * sub * U;
-    i64 c = blockIdx.x, j = 0;
-    int par = 0;
-    T stk[LV + 1];
-    MinMaxAcc<T, OP == 3> acc;
-    HalfRows<T> cur, nxt;
-    half_load<T>(BufSrc<T>{a + c * lda + base, 1}, 0, cur);
-    while (true) {
-        i64 nc = c, nj = j + 1;
-        if (nj == sub) { nj = 0; nc = c + step; }
-        if (nc < cols) half_load<T>(BufSrc<T>{a + nc * lda + base, 1}, nj * U, nxt);
-        if constexpr (MM) {
-#pragma unroll
-            for (int r = 0; r < 8; ++r)
-#pragma unroll
-                for (int k = 0; k < V; ++k) acc.add(cur.v[r][k]);
-        } else {
-            T v = half_reduce<T>(cur, tile);
-#pragma unroll
-            for (int l = 0; l <= LV; ++l) {
-                if (l < LV && ((j >> l) & 1)) {
-                    v = stk[l] + v;
-                } else {
-                    stk[l] = v;
-                    break;
-                }
-            }
-        }
-        if (nj == 0) {
-            if constexpr (MM) {
-                acc.warp_merge();
-                if (lane == 0) {
-                    res[par][warp] = acc.v;
-                    res_nan[par][warp] = acc.nan;
-                }
-                acc = MinMaxAcc<T, OP == 3>();
-            } else {
-                T r = stk[0];
-#pragma unroll
-                for (int l = 1; l <= LV; ++l)
-                    if (l == top) r = stk[l];
-                if (lane == 0) res[par][warp] = r;
-            }
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                const T* q = res[par];
-                T o;
-                if constexpr (MM) {
-                    MinMaxAcc<T, OP == 3> m;
-#pragma unroll
-                    for (int w = 0; w < 8; ++w) {
-                        MinMaxAcc<T, OP == 3> x;
-                        x.v = q[w];
-                        x.nan = res_nan[par][w] != 0;
-                        m.merge(x);
-                    }
-                    o = m.result();
-                } else {
-                    T sum = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
-                    sum = sum + T(0);
-                    o = sum;
-                    if constexpr (OP == 5) o = OpDiv::f(sum, KScal<T>::f((double)rows, rows));
-                }
-                out[c] = o;
-            }
-            par ^= 1;
-        }
-        if (nc >= cols) break;
-        c = nc;
-        j = nj;
-        cur = nxt;
-    }
+    rdim0_cta_body<T, OP>(BufSrc<T>{a, 1}, rows, cols, lda, out, smem, sub);
 }
 
 template <typename T, int OP>

@@ -325,6 +325,8 @@ int bm_enqueue(const bm_invocation* inv) {
             return launch_logistic_grad(inv);
         case BM_K_GEMM_FUSED:
             return launch_gemm_fused(inv);
+        case BM_K_RDIM_FUSED:
+            return launch_rdim_fused(inv);
         default:
             return launch_misc(inv);
     }

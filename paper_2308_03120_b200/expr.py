@@ -395,6 +395,7 @@ class EvalPlan:
 _GEN_KERNEL = {"gen_zeros": "gen_fill_const", "gen_ones": "gen_fill_const", "gen_fill": "gen_fill_const",
                "gen_eye": "gen_eye", "gen_linspace": "gen_linspace", "gen_randu": "gen_randu",
                "gen_randn": "gen_randn"}
+_FUSED_RDIM = frozenset({"op_sum_dim", "op_mean_dim", "op_min_dim", "op_max_dim"})
 _RDIM_KERNEL = {"op_sum_dim": "rdim_sum", "op_min_dim": "rdim_min", "op_max_dim": "rdim_max",
                 "op_mean_dim": "rdim_mean", "op_var_dim": "rdim_var", "op_stddev_dim": "rdim_var"}
 
@@ -491,6 +492,9 @@ class _Lowerer:
             return self.emit(kern, [a, b], ["2d", "2d"], shape_of(node), want, "2d", absorbed_from=node.elem_type)
         if k in REDUCE_DIM_KINDS:
             child = node.operands[0]
+            ref = self._fused_rdim(node, want)
+            if ref is not None:
+                return ref
             src = self.lower(child, child.elem_type)
             ref = self.emit(_RDIM_KERNEL[k], [src], ["2d"], shape_of(node), child.elem_type, "flat",
                             params={"dim": node.aux[0]})
@@ -704,6 +708,27 @@ class _Lowerer:
         return self.emit("fused_chain", prog.inputs, ["flat"] * len(prog.inputs), shape, want, "flat",
                          params={"program": tuple(prog.stages), "compute_dtype": NP_DTYPE[elem].str},
                          absorbed_from=elem)
+
+    def _fused_rdim(self, node: ExprNode, want: str):
+        """sum / mean / min / max over dim 0 of an element-wise tree: one
+        ``fused_rdim`` step (b200mat.h BM_K_RDIM_FUSED) whose column reductions
+        evaluate the tree's program instead of reading a materialised temporary
+        (the reference lowers the child first, expr.py:583-594).  Same values,
+        same reduction order: the same bits."""
+        k, child = node.kind, node.operands[0]
+        if not self.fuse or k not in _FUSED_RDIM or node.aux[0] != 0 or child.kind not in ELEMENTWISE_KINDS:
+            return None
+        shp = shape_of(child)
+        if shp.rows == 0 or shp.cols == 0:
+            return None
+        elem = child.elem_type
+        prog = self._fit_program(child, elem)
+        ref = self.emit("fused_rdim", prog.inputs, ["flat"] * len(prog.inputs), shape_of(node), elem, "flat",
+                        params={"program": tuple(prog.stages), "compute_dtype": NP_DTYPE[elem].str,
+                                "op": _RDIM_KERNEL[k], "rows": shp.rows})
+        if want != elem:
+            ref = self.emit("mov_copy", [ref], ["flat"], shape_of(node), want, "flat")
+        return ref
 
     def _ref_elem(self, ref) -> str:
         return ref[1].elem_type if ref[0] == "leaf" else self.slots[ref[1]].elem_type

@@ -281,6 +281,19 @@ def build_invocation(inv: KernelInvocation) -> _clib.Invocation:
             pb.stage(st)
         pb.finish()
         return c
+    if kind == "fused_rdim":
+        # dim-0 sum / mean / min / max of an element-wise program (b200mat.h BM_K_RDIM_FUSED)
+        c.kind = _clib.BM_K_RDIM_FUSED
+        elem = _NPSTR_TO_ELEM[np.dtype(p["compute_dtype"]).str]
+        c.compute_dtype = _clib.DTYPE_CODE[elem]
+        c.reduce_op = _RDIM_OP[p["op"]]
+        c.dim = 0
+        c.iparams[0] = int(p["rows"])
+        pb = _ProgramBuilder(c, elem)
+        for st in p["program"]:
+            pb.stage(st)
+        pb.finish()
+        return c
     if kind in _RDIM_OP:
         c.kind = _clib.BM_K_RDIM
         c.reduce_op = _RDIM_OP[kind]

@@ -250,6 +250,34 @@ def test_rdim0_minmax_cta_path_nan(dm, dt, shape):
         same(dm.evaluate(getattr(dm, op)(m, 0)).to_numpy(), O.rdim(op, a, 0))
 
 
+@pytest.mark.parametrize("dt,shape", [(np.float32, (8192, 40)), (np.float64, (4096, 37)), (np.float32, (4096, 300)),
+                                      (np.float64, (1000, 33)), (np.float32, (999, 17)), (np.int32, (2048, 9)),
+                                      (np.float64, (12288, 11))])
+def test_fused_dim0_reduction_of_a_tree(dm, dt, shape):
+    """sum / mean / min / max(·, 0) of an element-wise tree run as one fused
+    kernel and give the bits of reducing the materialised tree (the
+    reference's two steps), NaNs included"""
+    rng = np.random.default_rng(shape[0] + shape[1])
+    if np.issubdtype(dt, np.integer):
+        a = rng.integers(-1000, 1000, size=shape).astype(dt)
+        b = rng.integers(-1000, 1000, size=shape).astype(dt)
+    else:
+        a = rng.standard_normal(shape).astype(dt)
+        b = rng.standard_normal(shape).astype(dt)
+        b[shape[0] // 3, 0] = np.nan
+    A, B = dm.Matrix.from_numpy(a), dm.Matrix.from_numpy(b)
+    tree = lambda: 3 * A + B % A - 2
+    launches = []
+    for op in ("sum", "mean", "min", "max"):
+        assert [s.kernel for s in dm.plan(getattr(dm, op)(tree(), 0)).steps] == ["fused_rdim"]
+        c0 = dm.counters().launches
+        got = dm.evaluate(getattr(dm, op)(tree(), 0)).to_numpy()
+        launches.append(dm.counters().launches - c0)
+        mat = dm.evaluate(tree()).to_numpy()
+        same(got, O.rdim(op, mat, 0))
+    assert launches == [1, 1, 1, 1]
+
+
 # ---- GEMM ----------------------------------------------------------------------------------------
 
 def test_gemm_vs_reference(dm):

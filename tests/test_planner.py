@@ -286,3 +286,34 @@ def test_gemm_split_kernel_compiles():
     inv = build_invocation(KernelInvocation("gemm_fused", tuple(views), expr._make_view(C.mem, 256, 256, "2d"), (),
                                             st.params))
     assert inv.kind == _clib.BM_K_GEMM_FUSED and inv.iparams[0] == 1
+
+
+# ---- dim-0 reductions over element-wise trees ----------------------------------
+
+def test_dim0_reduction_of_a_tree_is_one_fused_step():
+    a, b = leaf(512, 40), leaf(512, 40)
+    for op, kern in (("sum", "rdim_sum"), ("mean", "rdim_mean"), ("min", "rdim_min"), ("max", "rdim_max")):
+        p = dm.plan(getattr(dm, op)(2 * a + b, 0))
+        assert [s.kernel for s in p.steps] == ["fused_rdim"], op
+        st = p.steps[0]
+        assert st.params["op"] == kern and st.params["rows"] == 512
+        assert st.params["program"] == (("load", 0), ("scalar", "eop_scalar_times", 2), ("load", 1),
+                                        ("glue", "eglue_plus"))
+    # a leaf, dim 1, var/stddev and empty shapes keep the reference's lowering
+    assert [s.kernel for s in dm.plan(dm.sum(a, 0)).steps] == ["rdim_sum"]
+    assert [s.kernel for s in dm.plan(dm.sum(2 * a + b, 1)).steps] == ["fused_chain", "rdim_sum"]
+    assert [s.kernel for s in dm.plan(dm.var(2 * a + b, 0)).steps] == ["fused_chain", "rdim_var"]
+    assert [s.kernel for s in dm.plan(dm.sum(2 * leaf(0, 5) + 1, 0)).steps] != ["fused_rdim"]
+
+
+def test_fused_dim0_kernels_compile():
+    for elem in ("f32", "f64", "i32"):
+        a, b = leaf(512, 40, elem), leaf(512, 40, elem)
+        for op in ("sum", "mean", "min", "max"):
+            p = dm.plan(getattr(dm, op)(a * b + 3, 0))
+            st = p.steps[0]
+            views = [expr._make_view(r[1].mem, 512, 40, "flat") for r in st.inputs]
+            out = FakeMatrix(1, 40, elem)
+            inv = build_invocation(KernelInvocation("fused_rdim", tuple(views), _flat(out), (), st.params))
+            rc = _clib.lib().bm_jit_compile_only(ctypes.byref(inv))
+            assert rc == 0, _clib.last_error()

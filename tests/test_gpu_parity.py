@@ -378,6 +378,25 @@ def test_large_reductions_external_fold(dm):
     same(np.float64(dm.accu(dm.Matrix.from_numpy(vd.reshape(-1, 1)))), O.reduce_accu(vd))
 
 
+def test_beyond_2_31_elements(dm):
+    """64-bit element indexing end to end: 2^31 + 1000 f64 elements (17 GB,
+    generated on the device) through a fused store, accu, min/max, dot and a
+    dim-0 sum; every value is exact in f64, so the results are known."""
+    n = (1 << 31) + 1000
+    x = dm.Matrix(n, 1, fill="ones", elem_type="f64")
+    assert dm.accu(x) == float(n)
+    assert dm.reduce_min(x) == 1.0 and dm.reduce_max(x) == 1.0
+    assert dm.dot(x, x) == float(n)
+    y = dm.evaluate(2 * x + 1)
+    assert dm.accu(y) == 3.0 * n
+    assert dm.accu(y - 3) == 0.0
+    del y
+    m = dm.Matrix(1 << 16, (1 << 15) + 3, fill="ones", elem_type="f64")   # 2^31 + 3 * 2^16 elements
+    s = dm.evaluate(dm.sum(m, 0)).to_numpy()
+    assert s.shape == (1, (1 << 15) + 3) and np.all(s == float(1 << 16))
+    assert dm.accu(m) == float(m.n_elem)
+
+
 def test_back_to_back_reductions_stay_ordered_with_stores(dm):
     """Reductions launch as programmatic dependents (PDL) and overlap their
     predecessor's final fold.  Interleave stores that rewrite the reduced

@@ -11,8 +11,11 @@
 // that streams at full HBM rate; 64-B rows stream at a third of it,
 // tools/tma2d_probe.cu) x 128 columns.  A slab of 64 x 1024 f32 is 256 KB --
 // more than one SM holds -- so a cluster of 4 CTAs shares it: CTA q of the
-// cluster owns columns [256q, 256q + 256) and keeps its 64 KB quarter in a
-// 3-stage TMA ring.  Per slab:
+// cluster owns columns [256q, 256q + 256), streamed through a 3-stage TMA ring
+// of 64 KB quarters.  Phase 1 moves its quarter from shared memory into
+// registers and parks it in TMEM (tcgen05.st, 128 columns per slab, two
+// slabs), so the stage is refilled at once and phase 2 reads the slab back
+// from TMEM: two stages stay in flight instead of one.  Per slab:
 //   phase 1  each CTA computes partial z over its columns (f32 chains as in
 //            the reference's sgemv, partials added in f64; fixed order) and
 //            pushes them into the peers' shared memory (st.async, completing
@@ -49,6 +52,7 @@ namespace bm {
 #define LG_STAGES ((192 * 1024) / (LG_RB * LG_COLS * 4))
 #define LG_THREADS (LG_COLS * 2)      // warps of 16 columns each
 #define LG_STAGE_BYTES (LG_RB * LG_COLS * 4)
+#define LG_TMEM_COLS 256                      // two slabs of 64 rows x 256 columns parked in TMEM
 
 struct alignas(64) LgTmap {
     unsigned long long v[16];   // CUtensorMap (128 B, opaque)
@@ -120,6 +124,32 @@ __device__ __forceinline__ unsigned lg_cluster_rank() {
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
     return r;
 }
+// TMEM as a per-thread parking space: 32 f32 of this thread's lane at column
+// offset `taddr` (32x32b shape: warp w owns lanes 32 (w % 4) .. + 31)
+__device__ __forceinline__ void lg_tmem_st32(unsigned taddr, const float (&v)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+        "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, "
+        "%17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+        "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+        "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]), "f"(v[17]), "f"(v[18]),
+        "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]),
+        "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+        : "memory");
+}
+__device__ __forceinline__ void lg_tmem_ld32(unsigned taddr, float (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+        "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]), "=f"(v[8]),
+          "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15]), "=f"(v[16]),
+          "=f"(v[17]), "=f"(v[18]), "=f"(v[19]), "=f"(v[20]), "=f"(v[21]), "=f"(v[22]), "=f"(v[23]), "=f"(v[24]),
+          "=f"(v[25]), "=f"(v[26]), "=f"(v[27]), "=f"(v[28]), "=f"(v[29]), "=f"(v[30]), "=f"(v[31])
+        : "r"(taddr)
+        : "memory");
+}
 __device__ __forceinline__ void lg_cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -133,6 +163,7 @@ __device__ void logistic_grad(const LgArgs& L) {
     __shared__ double zq_all[2][LG_CLUSTER][LG_RB];   // the cluster's partial z, by slab parity (pushed by each CTA)
     __shared__ __align__(16) float rs[2][LG_RB];
     __shared__ float ws[LG_COLS];
+    __shared__ unsigned tmem_slot;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const unsigned q = lg_cluster_rank();
     const i64 cluster = blockIdx.x / LG_CLUSTER, nclusters = gridDim.x / LG_CLUSTER;
@@ -149,7 +180,17 @@ __device__ void logistic_grad(const LgArgs& L) {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&L.tmx) : "memory");
     }
+    if (warp == 0) {                           // 2 slabs x 128 columns of TMEM
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(lg_smem(&tmem_slot)),
+                     "r"(LG_TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     lg_cluster_sync();                         // peers' zbar initialised before anyone pushes
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // this thread's parking place: its warp's lane quarter, 32 columns per warp group
+    const unsigned tmem_me = tmem_slot + ((unsigned)(32 * (warp & 3)) << 16) + (unsigned)(32 * (warp >> 2));
     auto issue = [&](i64 j) {   // this CTA's quarter of slab j into stage j % STAGES
         const int s = (int)(j % LG_STAGES);
         const i64 slab = cluster + j * nclusters;
@@ -160,7 +201,7 @@ __device__ void logistic_grad(const LgArgs& L) {
                       col0 + b * LG_BOXC, &full[s]);
     };
     if (tid == 0)
-        for (i64 j = 0; j < LG_STAGES - 1 && j < nmine; ++j) issue(j);
+        for (i64 j = 0; j < LG_STAGES && j < nmine; ++j) issue(j);
 
     typename E::Pre pre;                       // chain inputs of the next slab (threads < LG_RB)
     double gacc = 0.0;                         // one column per even lane (see phase 2)
@@ -181,15 +222,26 @@ __device__ void logistic_grad(const LgArgs& L) {
     auto phase1 = [&](i64 j) {
         const int s = (int)(j % LG_STAGES);
         lg_wait(&full[s], (unsigned)((j / LG_STAGES) & 1));
-        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+        float xs[32];                          // [column u][row h], parked in TMEM for phase 2
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const float4 x = ldx4(s, cw + u);
+            xs[4 * u] = x.x;
+            xs[4 * u + 1] = x.y;
+            xs[4 * u + 2] = x.z;
+            xs[4 * u + 3] = x.w;
+        }
+        __syncwarp();
+        if (lane == 0) lg_arrive(&empty[s]);   // the stage is free: its values are in registers
+        lg_tmem_st32(tmem_me + (unsigned)((j & 1) * 128), xs);
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
             const float w = ws[cw + u];
-            a0 = __fmaf_rn(x.x, w, a0);
-            a1 = __fmaf_rn(x.y, w, a1);
-            a2 = __fmaf_rn(x.z, w, a2);
-            a3 = __fmaf_rn(x.w, w, a3);
+            a0 = __fmaf_rn(xs[4 * u], w, a0);
+            a1 = __fmaf_rn(xs[4 * u + 1], w, a1);
+            a2 = __fmaf_rn(xs[4 * u + 2], w, a2);
+            a3 = __fmaf_rn(xs[4 * u + 3], w, a3);
         }
         const int par = (int)(j & 1);
         double d[4] = {(double)a0, (double)a1, (double)a2, (double)a3};
@@ -198,6 +250,7 @@ __device__ void logistic_grad(const LgArgs& L) {
             const double o = __shfl_xor_sync(0xffffffffu, d[h], 16);
             if (hc == 0) zpart[par][warp][4 * hl + h] = d[h] + o;   // low half + high half
         }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     };
     // publish this CTA's partial z of slab j: st.async into the three peers'
     // zq_all, each store completing bytes on the peer's zbar[parity] (no
@@ -253,16 +306,17 @@ __device__ void logistic_grad(const LgArgs& L) {
     // columns, then one across the lane pair), after which even lanes own
     // column cw + 4 b3 + 2 b2 + b1 (b = lane bits) for the whole kernel
     auto phase2 = [&](i64 j) {
-        const int s = (int)(j % LG_STAGES), par = (int)(j & 1);
+        const int par = (int)(j & 1);
         const float4 rr = *reinterpret_cast<const float4*>(&rs[par][4 * hl]);
+        float xs[32];
+        lg_tmem_ld32(tmem_me + (unsigned)((j & 1) * 128), xs);
         float v[8];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-            const float4 x = ldx4(s, cw + c);
-            float acc = x.x * rr.x;
-            acc = __fmaf_rn(x.y, rr.y, acc);
-            acc = __fmaf_rn(x.z, rr.z, acc);
-            v[c] = __fmaf_rn(x.w, rr.w, acc);
+            float acc = xs[4 * c] * rr.x;
+            acc = __fmaf_rn(xs[4 * c + 1], rr.y, acc);
+            acc = __fmaf_rn(xs[4 * c + 2], rr.z, acc);
+            v[c] = __fmaf_rn(xs[4 * c + 3], rr.w, acc);
         }
 #pragma unroll
         for (int off = 8, n = 4; off >= 2; off >>= 1, n >>= 1) {
@@ -276,8 +330,6 @@ __device__ void logistic_grad(const LgArgs& L) {
         }
         v[0] = v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
         gacc += (double)v[0];
-        __syncwarp();
-        if (lane == 0) lg_arrive(&empty[s]);
     };
 
     // Software pipeline: the partials of slab j + 1 are in flight while
@@ -292,9 +344,9 @@ __device__ void logistic_grad(const LgArgs& L) {
         publish(0);
     }
     for (i64 j = 0; j < nmine; ++j) {
-        if (tid == 0 && j + LG_STAGES - 1 < nmine) {
-            const i64 jn = j + LG_STAGES - 1;
-            if (jn >= LG_STAGES) lg_wait(&empty[jn % LG_STAGES], (unsigned)(((jn / LG_STAGES) - 1) & 1));
+        if (tid == 0 && j + LG_STAGES < nmine) {   // stage j % STAGES was freed by phase 1 of slab j
+            const i64 jn = j + LG_STAGES;
+            lg_wait(&empty[jn % LG_STAGES], (unsigned)(((jn / LG_STAGES) - 1) & 1));
             issue(jn);
         }
         chain(j);
@@ -311,7 +363,11 @@ __device__ void logistic_grad(const LgArgs& L) {
         const i64 c = col0 + cw + 4 * ((lane >> 3) & 1) + 2 * ((lane >> 2) & 1) + ((lane >> 1) & 1);
         if (c < L.k) L.gpart[cluster * L.k + c] = gacc;
     }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     lg_cluster_sync();                             // no CTA exits while a peer may still read its zq
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_slot), "r"(LG_TMEM_COLS)
+                     : "memory");
 }
 
 }  // namespace bm

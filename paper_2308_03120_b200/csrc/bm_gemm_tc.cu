@@ -227,6 +227,249 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 }
 
 // ---------------------------------------------------------------------------
+// The same product on CTA pairs (cta_group::2).  A cluster of two CTAs owns
+// a 256 x 256 tile: CTA r loads rows [128 r, 128 r + 128) of the A tile and
+// columns [128 r, 128 r + 128) of the B tile (hi and lo), and the leader
+// issues tcgen05.mma.cta_group::2 with M = 256, N = 256, which reads each
+// CTA's A rows and both B halves and accumulates each CTA's 128 rows in its
+// own TMEM.  Per SM the tensor cores then read 4 KB of A and 4 KB of B per
+// k8 MMA instead of 4 + 8 KB, which takes the single-CTA kernel off its
+// shared-memory bandwidth bound (128 B/clk: MMA operand reads plus TMA
+// writes needed ~156 B/clk there).  Both CTAs' TMA loads complete on the
+// leader's full barrier; the leader's commits arrive on both CTAs' empty and
+// accumulator barriers (multicast); both CTAs' epilogue warps release a TMEM
+// buffer on the leader's acc_empty.
+
+#define T2_BM 128                         // A rows per CTA (256 per pair)
+#define T2_BNH 128                        // B columns per CTA (256 per pair)
+#define T2_STAGES 6
+#define T2_TILE_A (T2_BM * TC_BK * 4)
+#define T2_TILE_B (T2_BNH * TC_BK * 4)
+#define T2_STAGE_BYTES (2 * T2_TILE_A + 2 * T2_TILE_B)
+#define T2_SMEM (T2_STAGES * T2_STAGE_BYTES + 1024 + 256)
+
+__device__ __forceinline__ uint32_t t2_mapa(const void* p, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void t2_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    do {
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n"
+            "}\n"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+// wait with cluster-scope acquire (the phase was completed from the peer CTA)
+__device__ __forceinline__ void t2_wait_cluster(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    do {
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n"
+            "}\n"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+__device__ __forceinline__ void t2_tma(void* dst, const void* tmap, int c0, int c1, uint32_t leader_bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+        "[%4];" ::"r"(smem_u32(dst)),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(leader_bar)
+        : "memory");
+}
+__device__ __forceinline__ void t2_mma(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                       uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void t2_commit_both(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+}
+__device__ __forceinline__ void t2_arrive_remote(uint32_t cluster_bar) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
+}
+__device__ __forceinline__ void t2_cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
+    gemm_3xtf32_pair_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
+                            const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_blo,
+                            float* __restrict__ C, i64 m, i64 n, i64 ldc, int nk, int group_m, int kb0,
+                            int accumulate) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + T2_STAGES * T2_STAGE_BYTES);
+    uint64_t* empty = full + T2_STAGES;
+    uint64_t* acc_full = empty + T2_STAGES;   // [2]
+    uint64_t* acc_empty = acc_full + 2;       // [2] (the leader's counts both CTAs' epilogue warps)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t rank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    const bool leader = rank == 0;
+    // grouped raster over 256 x 256 pair tiles (see gemm_3xtf32_kernel)
+    int m0, n0;
+    {
+        const int nm = (int)((m + 2 * T2_BM - 1) / (2 * T2_BM)), nn = (int)((n + 2 * T2_BNH - 1) / (2 * T2_BNH));
+        const int t = blockIdx.x >> 1;
+        const int per_group = group_m * nn;
+        const int g = t / per_group, first_m = g * group_m;
+        const int gsize = (nm - first_m) < group_m ? (nm - first_m) : group_m;
+        const int r = t - g * per_group;
+        m0 = (first_m + r % gsize) * (2 * T2_BM) + (int)rank * T2_BM;
+        n0 = (r / gsize) * (2 * T2_BNH);
+    }
+    const int nb0 = n0 + (int)rank * T2_BNH;   // this CTA's half of the B tile
+    const int nchunks = (nk + TC_CHUNK_KB - 1) / TC_CHUNK_KB;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < T2_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&acc_full[b], 1);
+            mbar_init(&acc_empty[b], 16);
+        }
+        mbar_fence_init();
+        tma_prefetch_desc(&tm_ahi);
+        tma_prefetch_desc(&tm_alo);
+        tma_prefetch_desc(&tm_bhi);
+        tma_prefetch_desc(&tm_blo);
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(2 * TC_BN)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    t2_cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    auto tile_ahi = [&](int s) { return smem + s * T2_STAGE_BYTES; };
+    auto tile_alo = [&](int s) { return smem + s * T2_STAGE_BYTES + T2_TILE_A; };
+    auto tile_bhi = [&](int s) { return smem + s * T2_STAGE_BYTES + 2 * T2_TILE_A; };
+    auto tile_blo = [&](int s) { return smem + s * T2_STAGE_BYTES + 2 * T2_TILE_A + T2_TILE_B; };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int kb = 0; kb < nk; ++kb) {
+                const int s = kb % T2_STAGES;
+                if (kb >= T2_STAGES) t2_wait_cluster(&empty[s], (uint32_t)(((kb / T2_STAGES) - 1) & 1));
+                if (leader) mbar_expect_tx(&full[s], 2 * T2_STAGE_BYTES);   // both CTAs' bytes
+                const uint32_t lbar = t2_mapa(&full[s], 0);
+                const int kc = (kb0 + kb) * TC_BK;
+                t2_tma(tile_ahi(s), &tm_ahi, kc, m0, lbar);
+                t2_tma(tile_alo(s), &tm_alo, kc, m0, lbar);
+                t2_tma(tile_bhi(s), &tm_bhi, kc, nb0, lbar);
+                t2_tma(tile_blo(s), &tm_blo, kc, nb0, lbar);
+            }
+        }
+    } else if (warp == 1) {
+        if (leader && lane == 0) {
+            constexpr uint32_t idesc = tf32_idesc(2 * T2_BM, 2 * T2_BNH);
+            for (int c = 0; c < nchunks; ++c) {
+                const int b = c & 1;
+                if (c >= 2) t2_wait_cluster(&acc_empty[b], (uint32_t)(((c >> 1) - 1) & 1));
+                tc_fence_after();
+                const uint32_t d = tmem + (uint32_t)(b * TC_BN);
+                const int kb_end = (c + 1) * TC_CHUNK_KB < nk ? (c + 1) * TC_CHUNK_KB : nk;
+                for (int kb = c * TC_CHUNK_KB; kb < kb_end; ++kb) {
+                    const int s = kb % T2_STAGES;
+                    t2_wait_cluster(&full[s], (uint32_t)((kb / T2_STAGES) & 1));
+                    tc_fence_after();
+                    const uint64_t ahi = sw64_kmajor_desc(smem_u32(tile_ahi(s)));
+                    const uint64_t alo = sw64_kmajor_desc(smem_u32(tile_alo(s)));
+                    const uint64_t bhi = sw64_kmajor_desc(smem_u32(tile_bhi(s)));
+                    const uint64_t blo = sw64_kmajor_desc(smem_u32(tile_blo(s)));
+#pragma unroll
+                    for (int kk = 0; kk < TC_BK / 8; ++kk) {
+                        const uint64_t adv = (uint64_t)((kk * 32) >> 4);
+                        const uint32_t first = (kb == c * TC_CHUNK_KB && kk == 0) ? 0u : 1u;
+                        t2_mma(d, alo + adv, bhi + adv, idesc, first);
+                        t2_mma(d, ahi + adv, blo + adv, idesc, 1u);
+                        t2_mma(d, ahi + adv, bhi + adv, idesc, 1u);
+                    }
+                    t2_commit_both(&empty[s]);
+                }
+                t2_commit_both(&acc_full[b]);
+            }
+        }
+    } else {
+        // epilogue warps 2..9 of both CTAs: this CTA's 128 rows of the tile
+        const int q = warp & 3;
+        const int h = (warp - 2) >> 2;
+        const i64 row = (i64)m0 + 32 * q + lane;
+        float acc[128];
+        if (accumulate && row < m) {
+            const float* cp = C + row + ((i64)n0 + h * 128) * ldc;
+            const int ncol = (int)(n - n0 - h * 128 < 128 ? n - n0 - h * 128 : 128);
+#pragma unroll
+            for (int t = 0; t < 128; ++t) acc[t] = t < ncol ? __ldg(cp + t * ldc) : 0.f;
+        } else {
+#pragma unroll
+            for (int t = 0; t < 128; ++t) acc[t] = 0.f;
+        }
+        for (int c = 0; c < nchunks; ++c) {
+            const int b = c & 1;
+            t2_wait_cluster(&acc_full[b], (uint32_t)((c >> 1) & 1));
+            tc_fence_after();
+            const uint32_t base = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(b * TC_BN + h * 128);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                uint32_t v[32];
+                tmem_ld_32x32b_x32(base + (uint32_t)(j * 32), v);
+                tmem_ld_wait();
+#pragma unroll
+                for (int t = 0; t < 32; ++t) acc[j * 32 + t] += __uint_as_float(v[t]);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) t2_arrive_remote(t2_mapa(&acc_empty[b], 0));
+        }
+        if (row < m) {
+#pragma unroll
+            for (int t = 0; t < 128; ++t) {
+                const i64 col = (i64)n0 + h * 128 + t;
+                if (col < n) C[row + col * ldc] = acc[t];
+            }
+        }
+    }
+    tc_fence_before();
+    t2_cluster_sync();
+    tc_fence_after();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * TC_BN) : "memory");
+}
+
+// ---------------------------------------------------------------------------
 // f64: DMMA m8n8k4 (mma.sync f64 runs on the FP64 tensor path of sm_100).
 // CTA tile 64x128 (two CTAs per SM), 4 warps of 32x64 (4x8 DMMA tiles each,
 // 64 f64 accumulators per lane), K staged 16 at a time through a 4-stage
@@ -412,10 +655,13 @@ static int split_operand(const float* src, int64_t ld, bool kmajor, int64_t rows
 int gemm_tc_f32_core(int64_t m, int64_t n, int64_t k, const SplitFn& split_a, const SplitFn& split_b, float* C,
                      int64_t ldc, bool* handled) {
     *handled = false;
-    const int64_t mp = (m + TC_BM - 1) / TC_BM * TC_BM;
-    const int64_t np = (n + TC_BN - 1) / TC_BN * TC_BN;
+    // CTA pairs (cta_group::2, 256 x 256 tiles) unless BM_GEMM_PAIR=0
+    static const bool pair = !std::getenv("BM_GEMM_PAIR") || std::atoi(std::getenv("BM_GEMM_PAIR")) != 0;
+    const int64_t tm_ = pair ? 2 * T2_BM : TC_BM, tn_ = pair ? 2 * T2_BNH : TC_BN;
+    const int64_t mp = (m + tm_ - 1) / tm_ * tm_;
+    const int64_t np = (n + tn_ - 1) / tn_ * tn_;
     const int64_t kp = (k + 31) / 32 * 32;   // split kernel tiles K by 32
-    if (mp / TC_BM > 65535 || np / TC_BN > (1LL << 31) - 1) return BM_OK;
+    if ((mp / tm_) * (np / tn_) * (pair ? 2 : 1) > (1LL << 31) - 1) return BM_OK;
     cudaStream_t s = st().stream;
     float* buf = nullptr;
     const int64_t a_elems = mp * kp, b_elems = np * kp;
@@ -426,19 +672,21 @@ int gemm_tc_f32_core(int64_t m, int64_t n, int64_t k, const SplitFn& split_a, co
     CUtensorMap tm[4];
     if (!rc) rc = encode_kmajor(&tm[0], ahi, kp, mp, TC_BM);
     if (!rc) rc = encode_kmajor(&tm[1], alo, kp, mp, TC_BM);
-    if (!rc) rc = encode_kmajor(&tm[2], bhi, kp, np, TC_BN);
-    if (!rc) rc = encode_kmajor(&tm[3], blo, kp, np, TC_BN);
+    if (!rc) rc = encode_kmajor(&tm[2], bhi, kp, np, pair ? T2_BNH : TC_BN);
+    if (!rc) rc = encode_kmajor(&tm[3], blo, kp, np, pair ? T2_BNH : TC_BN);
     if (!rc) {
         static bool attr = false;
         if (!attr) {
             cudaError_t e = cudaFuncSetAttribute(bm::gemm_3xtf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  TC_SMEM);
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(bm::gemm_3xtf32_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, T2_SMEM);
             if (e != cudaSuccess) rc = cuda_fail(e, "cudaFuncSetAttribute (3xTF32)");
             attr = true;
         }
     }
     if (!rc) {
-        dim3 grid((unsigned)((np / TC_BN) * (mp / TC_BM)));
+        dim3 grid((unsigned)((np / tn_) * (mp / tm_) * (pair ? 2 : 1)));
         static const int group_m = std::getenv("BM_GEMM_GROUP") ? std::atoi(std::getenv("BM_GEMM_GROUP")) : 8;
         // Long K runs as several stream-ordered passes of at most kpass K
         // (the later ones add into C): within one launch the resident CTAs
@@ -452,8 +700,12 @@ int gemm_tc_f32_core(int64_t m, int64_t n, int64_t k, const SplitFn& split_a, co
         if (pass_kb <= 0 || pass_kb >= nk) pass_kb = nk;
         for (int kb0 = 0; kb0 < nk && !rc; kb0 += pass_kb) {
             const int len = nk - kb0 < pass_kb ? nk - kb0 : pass_kb;
-            bm::gemm_3xtf32_kernel<<<grid, TC_THREADS, TC_SMEM, s>>>(tm[0], tm[1], tm[2], tm[3], C, m, n, ldc, len,
-                                                                      group_m > 0 ? group_m : 8, kb0, kb0 > 0);
+            if (pair)
+                bm::gemm_3xtf32_pair_kernel<<<grid, TC_THREADS, T2_SMEM, s>>>(tm[0], tm[1], tm[2], tm[3], C, m, n, ldc,
+                                                                               len, group_m > 0 ? group_m : 8, kb0, kb0 > 0);
+            else
+                bm::gemm_3xtf32_kernel<<<grid, TC_THREADS, TC_SMEM, s>>>(tm[0], tm[1], tm[2], tm[3], C, m, n, ldc, len,
+                                                                          group_m > 0 ? group_m : 8, kb0, kb0 > 0);
             cudaError_t e = cudaGetLastError();
             if (e != cudaSuccess) rc = cuda_fail(e, "3xTF32 GEMM launch");
             else st().launches++;

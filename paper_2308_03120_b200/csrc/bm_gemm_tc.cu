@@ -687,7 +687,10 @@ int gemm_tc_f32_core(int64_t m, int64_t n, int64_t k, const SplitFn& split_a, co
     }
     if (!rc) {
         dim3 grid((unsigned)((np / tn_) * (mp / tm_) * (pair ? 2 : 1)));
-        static const int group_m = std::getenv("BM_GEMM_GROUP") ? std::atoi(std::getenv("BM_GEMM_GROUP")) : 8;
+        // tile rows per raster group: 4 pair rows (1024 rows of C) measured best for
+        // the pair kernel (8192^3..32768^3), 8 single-CTA rows for the other
+        static const int group_env = std::getenv("BM_GEMM_GROUP") ? std::atoi(std::getenv("BM_GEMM_GROUP")) : 0;
+        const int group_m = group_env > 0 ? group_env : (pair ? 4 : 8);
         // Long K runs as several stream-ordered passes of at most kpass K
         // (the later ones add into C): within one launch the resident CTAs
         // drift apart along K, and at K = 32768 their A/B slabs stop meeting

@@ -369,7 +369,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
     }
     tc_fence_before();
-    t2_cluster_sync();
+    t2_cluster_sync();                         // peers' barriers initialised
+    __syncthreads();                           // and this CTA's TMEM address published
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 

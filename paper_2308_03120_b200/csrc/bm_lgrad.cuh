@@ -44,15 +44,18 @@ namespace bm {
 #define LG_RB 64            // rows per slab (256 B of f32: full-rate TMA rows)
 #endif
 #define LG_BOXC 128         // columns per TMA box (32 KB)
-#ifndef LG_CLUSTER
-#define LG_CLUSTER 4        // CTAs per slab (clusters of 8 fit only 15 x 8 SMs at once)
-#endif
+#define LG_CLUSTER 2        // CTAs per slab: a CTA pair is one TPC, so pairs tile all 148 SMs
 #define LG_COLS (1024 / LG_CLUSTER)   // columns per CTA (LG_CLUSTER * LG_COLS = 1024 = k max)
 #define LG_KMAX (LG_CLUSTER * LG_COLS)
-#define LG_STAGES ((192 * 1024) / (LG_RB * LG_COLS * 4))
-#define LG_THREADS (LG_COLS * 2)      // warps of 16 columns each
-#define LG_STAGE_BYTES (LG_RB * LG_COLS * 4)
-#define LG_TMEM_COLS 256                      // two slabs of 64 rows x 256 columns parked in TMEM
+#define LG_NB (LG_COLS / LG_BOXC)     // boxes per slab per CTA
+#define LG_NBOX 6                     // ring of boxes (192 KB)
+#define LG_BOX_BYTES (LG_RB * LG_BOXC * 4)
+#define LG_STAGES (LG_NBOX / LG_NB)   // (launcher: ring bytes = LG_STAGES * LG_STAGE_BYTES)
+#define LG_STAGE_BYTES (LG_NBOX * LG_BOX_BYTES / LG_STAGES)
+#define LG_CW 32                      // columns per compute warp
+#define LG_THREADS (LG_COLS / LG_CW * 32)   // compute threads (16 warps)
+#define LG_BLOCK (LG_THREADS + 32)    // + one TMA producer warp
+#define LG_TMEM_COLS 512              // two slabs x 64 values per thread parked in TMEM
 
 struct alignas(64) LgTmap {
     unsigned long long v[16];   // CUtensorMap (128 B, opaque)
@@ -157,10 +160,10 @@ template <class E>
 __device__ void logistic_grad(const LgArgs& L) {
     extern __shared__ __align__(1024) char lg_raw[];
     char* ring = lg_raw + ((1024 - (lg_smem(lg_raw) & 1023)) & 1023);
-    __shared__ unsigned long long full[LG_STAGES], empty[LG_STAGES];
-    __shared__ unsigned long long zbar[2];                // peers' z partials of a slab landed (by parity)
+    __shared__ unsigned long long full[LG_NBOX], empty[LG_NBOX];
+    __shared__ unsigned long long zbar[2];                // the peer's z partial of a slab landed (by parity)
     __shared__ double zpart[2][LG_THREADS / 32][LG_RB];   // by slab parity
-    __shared__ double zq_all[2][LG_CLUSTER][LG_RB];   // the cluster's partial z, by slab parity (pushed by each CTA)
+    __shared__ double zq_all[2][LG_CLUSTER][LG_RB];   // the cluster's partial z, by slab parity
     __shared__ __align__(16) float rs[2][LG_RB];
     __shared__ float ws[LG_COLS];
     __shared__ unsigned tmem_slot;
@@ -169,202 +172,209 @@ __device__ void logistic_grad(const LgArgs& L) {
     const i64 cluster = blockIdx.x / LG_CLUSTER, nclusters = gridDim.x / LG_CLUSTER;
     const i64 nmine = L.nslabs > cluster ? (L.nslabs - cluster + nclusters - 1) / nclusters : 0;
     const int col0 = (int)q * LG_COLS;                  // this CTA's first column
-    for (int c = tid; c < LG_COLS; c += LG_THREADS) ws[c] = (col0 + c < L.k) ? L.w[col0 + c] : 0.f;
+    for (int c = tid; c < LG_COLS; c += LG_BLOCK) ws[c] = (col0 + c < L.k) ? L.w[col0 + c] : 0.f;
     if (tid == 0) {
-        for (int s = 0; s < LG_STAGES; ++s) {
+        for (int s = 0; s < LG_NBOX; ++s) {
             lg_bar_init(&full[s], 1);
-            lg_bar_init(&empty[s], LG_THREADS / 32);
+            lg_bar_init(&empty[s], LG_BOXC / LG_CW);   // the compute warps reading the box
         }
         lg_bar_init(&zbar[0], 1);
         lg_bar_init(&zbar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&L.tmx) : "memory");
     }
-    if (warp == 0) {                           // 2 slabs x 128 columns of TMEM
+    if (warp == 0) {                           // 2 slabs x 256 columns of TMEM
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(lg_smem(&tmem_slot)),
                      "r"(LG_TMEM_COLS)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    lg_cluster_sync();                         // peers' zbar initialised before anyone pushes
+    lg_cluster_sync();                         // the peer's zbar initialised before anyone pushes
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    // this thread's parking place: its warp's lane quarter, 32 columns per warp group
-    const unsigned tmem_me = tmem_slot + ((unsigned)(32 * (warp & 3)) << 16) + (unsigned)(32 * (warp >> 2));
-    auto issue = [&](i64 j) {   // this CTA's quarter of slab j into stage j % STAGES
-        const int s = (int)(j % LG_STAGES);
-        const i64 slab = cluster + j * nclusters;
-        lg_expect_tx(&full[s], LG_STAGE_BYTES);
-#pragma unroll
-        for (int b = 0; b < (LG_COLS + LG_BOXC - 1) / LG_BOXC; ++b)
-            lg_tma_2d(ring + s * LG_STAGE_BYTES + b * (LG_BOXC * LG_RB * 4), &L.tmx, (int)(slab * LG_RB),
-                      col0 + b * LG_BOXC, &full[s]);
-    };
-    if (tid == 0)
-        for (i64 j = 0; j < LG_STAGES && j < nmine; ++j) issue(j);
 
-    typename E::Pre pre;                       // chain inputs of the next slab (threads < LG_RB)
-    double gacc = 0.0;                         // one column per even lane (see phase 2)
-    const int wc = 16 * warp;                  // this warp's 16 columns within the CTA's 256
-    // Lane layout (LG_RB = 64): half-warp hc = lane / 16 takes columns
-    // wc + 8 hc .. wc + 8 hc + 7, lane hl = lane % 16 rows 4 hl .. 4 hl + 3, so
-    // every shared-memory read is one 16-byte row quad of one column.
-    static_assert(LG_RB == 64, "lane layout assumes 64-row slabs");
-    const int hl = lane & 15, hc = lane >> 4;
-    const int cw = wc + 8 * hc;                // this half-warp's first column
-    auto ldx4 = [&](int s, int c) -> float4 {
-        return *reinterpret_cast<const float4*>(ring + s * LG_STAGE_BYTES + (c >> 7) * (LG_BOXC * LG_RB * 4) +
-                                                (c & 127) * (LG_RB * 4) + 16 * hl);
-    };
-    // phase 1 of slab j: an f32 chain per row over the half-warp's 8 columns
-    // (the reference's z is an f32 sgemv); the two halves, the 16 warp
-    // partials and the 4 CTA partials are added in f64 in a fixed order
-    auto phase1 = [&](i64 j) {
-        const int s = (int)(j % LG_STAGES);
-        lg_wait(&full[s], (unsigned)((j / LG_STAGES) & 1));
-        float xs[32];                          // [column u][row h], parked in TMEM for phase 2
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const float4 x = ldx4(s, cw + u);
-            xs[4 * u] = x.x;
-            xs[4 * u + 1] = x.y;
-            xs[4 * u + 2] = x.z;
-            xs[4 * u + 3] = x.w;
-        }
-        __syncwarp();
-        if (lane == 0) lg_arrive(&empty[s]);   // the stage is free: its values are in registers
-        lg_tmem_st32(tmem_me + (unsigned)((j & 1) * 128), xs);
-        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const float w = ws[cw + u];
-            a0 = __fmaf_rn(xs[4 * u], w, a0);
-            a1 = __fmaf_rn(xs[4 * u + 1], w, a1);
-            a2 = __fmaf_rn(xs[4 * u + 2], w, a2);
-            a3 = __fmaf_rn(xs[4 * u + 3], w, a3);
-        }
-        const int par = (int)(j & 1);
-        double d[4] = {(double)a0, (double)a1, (double)a2, (double)a3};
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-            const double o = __shfl_xor_sync(0xffffffffu, d[h], 16);
-            if (hc == 0) zpart[par][warp][4 * hl + h] = d[h] + o;   // low half + high half
-        }
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-    };
-    // publish this CTA's partial z of slab j: st.async into the three peers'
-    // zq_all, each store completing bytes on the peer's zbar[parity] (no
-    // fence, no cluster barrier); its own copy is a plain local store.  The
-    // expect_tx for the peers' bytes is posted by thread 0 (the phase may see
-    // the bytes first: the tx-count goes negative until then).  A slot is
-    // rewritten two slabs later only after its reader published the slab in
-    // between, which the writer had to receive first.
-    auto publish = [&](i64 j) {
-        const int par = (int)(j & 1);
-        if (tid == 0) lg_expect_tx(&zbar[par], (LG_CLUSTER - 1) * LG_RB * 8);
-        if (tid < LG_RB) {
-            // balanced tree over the warp partials (fixed order, 4 levels deep)
-            double t[LG_THREADS / 32];
-#pragma unroll
-            for (int w = 0; w < LG_THREADS / 32; ++w) t[w] = zpart[par][w][tid];
-#pragma unroll
-            for (int h = 1; h < LG_THREADS / 32; h <<= 1)
-#pragma unroll
-                for (int w = 0; w + h < LG_THREADS / 32; w += 2 * h) t[w] = t[w] + t[w + h];
-            zq_all[par][q][tid] = t[0];
-#pragma unroll
-            for (unsigned p = 1; p < LG_CLUSTER; ++p) {
-                const unsigned peer = (q + p) % LG_CLUSTER;
-                unsigned raddr, rbar;
-                asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(lg_smem(&zq_all[par][q][tid])), "r"(peer));
-                asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbar) : "r"(lg_smem(&zbar[par])), "r"(peer));
-                asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(raddr),
-                             "d"(t[0]), "r"(rbar)
-                             : "memory");
+    // ---- producer warp: boxes (slab j, box b) in order through the 6-box ring
+    if (warp == LG_THREADS / 32) {
+        if (lane == 0) {
+            const i64 nboxes = nmine * LG_NB;
+            for (i64 i = 0; i < nboxes; ++i) {
+                const int s = (int)(i % LG_NBOX);
+                if (i >= LG_NBOX) lg_wait(&empty[s], (unsigned)(((i / LG_NBOX) - 1) & 1));
+                const i64 j = i / LG_NB;
+                const int b = (int)(i % LG_NB);
+                const i64 slab = cluster + j * nclusters;
+                lg_expect_tx(&full[s], LG_BOX_BYTES);
+                lg_tma_2d(ring + s * LG_BOX_BYTES, &L.tmx, (int)(slab * LG_RB), col0 + b * LG_BOXC, &full[s]);
             }
         }
-    };
-    // z of slab j (four partials in rank order, once the peers' bytes landed) and r
-    auto chain = [&](i64 j) {
-        const int par = (int)(j & 1);
-        if (tid < LG_RB) {
-            lg_wait_cluster(&zbar[par], (unsigned)((j >> 1) & 1));
-            double z = zq_all[par][0][tid];
+    } else {
+        // ---- compute warps
+        typename E::Pre pre;                   // chain inputs of the next slab (threads < LG_RB)
+        double gacc = 0.0;                     // this lane's column (see phase 2)
+        // Lane layout (LG_RB = 64): warp w owns columns 32 w .. 32 w + 31 (inside box
+        // w / 4); half-warp hc = lane / 16 takes 16 of them, lane hl = lane % 16 rows
+        // 4 hl .. 4 hl + 3, so every shared-memory read is one 16-byte row quad.
+        static_assert(LG_RB == 64, "lane layout assumes 64-row slabs");
+        const int hl = lane & 15, hc = lane >> 4;
+        const int cw = LG_CW * warp + 16 * hc;     // this half-warp's first column (CTA-relative)
+        const int bx = (LG_CW * warp) / LG_BOXC;   // the box holding them
+        const int cb = cw - bx * LG_BOXC;          // ... and their offset in it
+        // TMEM parking place: the warp's lane quarter, 64 columns per warp group of 4
+        const unsigned tmem_me = tmem_slot + ((unsigned)(32 * (warp & 3)) << 16) + (unsigned)(64 * (warp >> 2));
+        auto ldx4 = [&](int s, int c) -> float4 {
+            return *reinterpret_cast<const float4*>(ring + s * LG_BOX_BYTES + c * (LG_RB * 4) + 16 * hl);
+        };
+        // phase 1 of slab j: an f32 chain per row over the half-warp's 16 columns
+        // (the reference's z is an f32 sgemv); the two halves, the 16 warp
+        // partials and the 2 CTA partials are added in f64 in a fixed order
+        auto phase1 = [&](i64 j) {
+            const i64 i = j * LG_NB + bx;
+            const int s = (int)(i % LG_NBOX);
+            lg_wait(&full[s], (unsigned)((i / LG_NBOX) & 1));
+            float xs[64];                      // [column u][row h], parked in TMEM for phase 2
 #pragma unroll
-            for (unsigned p = 1; p < LG_CLUSTER; ++p) z = z + zq_all[par][p][tid];
-            const i64 row = (cluster + j * nclusters) * LG_RB + tid;
-            float r = 0.f;
-            if (row < L.m) {
-                r = E::at(L.a, pre, (float)z);
-                if (q == 0) L.r[row] = r;
+            for (int u = 0; u < 16; ++u) {
+                const float4 x = ldx4(s, cb + u);
+                xs[4 * u] = x.x;
+                xs[4 * u + 1] = x.y;
+                xs[4 * u + 2] = x.z;
+                xs[4 * u + 3] = x.w;
             }
-            rs[par][tid] = r;
-        }
-    };
-    // phase 2 of slab j: each lane's 4-row partial sums for its 8 columns, a
-    // transpose-reduce across the 16 lanes of the half-warp (7 shuffles for 8
-    // columns, then one across the lane pair), after which even lanes own
-    // column cw + 4 b3 + 2 b2 + b1 (b = lane bits) for the whole kernel
-    auto phase2 = [&](i64 j) {
-        const int par = (int)(j & 1);
-        const float4 rr = *reinterpret_cast<const float4*>(&rs[par][4 * hl]);
-        float xs[32];
-        lg_tmem_ld32(tmem_me + (unsigned)((j & 1) * 128), xs);
-        float v[8];
+            __syncwarp();
+            if (lane == 0) lg_arrive(&empty[s]);   // the box is free: its values are in registers
+            const unsigned t = tmem_me + (unsigned)((j & 1) * 256);
+            lg_tmem_st32(t, *reinterpret_cast<const float(*)[32]>(&xs[0]));
+            lg_tmem_st32(t + 32, *reinterpret_cast<const float(*)[32]>(&xs[32]));
+            float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-            float acc = xs[4 * c] * rr.x;
-            acc = __fmaf_rn(xs[4 * c + 1], rr.y, acc);
-            acc = __fmaf_rn(xs[4 * c + 2], rr.z, acc);
-            v[c] = __fmaf_rn(xs[4 * c + 3], rr.w, acc);
-        }
-#pragma unroll
-        for (int off = 8, n = 4; off >= 2; off >>= 1, n >>= 1) {
-            const bool upper = (lane & off) != 0;
-#pragma unroll
-            for (int c = 0; c < n; ++c) {
-                const float send = upper ? v[c] : v[c + n];
-                const float keep = upper ? v[c + n] : v[c];
-                v[c] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+            for (int u = 0; u < 16; ++u) {
+                const float w = ws[cw + u];
+                a0 = __fmaf_rn(xs[4 * u], w, a0);
+                a1 = __fmaf_rn(xs[4 * u + 1], w, a1);
+                a2 = __fmaf_rn(xs[4 * u + 2], w, a2);
+                a3 = __fmaf_rn(xs[4 * u + 3], w, a3);
             }
-        }
-        v[0] = v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
-        gacc += (double)v[0];
-    };
+            const int par = (int)(j & 1);
+            double d[4] = {(double)a0, (double)a1, (double)a2, (double)a3};
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const double o = __shfl_xor_sync(0xffffffffu, d[h], 16);
+                if (hc == 0) zpart[par][warp][4 * hl + h] = d[h] + o;   // low half + high half
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        };
+        // publish this CTA's partial z of slab j: st.async into the peer's zq_all,
+        // completing bytes on the peer's zbar[parity] (no fence, no cluster
+        // barrier); its own copy is a plain local store.  Thread 0 posts the
+        // expect_tx for the peer's bytes (the phase may see the bytes first: the
+        // tx-count goes negative until then).  A slot is rewritten two slabs later
+        // only after its reader published the slab in between, which the writer
+        // had to receive first.
+        auto publish = [&](i64 j) {
+            const int par = (int)(j & 1);
+            if (tid == 0) lg_expect_tx(&zbar[par], (LG_CLUSTER - 1) * LG_RB * 8);
+            if (tid < LG_RB) {
+                // balanced tree over the warp partials (fixed order, 4 levels deep)
+                double t[LG_THREADS / 32];
+#pragma unroll
+                for (int w = 0; w < LG_THREADS / 32; ++w) t[w] = zpart[par][w][tid];
+#pragma unroll
+                for (int h = 1; h < LG_THREADS / 32; h <<= 1)
+#pragma unroll
+                    for (int w = 0; w + h < LG_THREADS / 32; w += 2 * h) t[w] = t[w] + t[w + h];
+                zq_all[par][q][tid] = t[0];
+#pragma unroll
+                for (unsigned p = 1; p < LG_CLUSTER; ++p) {
+                    const unsigned peer = (q + p) % LG_CLUSTER;
+                    unsigned raddr, rbar;
+                    asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(lg_smem(&zq_all[par][q][tid])), "r"(peer));
+                    asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbar) : "r"(lg_smem(&zbar[par])), "r"(peer));
+                    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(raddr),
+                                 "d"(t[0]), "r"(rbar)
+                                 : "memory");
+                }
+            }
+        };
+        // z of slab j (the partials in rank order, once the peer's bytes landed) and r
+        auto chain = [&](i64 j) {
+            const int par = (int)(j & 1);
+            if (tid < LG_RB) {
+                lg_wait_cluster(&zbar[par], (unsigned)((j >> 1) & 1));
+                double z = zq_all[par][0][tid];
+#pragma unroll
+                for (unsigned p = 1; p < LG_CLUSTER; ++p) z = z + zq_all[par][p][tid];
+                const i64 row = (cluster + j * nclusters) * LG_RB + tid;
+                float r = 0.f;
+                if (row < L.m) {
+                    r = E::at(L.a, pre, (float)z);
+                    if (q == 0) L.r[row] = r;
+                }
+                rs[par][tid] = r;
+            }
+        };
+        // phase 2 of slab j: the slab's values back from TMEM, each lane's 4-row
+        // partial sums for its 16 columns, then a transpose-reduce across the 16
+        // lanes of the half-warp (15 shuffles), after which lane l owns column
+        // cw + (l & 15) (bit-reversed order: 8 b3 + 4 b2 + 2 b1 + b0)
+        auto phase2 = [&](i64 j) {
+            const int par = (int)(j & 1);
+            const float4 rr = *reinterpret_cast<const float4*>(&rs[par][4 * hl]);
+            float xs[64];
+            const unsigned t = tmem_me + (unsigned)((j & 1) * 256);
+            lg_tmem_ld32(t, *reinterpret_cast<float(*)[32]>(&xs[0]));
+            lg_tmem_ld32(t + 32, *reinterpret_cast<float(*)[32]>(&xs[32]));
+            float v[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+                float acc = xs[4 * c] * rr.x;
+                acc = __fmaf_rn(xs[4 * c + 1], rr.y, acc);
+                acc = __fmaf_rn(xs[4 * c + 2], rr.z, acc);
+                v[c] = __fmaf_rn(xs[4 * c + 3], rr.w, acc);
+            }
+#pragma unroll
+            for (int off = 8, n = 8; off >= 1; off >>= 1, n >>= 1) {
+                const bool upper = (lane & off) != 0;
+#pragma unroll
+                for (int c = 0; c < n; ++c) {
+                    const float send = upper ? v[c] : v[c + n];
+                    const float keep = upper ? v[c + n] : v[c];
+                    v[c] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+                }
+            }
+            gacc += (double)v[0];
+        };
 
-    // Software pipeline: the partials of slab j + 1 are in flight while
-    // this CTA runs phase 2 of slab j.
-    if (nmine > 0) {
-        if (tid < LG_RB) {
-            const i64 row = cluster * LG_RB + tid;
-            if (row < L.m) E::load(L.a, row, pre);
+        // Software pipeline: the partials of slab j + 1 travel while this CTA
+        // runs phase 2 of slab j.  Named barrier 1 spans the compute warps only
+        // (the producer warp never joins).
+        auto csync = [&]() { asm volatile("bar.sync 1, %0;" ::"n"(LG_THREADS) : "memory"); };
+        if (nmine > 0) {
+            if (tid < LG_RB) {
+                const i64 row = cluster * LG_RB + tid;
+                if (row < L.m) E::load(L.a, row, pre);
+            }
+            phase1(0);
+            csync();
+            publish(0);
         }
-        phase1(0);
-        __syncthreads();
-        publish(0);
-    }
-    for (i64 j = 0; j < nmine; ++j) {
-        if (tid == 0 && j + LG_STAGES < nmine) {   // stage j % STAGES was freed by phase 1 of slab j
-            const i64 jn = j + LG_STAGES;
-            lg_wait(&empty[jn % LG_STAGES], (unsigned)(((jn / LG_STAGES) - 1) & 1));
-            issue(jn);
+        for (i64 j = 0; j < nmine; ++j) {
+            chain(j);
+            if (j + 1 < nmine && tid < LG_RB) {   // y & co. of slab j + 1 into registers now
+                const i64 row = (cluster + (j + 1) * nclusters) * LG_RB + tid;
+                if (row < L.m) E::load(L.a, row, pre);
+            }
+            if (j + 1 < nmine) phase1(j + 1);
+            csync();                              // r of slab j and the z partials of slab j + 1
+            if (j + 1 < nmine) publish(j + 1);
+            phase2(j);
         }
-        chain(j);
-        if (j + 1 < nmine && tid < LG_RB) {      // y & co. of slab j + 1 into registers now
-            const i64 row = (cluster + (j + 1) * nclusters) * LG_RB + tid;
-            if (row < L.m) E::load(L.a, row, pre);
+        {
+            const int c = col0 + cw + 8 * ((lane >> 3) & 1) + 4 * ((lane >> 2) & 1) + 2 * ((lane >> 1) & 1) + (lane & 1);
+            if (c < L.k) L.gpart[cluster * L.k + c] = gacc;
         }
-        if (j + 1 < nmine) phase1(j + 1);
-        __syncthreads();                       // r of slab j and the z partials of slab j + 1
-        if (j + 1 < nmine) publish(j + 1);
-        phase2(j);
-    }
-    if ((lane & 1) == 0) {
-        const i64 c = col0 + cw + 4 * ((lane >> 3) & 1) + 2 * ((lane >> 2) & 1) + ((lane >> 1) & 1);
-        if (c < L.k) L.gpart[cluster * L.k + c] = gacc;
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    lg_cluster_sync();                             // no CTA exits while a peer may still read its zq
+    lg_cluster_sync();                             // no CTA exits while its peer may still write its zq
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_slot), "r"(LG_TMEM_COLS)
                      : "memory");

@@ -10,25 +10,26 @@
 // x all k columns.  TMA moves 2-D boxes of 64 rows (256 B, the inner extent
 // that streams at full HBM rate; 64-B rows stream at a third of it,
 // tools/tma2d_probe.cu) x 128 columns.  A slab of 64 x 1024 f32 is 256 KB --
-// more than one SM holds -- so a cluster of 4 CTAs shares it: CTA q of the
-// cluster owns columns [256q, 256q + 256), streamed through a 3-stage TMA ring
-// of 64 KB quarters.  Phase 1 moves its quarter from shared memory into
-// registers and parks it in TMEM (tcgen05.st, 128 columns per slab, two
-// slabs), so the stage is refilled at once and phase 2 reads the slab back
-// from TMEM: two stages stay in flight instead of one.  Per slab:
+// more than one SM holds -- so a CTA pair (cluster of 2: one TPC, so 74
+// pairs tile all 148 SMs, where clusters of 4 fitted only 33 times) shares
+// it: CTA q owns columns [512q, 512q + 512), four boxes per slab, which a
+// producer warp streams through a 6-box ring.  Each compute warp owns 32
+// columns inside one box; phase 1 moves its values from shared memory into
+// registers, releases the box, and parks them in TMEM (tcgen05.st, 256
+// columns per slab, two slabs), so boxes refill at once and phase 2 reads
+// the slab back from TMEM.  Per slab:
 //   phase 1  each CTA computes partial z over its columns (f32 chains as in
 //            the reference's sgemv, partials added in f64; fixed order) and
-//            pushes them into the peers' shared memory (st.async, completing
+//            pushes it into the peer's shared memory (st.async, completing
 //            bytes on the peer's mbarrier -- no fence, no cluster barrier);
-//            once they land every CTA sums the four partials in rank order
-//            (identical z in all four CTAs);
+//            once it lands both CTAs sum the two partials in rank order
+//            (identical z in both);
 //            the program inputs of the next slab are loaded into registers;
 //   chain    r_i = F(round_f32(z_i), y_i, ...) -- the fused element-wise
 //            program, every stage rounded to f32 like the unfused plan;
-//   phase 2  each CTA adds sum_i X_ic r_i for its columns from its resident
-//            quarter: a lane reads 4-row quads of 8 columns (16-byte shared
-//            loads), then a transpose-reduce across its half-warp (8 shuffles
-//            for 8 columns) leaves each even lane one column's f64
+//   phase 2  each CTA adds sum_i X_ic r_i for its columns: a lane holds
+//            4-row quads of 16 columns, then a transpose-reduce across its
+//            half-warp (15 shuffles) leaves each lane one column's f64
 //            accumulator for the whole kernel.
 // The loop is software-pipelined: while the partials of slab j + 1 travel,
 // the CTA runs phase 2 of slab j.

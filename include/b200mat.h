@@ -85,11 +85,13 @@ extern "C" {
                                     (iparams[0] of them), then B's; prog: A's stages (iparams[1]),
                                     then B's (loads relative to B's inputs); iparams[2], [3] = stored
                                     rows of A and B; [4..6] = m, n, k; output C (m x n)            */
-#define BM_K_RDIM_FUSED     17   /* sum / mean / min / max over dim 0 of an element-wise program
+#define BM_K_RDIM_FUSED     17   /* sum / mean / min / max over dim 0 or 1 of an element-wise program
                                     (expr.py:583-594 materialises it first): inputs = the program's
-                                    flat inputs of rows * cols elements (column-major); iparams[0] =
-                                    rows; reduce_op = BM_R_ACCU / MIN / MAX / MEAN; output = cols
-                                    values of the compute dtype                                     */
+                                    flat inputs of rows * cols elements (column-major); dim = 0 / 1;
+                                    iparams[0] = rows, iparams[1] = cols (dim 1); reduce_op =
+                                    BM_R_ACCU / MIN / MAX / MEAN; output = cols (dim 0) or rows
+                                    (dim 1) values of the compute dtype.  dim 1 takes 1-4 inputs of
+                                    the compute dtype, 16-B aligned, rows * size % 16 == 0 (TMA)   */
 
 /* comparison of a predicate (kernels.py:643-657 _predicate_mask) */
 #define BM_CMP_GT 0

@@ -157,3 +157,98 @@ __device__ __forceinline__ void rdim0_col_body(const S& s, i64 rows, i64 cols, i
 }
 
 }  // namespace bm
+
+// ---------------------------------------------------------------------------
+// dim 1 (one value per row) of an element-wise program, TMA-staged: the
+// reference folds each row left to right, 0 + v[:,0] + v[:,1] + ... (numpy's
+// row-block reduction, kernels.py:502-531).  A CTA owns 112 rows; a producer
+// warp streams every input's [112 rows x CT columns] tile of the slab through
+// a 3-stage mbarrier ring (CT = 64 / inputs, so a stage stays <= 56 KB), and
+// thread r folds row r column by column, evaluating the program on the staged
+// values (E::at over E::Pre) -- the same values and order as reducing the
+// materialised matrix.  Used by the JIT's fused variant (bm_jit.cu).
+#include "bm_lgrad.cuh"
+
+namespace bm {
+
+#define BM_R1F_ROWS 112
+#define BM_R1F_STAGES 3
+
+struct R1Args {                 // one __grid_constant__ parameter, like LgArgs
+    Args a;                     // program inputs and scalars
+    LgTmap m[4];                // the inputs as [rows x cols] tensor maps
+    i64 rows, cols;
+    void* out;
+};
+
+template <typename T, int OP, class E, int NIN>
+__device__ __forceinline__ void rdim1_fused_body(const R1Args& P) {
+    const Args& a = P.a;
+    const i64 rows = P.rows, cols = P.cols;
+    T* out = reinterpret_cast<T*>(P.out);
+    constexpr int RT = BM_R1F_ROWS;
+    constexpr int CT = NIN == 1 ? 64 : (NIN == 2 ? 32 : 16);
+    constexpr int ST = BM_R1F_STAGES;
+    constexpr unsigned TILE = RT * CT * sizeof(T);
+    constexpr unsigned STAGE = NIN * TILE;
+    extern __shared__ __align__(128) char smem[];
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + ST * STAGE);
+    unsigned long long* empty = full + ST;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const i64 row0 = (i64)blockIdx.x * RT;
+    const i64 ntiles = (cols + CT - 1) / CT;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < ST; ++s) {
+            lg_bar_init(&full[s], 1);
+            lg_bar_init(&empty[s], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < NIN; ++j) asm volatile("prefetch.tensormap [%0];" ::"l"(&P.m[j]) : "memory");
+    }
+    __syncthreads();
+    if (warp == 0) {
+        if (lane == 0) {
+            for (i64 t = 0; t < ntiles; ++t) {
+                const int s = (int)(t % ST);
+                if (t >= ST) lg_wait(&empty[s], (unsigned)(((t / ST) - 1) & 1));
+                lg_expect_tx(&full[s], STAGE);
+#pragma unroll
+                for (int j = 0; j < NIN; ++j)
+                    lg_tma_2d(smem + s * STAGE + j * TILE, &P.m[j], (int)row0, (int)(t * CT), &full[s]);
+            }
+        }
+        return;
+    }
+    const int r = (warp - 1) * 32 + lane;   // row within the slab
+    const bool active = r < RT && row0 + r < rows;
+    T acc = T(0);
+    MinMaxAcc<T, OP == 3> mm;
+    for (i64 t = 0; t < ntiles; ++t) {
+        const int s = (int)(t % ST);
+        lg_wait(&full[s], (unsigned)((t / ST) & 1));
+        const T* st = reinterpret_cast<const T*>(smem + s * STAGE);
+        i64 nc = cols - t * CT;
+        if (nc > CT) nc = CT;
+        if (active) {
+            for (int c = 0; c < nc; ++c) {
+                typename E::Pre pre;
+#pragma unroll
+                for (int j = 0; j < NIN; ++j) pre.x[j] = st[j * (TILE / sizeof(T)) + c * RT + r];
+                const T v = E::at(a, pre);
+                if constexpr (OP == 2 || OP == 3) mm.add(v);
+                else acc = OpPlus::f(acc, v);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) lg_arrive(&empty[s]);
+    }
+    if (!active) return;
+    T res;
+    if constexpr (OP == 5) res = OpDiv::f(acc, KScal<T>::f((double)cols, cols));
+    else if constexpr (OP == 2 || OP == 3) res = mm.result();
+    else res = acc;
+    out[row0 + r] = res;
+}
+
+}  // namespace bm

@@ -716,16 +716,30 @@ class _Lowerer:
         (the reference lowers the child first, expr.py:583-594).  Same values,
         same reduction order: the same bits."""
         k, child = node.kind, node.operands[0]
-        if not self.fuse or k not in _FUSED_RDIM or node.aux[0] != 0 or child.kind not in ELEMENTWISE_KINDS:
+        dim = node.aux[0]
+        if not self.fuse or k not in _FUSED_RDIM or child.kind not in ELEMENTWISE_KINDS:
             return None
         shp = shape_of(child)
         if shp.rows == 0 or shp.cols == 0:
             return None
         elem = child.elem_type
+        if dim == 1:
+            # TMA-staged row folds (bm_rdim0.cuh rdim1_fused_body): rows must make
+            # 16-B column strides, and numpy's lone-row block (rows % 64 == 1,
+            # kernels.py:89) sums pairwise, so it keeps the two-step plan
+            isz = NP_DTYPE[elem].itemsize
+            if (shp.rows * isz) % 16 or shp.rows % 64 == 1:
+                return None
+        mark = (len(self.steps), len(self.slots), len(self.absorbed))
         prog = self._fit_program(child, elem)
+        if dim == 1 and (len(prog.inputs) > 4 or any(self._ref_elem(r) != elem for r in prog.inputs)):
+            del self.steps[mark[0]:]
+            del self.slots[mark[1]:]
+            del self.absorbed[mark[2]:]
+            return None
         ref = self.emit("fused_rdim", prog.inputs, ["flat"] * len(prog.inputs), shape_of(node), elem, "flat",
                         params={"program": tuple(prog.stages), "compute_dtype": NP_DTYPE[elem].str,
-                                "op": _RDIM_KERNEL[k], "rows": shp.rows})
+                                "op": _RDIM_KERNEL[k], "rows": shp.rows, "cols": shp.cols, "dim": dim})
         if want != elem:
             ref = self.emit("mov_copy", [ref], ["flat"], shape_of(node), want, "flat")
         return ref

@@ -287,8 +287,9 @@ def build_invocation(inv: KernelInvocation) -> _clib.Invocation:
         elem = _NPSTR_TO_ELEM[np.dtype(p["compute_dtype"]).str]
         c.compute_dtype = _clib.DTYPE_CODE[elem]
         c.reduce_op = _RDIM_OP[p["op"]]
-        c.dim = 0
+        c.dim = int(p.get("dim", 0))
         c.iparams[0] = int(p["rows"])
+        c.iparams[1] = int(p.get("cols", 0))
         pb = _ProgramBuilder(c, elem)
         for st in p["program"]:
             pb.stage(st)

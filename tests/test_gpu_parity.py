@@ -15,6 +15,18 @@ from conftest import golden
 pytestmark = pytest.mark.gpu
 
 
+def same_nan(a, b):
+    """Bit-identical except that NaNs only have to be NaN on both sides: a NaN
+    produced by device arithmetic (0x7fffffff) and numpy's reductions (the
+    operand's payload on some paths, 0x7fc00000 on its SIMD paths) need not
+    share a payload."""
+    a, b = np.asarray(a), np.asarray(b)
+    assert a.dtype == b.dtype and a.shape == b.shape, (a.dtype, b.dtype, a.shape, b.shape)
+    na, nb = np.isnan(a), np.isnan(b)
+    assert np.array_equal(na, nb), "NaN positions differ"
+    same(np.where(na, 0, a).astype(a.dtype), np.where(nb, 0, b).astype(b.dtype))
+
+
 def same(a, b):
     a, b = np.asarray(a), np.asarray(b)
     assert a.dtype == b.dtype, (a.dtype, b.dtype)
@@ -276,6 +288,33 @@ def test_fused_dim0_reduction_of_a_tree(dm, dt, shape):
         mat = dm.evaluate(tree()).to_numpy()
         same(got, O.rdim(op, mat, 0))
     assert launches == [1, 1, 1, 1]
+
+
+@pytest.mark.parametrize("dt,shape", [(np.float32, (8192, 40)), (np.float64, (4096, 37)), (np.float32, (300, 1000)),
+                                      (np.float64, (1000, 33)), (np.int32, (2048, 9)), (np.float32, (130, 70)),
+                                      (np.float32, (64 * 5 + 1, 20)), (np.float32, (999, 17))])
+def test_fused_dim1_reduction_of_a_tree(dm, dt, shape):
+    """sum / mean / min / max(·, 1) of an element-wise tree: one TMA-staged
+    kernel where the rows allow it (16-B columns, no lone-row block), the
+    reference's two steps otherwise -- the bits of reducing the materialised
+    tree either way, NaNs included"""
+    rng = np.random.default_rng(shape[0] * 7 + shape[1])
+    if np.issubdtype(dt, np.integer):
+        a = rng.integers(-1000, 1000, size=shape).astype(dt)
+        b = rng.integers(-1000, 1000, size=shape).astype(dt)
+    else:
+        a = rng.standard_normal(shape).astype(dt)
+        b = rng.standard_normal(shape).astype(dt)
+        b[0, shape[1] // 2] = np.nan
+    A, B = dm.Matrix.from_numpy(a), dm.Matrix.from_numpy(b)
+    tree = lambda: 3 * A + B % A - 2
+    fusable = (shape[0] * a.itemsize) % 16 == 0 and shape[0] % 64 != 1
+    for op in ("sum", "mean", "min", "max"):
+        kernels = [s.kernel for s in dm.plan(getattr(dm, op)(tree(), 1)).steps]
+        assert (kernels == ["fused_rdim"]) == fusable, kernels
+        got = dm.evaluate(getattr(dm, op)(tree(), 1)).to_numpy()
+        mat = dm.evaluate(tree()).to_numpy()
+        (same_nan if np.issubdtype(dt, np.floating) else same)(got, O.rdim(op, mat, 1))
 
 
 # ---- GEMM ----------------------------------------------------------------------------------------

@@ -299,21 +299,29 @@ def test_dim0_reduction_of_a_tree_is_one_fused_step():
         assert st.params["op"] == kern and st.params["rows"] == 512
         assert st.params["program"] == (("load", 0), ("scalar", "eop_scalar_times", 2), ("load", 1),
                                         ("glue", "eglue_plus"))
-    # a leaf, dim 1, var/stddev and empty shapes keep the reference's lowering
+    # dim 1 too, with TMA-compatible rows; a leaf, numpy's lone-row block, var/stddev and
+    # empty shapes keep the reference's lowering
+    p1 = dm.plan(dm.sum(2 * a + b, 1))
+    assert [s.kernel for s in p1.steps] == ["fused_rdim"] and p1.steps[0].params["dim"] == 1
+    assert p1.steps[0].params["cols"] == 40
     assert [s.kernel for s in dm.plan(dm.sum(a, 0)).steps] == ["rdim_sum"]
-    assert [s.kernel for s in dm.plan(dm.sum(2 * a + b, 1)).steps] == ["fused_chain", "rdim_sum"]
+    lone = leaf(65, 8)
+    assert [s.kernel for s in dm.plan(dm.sum(2 * lone + 1, 1)).steps] == ["fused_chain", "rdim_sum"]
+    odd = leaf(6, 8)                                            # 24-B columns: no TMA
+    assert [s.kernel for s in dm.plan(dm.sum(2 * odd + 1, 1)).steps] == ["fused_chain", "rdim_sum"]
     assert [s.kernel for s in dm.plan(dm.var(2 * a + b, 0)).steps] == ["fused_chain", "rdim_var"]
     assert [s.kernel for s in dm.plan(dm.sum(2 * leaf(0, 5) + 1, 0)).steps] != ["fused_rdim"]
 
 
-def test_fused_dim0_kernels_compile():
+@pytest.mark.parametrize("dim", [0, 1])
+def test_fused_dim_kernels_compile(dim):
     for elem in ("f32", "f64", "i32"):
         a, b = leaf(512, 40, elem), leaf(512, 40, elem)
         for op in ("sum", "mean", "min", "max"):
-            p = dm.plan(getattr(dm, op)(a * b + 3, 0))
+            p = dm.plan(getattr(dm, op)(a * b + 3, dim))
             st = p.steps[0]
             views = [expr._make_view(r[1].mem, 512, 40, "flat") for r in st.inputs]
-            out = FakeMatrix(1, 40, elem)
+            out = FakeMatrix(1, 40, elem) if dim == 0 else FakeMatrix(512, 1, elem)
             inv = build_invocation(KernelInvocation("fused_rdim", tuple(views), _flat(out), (), st.params))
             rc = _clib.lib().bm_jit_compile_only(ctypes.byref(inv))
             assert rc == 0, _clib.last_error()

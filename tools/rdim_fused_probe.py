@@ -1,4 +1,4 @@
-"""Time sum/mean/min/max(2*A + B, 0) on 16384^2 f64: fused (one kernel over A
+"""Time sum/mean/min/max(2*A + B, dim) on 16384^2 f64: fused (one kernel over A
 and B) against the reference's plan (materialise 2*A + B, then reduce)."""
 import pathlib
 import sys
@@ -29,12 +29,13 @@ def main():
             best = min(best, s.elapsed_time(e))
         return best
 
-    for op in ("sum", "mean", "min", "max"):
-        f = getattr(dm, op)
-        fused = timeit(lambda: dm.evaluate(f(2 * A + B, 0)))
-        unfused = timeit(lambda: dm.evaluate(f(dm.evaluate(2 * A + B), 0)))
-        print(f"{op}(2*A + B, 0): fused {fused:.3f} ms ({16 * n * n / fused / 1e6:.0f} GB/s of inputs), "
-              f"materialise + reduce {unfused:.3f} ms", flush=True)
+    for dim in (0, 1):
+        for op in ("sum", "mean", "min", "max"):
+            f = getattr(dm, op)
+            fused = timeit(lambda: dm.evaluate(f(2 * A + B, dim)))
+            unfused = timeit(lambda: dm.evaluate(f(dm.evaluate(2 * A + B), dim)))
+            print(f"{op}(2*A + B, {dim}): fused {fused:.3f} ms ({16 * n * n / fused / 1e6:.0f} GB/s of inputs), "
+                  f"materialise + reduce {unfused:.3f} ms", flush=True)
     dm.shutdown()
 
 

@@ -89,7 +89,7 @@ extern "C" {
                                     (expr.py:583-594 materialises it first): inputs = the program's
                                     flat inputs of rows * cols elements (column-major); dim = 0 / 1;
                                     iparams[0] = rows, iparams[1] = cols (dim 1); reduce_op =
-                                    BM_R_ACCU / MIN / MAX / MEAN; output = cols (dim 0) or rows
+                                    BM_R_ACCU / MIN / MAX / MEAN / VAR; output = cols (dim 0) or rows
                                     (dim 1) values of the compute dtype.  dim 1 takes 1-4 inputs of
                                     the compute dtype, 16-B aligned, rows * size % 16 == 0 (TMA)   */
 

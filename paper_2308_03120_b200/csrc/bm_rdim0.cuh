@@ -133,6 +133,25 @@ __device__ __forceinline__ void rdim0_col_body(const S& s, i64 rows, i64 cols, i
             }
             r = sum;
             if constexpr (OP == 5) r = OpDiv::f(sum, KScal<T>::f((double)rows, rows));
+        } else if constexpr (OP == 6) {
+            // unbiased variance, two passes in f64 (kernels.py:519-527)
+            if (rows < 2) {
+                r = T(0);
+            } else {
+                double s1 = 0;
+                for (i64 i = lane; i < rows; i += 32) s1 += cvt<double>(s.at(c0 + i));
+#pragma unroll
+                for (int m = 16; m >= 1; m >>= 1) s1 += warp_shfl_xor(s1, m);
+                const double mean = s1 / (double)rows;
+                double s2 = 0;
+                for (i64 i = lane; i < rows; i += 32) {
+                    const double d = cvt<double>(s.at(c0 + i)) - mean;
+                    s2 += d * d;
+                }
+#pragma unroll
+                for (int m = 16; m >= 1; m >>= 1) s2 += warp_shfl_xor(s2, m);
+                r = cvt<T>(s2 / (double)(rows - 1));
+            }
         } else {
             constexpr int V = 16 / sizeof(T);
             MinMaxAcc<T, OP == 3> acc;
@@ -197,6 +216,7 @@ __device__ __forceinline__ void rdim1_fused_body(const R1Args& P) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const i64 row0 = (i64)blockIdx.x * RT;
     const i64 ntiles = (cols + CT - 1) / CT;
+    constexpr int PASSES = OP == 6 ? 2 : 1;    // var: mean, then squared deviations
     if (threadIdx.x == 0) {
         for (int s = 0; s < ST; ++s) {
             lg_bar_init(&full[s], 1);
@@ -209,13 +229,13 @@ __device__ __forceinline__ void rdim1_fused_body(const R1Args& P) {
     __syncthreads();
     if (warp == 0) {
         if (lane == 0) {
-            for (i64 t = 0; t < ntiles; ++t) {
+            for (i64 t = 0; t < PASSES * ntiles; ++t) {
                 const int s = (int)(t % ST);
                 if (t >= ST) lg_wait(&empty[s], (unsigned)(((t / ST) - 1) & 1));
                 lg_expect_tx(&full[s], STAGE);
 #pragma unroll
                 for (int j = 0; j < NIN; ++j)
-                    lg_tma_2d(smem + s * STAGE + j * TILE, &P.m[j], (int)row0, (int)(t * CT), &full[s]);
+                    lg_tma_2d(smem + s * STAGE + j * TILE, &P.m[j], (int)row0, (int)((t % ntiles) * CT), &full[s]);
             }
         }
         return;
@@ -224,11 +244,13 @@ __device__ __forceinline__ void rdim1_fused_body(const R1Args& P) {
     const bool active = r < RT && row0 + r < rows;
     T acc = T(0);
     MinMaxAcc<T, OP == 3> mm;
-    for (i64 t = 0; t < ntiles; ++t) {
+    double dacc = 0.0, mean = 0.0;
+    for (i64 t = 0; t < PASSES * ntiles; ++t) {
         const int s = (int)(t % ST);
         lg_wait(&full[s], (unsigned)((t / ST) & 1));
         const T* st = reinterpret_cast<const T*>(smem + s * STAGE);
-        i64 nc = cols - t * CT;
+        const i64 tc = t % ntiles;
+        i64 nc = cols - tc * CT;
         if (nc > CT) nc = CT;
         if (active) {
             for (int c = 0; c < nc; ++c) {
@@ -236,16 +258,33 @@ __device__ __forceinline__ void rdim1_fused_body(const R1Args& P) {
 #pragma unroll
                 for (int j = 0; j < NIN; ++j) pre.x[j] = st[j * (TILE / sizeof(T)) + c * RT + r];
                 const T v = E::at(a, pre);
-                if constexpr (OP == 2 || OP == 3) mm.add(v);
-                else acc = OpPlus::f(acc, v);
+                if constexpr (OP == 2 || OP == 3) {
+                    mm.add(v);
+                } else if constexpr (OP == 6) {
+                    if (t < ntiles) {
+                        dacc += cvt<double>(v);
+                    } else {
+                        const double d = cvt<double>(v) - mean;
+                        dacc += d * d;
+                    }
+                } else {
+                    acc = OpPlus::f(acc, v);
+                }
             }
         }
         __syncwarp();
         if (lane == 0) lg_arrive(&empty[s]);
+        if constexpr (OP == 6) {
+            if (t == ntiles - 1) {
+                mean = dacc / (double)cols;
+                dacc = 0.0;
+            }
+        }
     }
     if (!active) return;
     T res;
     if constexpr (OP == 5) res = OpDiv::f(acc, KScal<T>::f((double)cols, cols));
+    else if constexpr (OP == 6) res = (cols < 2) ? T(0) : cvt<T>(dacc / (double)(cols - 1));
     else if constexpr (OP == 2 || OP == 3) res = mm.result();
     else res = acc;
     out[row0 + r] = res;

@@ -395,7 +395,7 @@ class EvalPlan:
 _GEN_KERNEL = {"gen_zeros": "gen_fill_const", "gen_ones": "gen_fill_const", "gen_fill": "gen_fill_const",
                "gen_eye": "gen_eye", "gen_linspace": "gen_linspace", "gen_randu": "gen_randu",
                "gen_randn": "gen_randn"}
-_FUSED_RDIM = frozenset({"op_sum_dim", "op_mean_dim", "op_min_dim", "op_max_dim"})
+_FUSED_RDIM = frozenset({"op_sum_dim", "op_mean_dim", "op_min_dim", "op_max_dim", "op_var_dim", "op_stddev_dim"})
 _RDIM_KERNEL = {"op_sum_dim": "rdim_sum", "op_min_dim": "rdim_min", "op_max_dim": "rdim_max",
                 "op_mean_dim": "rdim_mean", "op_var_dim": "rdim_var", "op_stddev_dim": "rdim_var"}
 
@@ -740,6 +740,8 @@ class _Lowerer:
         ref = self.emit("fused_rdim", prog.inputs, ["flat"] * len(prog.inputs), shape_of(node), elem, "flat",
                         params={"program": tuple(prog.stages), "compute_dtype": NP_DTYPE[elem].str,
                                 "op": _RDIM_KERNEL[k], "rows": shp.rows, "cols": shp.cols, "dim": dim})
+        if k == "op_stddev_dim":
+            ref = self.emit("eop_sqrt", [ref], ["flat"], shape_of(node), elem, "flat")
         if want != elem:
             ref = self.emit("mov_copy", [ref], ["flat"], shape_of(node), want, "flat")
         return ref

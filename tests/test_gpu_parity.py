@@ -288,6 +288,19 @@ def test_fused_dim0_reduction_of_a_tree(dm, dt, shape):
         mat = dm.evaluate(tree()).to_numpy()
         same(got, O.rdim(op, mat, 0))
     assert launches == [1, 1, 1, 1]
+    if np.issubdtype(dt, np.floating):
+        mat = dm.evaluate(tree()).to_numpy()
+        tol = 1e-5 if dt == np.float32 else 1e-12
+        for op in ("var", "stddev"):
+            assert [s.kernel for s in dm.plan(getattr(dm, op)(tree(), 0)).steps][0] == "fused_rdim"
+            got = dm.evaluate(getattr(dm, op)(tree(), 0)).to_numpy().astype(np.float64)
+            want = O.rdim("var", mat, 0).astype(np.float64)
+            if op == "stddev":
+                want = np.sqrt(want)
+            ok = np.isnan(want) == np.isnan(got)
+            assert ok.all()
+            m = ~np.isnan(want)
+            np.testing.assert_allclose(got[m], want[m], rtol=tol, atol=tol)
 
 
 @pytest.mark.parametrize("dt,shape", [(np.float32, (8192, 40)), (np.float64, (4096, 37)), (np.float32, (300, 1000)),
@@ -315,6 +328,14 @@ def test_fused_dim1_reduction_of_a_tree(dm, dt, shape):
         got = dm.evaluate(getattr(dm, op)(tree(), 1)).to_numpy()
         mat = dm.evaluate(tree()).to_numpy()
         (same_nan if np.issubdtype(dt, np.floating) else same)(got, O.rdim(op, mat, 1))
+    if np.issubdtype(dt, np.floating):
+        mat = dm.evaluate(tree()).to_numpy()
+        tol = 1e-5 if dt == np.float32 else 1e-12
+        got = dm.evaluate(dm.var(tree(), 1)).to_numpy().astype(np.float64)
+        want = O.rdim("var", mat, 1).astype(np.float64)
+        assert (np.isnan(want) == np.isnan(got)).all()
+        m = ~np.isnan(want)
+        np.testing.assert_allclose(got[m], want[m], rtol=tol, atol=tol)
 
 
 # ---- GEMM ----------------------------------------------------------------------------------------

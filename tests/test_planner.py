@@ -309,7 +309,8 @@ def test_dim0_reduction_of_a_tree_is_one_fused_step():
     assert [s.kernel for s in dm.plan(dm.sum(2 * lone + 1, 1)).steps] == ["fused_chain", "rdim_sum"]
     odd = leaf(6, 8)                                            # 24-B columns: no TMA
     assert [s.kernel for s in dm.plan(dm.sum(2 * odd + 1, 1)).steps] == ["fused_chain", "rdim_sum"]
-    assert [s.kernel for s in dm.plan(dm.var(2 * a + b, 0)).steps] == ["fused_chain", "rdim_var"]
+    assert [s.kernel for s in dm.plan(dm.var(2 * a + b, 0)).steps] == ["fused_rdim"]
+    assert [s.kernel for s in dm.plan(dm.stddev(2 * a + b, 1)).steps] == ["fused_rdim", "eop_sqrt"]
     assert [s.kernel for s in dm.plan(dm.sum(2 * leaf(0, 5) + 1, 0)).steps] != ["fused_rdim"]
 
 
@@ -317,7 +318,7 @@ def test_dim0_reduction_of_a_tree_is_one_fused_step():
 def test_fused_dim_kernels_compile(dim):
     for elem in ("f32", "f64", "i32"):
         a, b = leaf(512, 40, elem), leaf(512, 40, elem)
-        for op in ("sum", "mean", "min", "max"):
+        for op in ("sum", "mean", "min", "max", "var"):
             p = dm.plan(getattr(dm, op)(a * b + 3, dim))
             st = p.steps[0]
             views = [expr._make_view(r[1].mem, 512, 40, "flat") for r in st.inputs]

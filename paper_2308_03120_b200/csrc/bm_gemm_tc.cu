@@ -30,12 +30,19 @@ struct PlainSrc {
     const float* src;
     i64 ld;
     __device__ __forceinline__ float at(i64 idx) const { return src[idx]; }
+    template <int V> __device__ __forceinline__ void vec(i64 idx, float (&v)[V]) const {
+        const float4 q = __ldg(reinterpret_cast<const float4*>(src + idx));
+        v[0] = q.x;
+        v[1] = q.y;
+        v[2] = q.z;
+        v[3] = q.w;
+    }
 };
-template <bool SRC_KMAJOR>
+template <bool SRC_KMAJOR, bool VEC>
 __global__ void __launch_bounds__(256) split_tf32_kernel(const float* __restrict__ src, i64 ld, i64 rows, i64 k,
                                                          float* __restrict__ hi, float* __restrict__ lo, i64 kp,
                                                          i64 rp) {
-    split_tf32_body<SRC_KMAJOR>(PlainSrc{src, ld}, ld, rows, k, hi, lo, kp, rp);
+    split_tf32_body<SRC_KMAJOR, VEC>(PlainSrc{src, ld}, ld, rows, k, hi, lo, kp, rp);
 }
 
 // ---------------------------------------------------------------------------
@@ -641,11 +648,15 @@ static int encode_kmajor(CUtensorMap* tm, const float* p, int64_t kp, int64_t ro
 
 static int split_operand(const float* src, int64_t ld, bool kmajor, int64_t rows, int64_t k, float* hi, float* lo,
                          int64_t kp, int64_t rp) {
-    dim3 grid((unsigned)(kp / 32), (unsigned)(rp / 32));
-    if (kmajor)
-        bm::split_tf32_kernel<true><<<grid, dim3(32, 8), 0, st().stream>>>(src, ld, rows, k, hi, lo, kp, rp);
-    else
-        bm::split_tf32_kernel<false><<<grid, dim3(32, 8), 0, st().stream>>>(src, ld, rows, k, hi, lo, kp, rp);
+    dim3 grid((unsigned)((kp + 63) / 64), (unsigned)((rp + 63) / 64));
+    const bool vec = (ld % 4 == 0) && (((uintptr_t)src & 15u) == 0);
+    if (kmajor) {
+        if (vec) bm::split_tf32_kernel<true, true><<<grid, dim3(32, 8), 0, st().stream>>>(src, ld, rows, k, hi, lo, kp, rp);
+        else bm::split_tf32_kernel<true, false><<<grid, dim3(32, 8), 0, st().stream>>>(src, ld, rows, k, hi, lo, kp, rp);
+    } else {
+        if (vec) bm::split_tf32_kernel<false, true><<<grid, dim3(32, 8), 0, st().stream>>>(src, ld, rows, k, hi, lo, kp, rp);
+        else bm::split_tf32_kernel<false, false><<<grid, dim3(32, 8), 0, st().stream>>>(src, ld, rows, k, hi, lo, kp, rp);
+    }
     BM_CUDA(cudaGetLastError());
     st().launches++;
     return BM_OK;

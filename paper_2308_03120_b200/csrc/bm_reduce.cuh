@@ -793,35 +793,76 @@ __device__ __forceinline__ float tf32_rna(float x) {
     return __uint_as_float(r);
 }
 
-template <bool SRC_KMAJOR, class SRC>
+template <bool SRC_KMAJOR, bool VEC, class SRC>
 __device__ __forceinline__ void split_tf32_body(const SRC& src, i64 ld, i64 rows, i64 k, float* __restrict__ hi,
                                                 float* __restrict__ lo, i64 kp, i64 rp) {
-    __shared__ float tile[32][33];
-    const i64 r0 = (i64)blockIdx.y * 32, c0 = (i64)blockIdx.x * 32;
-    if (SRC_KMAJOR) {
-        for (int j = threadIdx.y; j < 32; j += blockDim.y) {
-            const i64 r = r0 + j, c = c0 + threadIdx.x;
-            float v = 0.f;
-            if (r < rows && c < k) v = src.at(c + r * ld);
-            tile[j][threadIdx.x] = v;
-        }
-    } else {
-        // read with threadIdx.x along r (contiguous), park transposed
-        for (int j = threadIdx.y; j < 32; j += blockDim.y) {
-            const i64 r = r0 + threadIdx.x, c = c0 + j;
-            float v = 0.f;
-            if (r < rows && c < k) v = src.at(r + c * ld);
-            tile[threadIdx.x][j] = v;
+    // 64 (r) x 64 (c) tile per 256-thread CTA, moved as float4 along the
+    // source's contiguous dimension and written as float4 along K (kp is a
+    // multiple of 32, so a quad that starts inside [0, kp) ends inside it)
+    __shared__ float tile[64][65];   // [r][c]
+    const i64 r0 = (i64)blockIdx.y * 64, c0 = (i64)blockIdx.x * 64;
+    const int t = threadIdx.x + threadIdx.y * blockDim.x;
+#pragma unroll
+    for (int q = t; q < 1024; q += 256) {
+        if (SRC_KMAJOR) {                              // X[c + r * ld]: contiguous along c
+            const int rr = q >> 4, cc = (q & 15) * 4;
+            const i64 r = r0 + rr, c = c0 + cc;
+            float v[4] = {0.f, 0.f, 0.f, 0.f};
+            if (r < rows) {
+                bool done = false;
+                if constexpr (VEC) {
+                    if (c + 3 < k) {
+                        src.template vec<4>(c + r * ld, v);
+                        done = true;
+                    }
+                }
+                if (!done) {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        if (c + e < k) v[e] = src.at(c + e + r * ld);
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) tile[rr][cc + e] = v[e];
+        } else {                                       // X[r + c * ld]: contiguous along r
+            const int cc = q >> 4, rr = (q & 15) * 4;
+            const i64 r = r0 + rr, c = c0 + cc;
+            float v[4] = {0.f, 0.f, 0.f, 0.f};
+            if (c < k) {
+                bool done = false;
+                if constexpr (VEC) {
+                    if (r + 3 < rows) {
+                        src.template vec<4>(r + c * ld, v);
+                        done = true;
+                    }
+                }
+                if (!done) {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        if (r + e < rows) v[e] = src.at(r + e + c * ld);
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) tile[rr + e][cc] = v[e];
         }
     }
     __syncthreads();
-    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
-        const i64 r = r0 + j, c = c0 + threadIdx.x;
+#pragma unroll
+    for (int q = t; q < 1024; q += 256) {
+        const int rr = q >> 4, cc = (q & 15) * 4;
+        const i64 r = r0 + rr, c = c0 + cc;
         if (r < rp && c < kp) {
-            const float x = tile[j][threadIdx.x];
-            const float h = tf32_rna(x);
-            hi[r * kp + c] = h;
-            lo[r * kp + c] = tf32_rna(x - h);
+            float4 h, l;
+            float* hp = &h.x;
+            float* lp = &l.x;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float x = tile[rr][cc + e];
+                hp[e] = tf32_rna(x);
+                lp[e] = tf32_rna(x - hp[e]);
+            }
+            *reinterpret_cast<float4*>(hi + r * kp + c) = h;
+            *reinterpret_cast<float4*>(lo + r * kp + c) = l;
         }
     }
 }

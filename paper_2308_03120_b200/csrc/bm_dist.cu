@@ -59,7 +59,8 @@ static int fold_typed(const void* parts, int64_t nitems, int64_t nfull, bool uni
     bm::fold_chunks_kernel<P, OP, UPB><<<nchunks, 512, smem, st().stream>>>(
         (const P*)parts, nitems, nfull, unit_mode ? 1 : 0, chunk, (P*)scratch);
     BM_CUDA(cudaGetLastError());
-    bm::fold_final_kernel<P, OP, NORM><<<1, 32, 0, st().stream>>>((const P*)scratch, nchunks, (P*)result);
+    bm::fold_final_kernel<P, OP, NORM><<<1, 256, (nchunks + nchunks / 256 + 1) * (int)sizeof(P), st().stream>>>(
+        (const P*)scratch, nchunks, (P*)result);
     BM_CUDA(cudaGetLastError());
     st().launches += 2;
     return BM_OK;

@@ -47,8 +47,7 @@ static int combine_typed(const void* parts, int64_t count, int op, void* out) {
 template <typename P, int OP, int UPB, bool NORM>
 static int fold_typed(const void* parts, int64_t nitems, int64_t nfull, bool unit_mode, int chunk, int nchunks,
                       void* result) {
-    static void* scratch = nullptr;
-    if (!scratch) BM_CUDA(cudaMalloc(&scratch, 8 * 8192));
+    void* scratch = st().fold_scratch;   // per initialised device (bm_init / bm_shutdown)
     const int smem = 2 * chunk * (int)sizeof(P);
     static bool attr = false;
     if (!attr) {

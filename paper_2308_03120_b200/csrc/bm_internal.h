@@ -25,6 +25,7 @@ struct State {
     // dependent launch) never touches the predecessor's partials or ticket
     void* partials[2] = {nullptr, nullptr};
     int64_t partials_cap = 0;          // capacity of each, in 8-byte entries
+    void* fold_scratch = nullptr;      // chunk results of the separate fold kernels (8192 x 8 B)
     int flip = 0;                      // buffer of the next reduction
     unsigned int* ticket = nullptr;    // two last-CTA counters (at +0 and +32), zero between launches
     void* result = nullptr;            // device slot of the final value

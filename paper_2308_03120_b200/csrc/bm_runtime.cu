@@ -119,6 +119,7 @@ int bm_init(int device) {
     BM_CUDA(cudaMalloc(&s.ticket, 256));
     BM_CUDA(cudaMemset(s.ticket, 0, 256));
     BM_CUDA(cudaMalloc(&s.result, 256));
+    BM_CUDA(cudaMalloc(&s.fold_scratch, 8 * 8192));
     BM_CUDA(cudaMallocHost(&s.host_slot, 256));
     BM_CUDA(cudaDeviceSynchronize());
     s.initialised = true;
@@ -134,6 +135,8 @@ int bm_shutdown(void) {
     cudaFree(s.partials[1]);
     cudaFree(s.ticket);
     cudaFree(s.result);
+    cudaFree(s.fold_scratch);
+    s.fold_scratch = nullptr;
     cudaFreeHost(s.host_slot);
     cudaStreamDestroy(s.own_stream);
     s.partials[0] = s.partials[1] = s.result = s.host_slot = nullptr;

@@ -557,7 +557,9 @@ class _Lowerer:
                 return n.elem_type == "f32" and s_.rows == m and s_.cols == 1
             return False
 
-        if not scan(b) or not found:
+        ok = scan(b)
+        scan = None  # noqa: F841  (break the closure's self-reference, as for walk below)
+        if not ok or not found:
             return None
         gnode = found[0]
         w = gnode.operands[1]

@@ -208,6 +208,15 @@ def test_planning_leaves_no_reference_cycles():
         g = leaf(64, 64) @ leaf(64, 64).t()
         p = expr.plan(g)
         del p, g
+        # the fused paths' pattern matchers (logistic step, GEMM prologue, dim reductions)
+        X, w, y = leaf(4096, 1024), leaf(1024, 1), leaf(4096, 1)
+        r = 1 / (1 + dm.exp(0 - X @ w)) - y
+        p = expr.plan(X.t() @ r)
+        del p, r, X, w, y
+        a, b = leaf(256, 256), leaf(256, 256)
+        p = expr.plan((2 * a + 1) @ (b - 3).t())
+        q = expr.plan(dm.sum(2 * a + b, 1))
+        del p, q, a, b
         assert gc.collect() == 0, [type(o).__name__ for o in gc.garbage][:20]
     finally:
         gc.set_debug(0)

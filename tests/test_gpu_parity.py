@@ -305,7 +305,8 @@ def test_fused_dim0_reduction_of_a_tree(dm, dt, shape):
 
 @pytest.mark.parametrize("dt,shape", [(np.float32, (8192, 40)), (np.float64, (4096, 37)), (np.float32, (300, 1000)),
                                       (np.float64, (1000, 33)), (np.int32, (2048, 9)), (np.float32, (130, 70)),
-                                      (np.float32, (64 * 5 + 1, 20)), (np.float32, (999, 17))])
+                                      (np.float32, (64 * 5 + 1, 20)), (np.float32, (999, 17)), (np.float32, (4, 3)),
+                                      (np.float32, (16, 5)), (np.float64, (8, 1000))])
 def test_fused_dim1_reduction_of_a_tree(dm, dt, shape):
     """sum / mean / min / max(·, 1) of an element-wise tree: one TMA-staged
     kernel where the rows allow it (16-B columns, no lone-row block), the

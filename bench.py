@@ -214,6 +214,27 @@ def _event_time_ms(torch, fn, steps: int) -> float:
     return start.elapsed_time(end)
 
 
+def torch_reference(torch, host) -> dict:
+    """The same workload in PyTorch eager on the same GPU (timing context
+    only: torch's summation order differs from the reference's), and
+    torch.sum over one 1 GiB f32 tensor as a library read-bandwidth figure."""
+    A, B, C, D = (torch.from_numpy(x).cuda() for x in host)
+
+    def cfg1():
+        return (2 * A + B * C - torch.exp(D)).sum()
+
+    big = torch.rand(1 << 28, device="cuda")
+    out = {}
+    for name, fn, nbytes in (("eager_cfg1", cfg1, BYTES_PER_STEP), ("sum_1GiB", lambda: big.sum(), 4 << 28)):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        best = min(_event_time_ms(torch, fn, 10) / 10 for _ in range(3))
+        out[name] = {"ms": best, "GB/s": nbytes / best / 1e6}
+    out["note"] = "torch eager: 4 element-wise kernels with temporaries + a sum; not bit-compatible"
+    return out
+
+
 def secondary_suite(dm, torch) -> dict:
     """The other SURVEY 8d configs on this GPU (inputs generated on device by
     the counter RNG; timings with CUDA events, best of a few)."""
@@ -406,6 +427,7 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
     cpu = None
     if rank == 0 and world == 1 and not args.no_secondary:
         secondary = secondary_suite(dm, torch)
+        secondary["torch_reference"] = torch_reference(torch, host)
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_reference_run(host, args.cpu_seconds, None, 1)
 

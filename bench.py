@@ -231,7 +231,24 @@ def torch_reference(torch, host) -> dict:
         torch.cuda.synchronize()
         best = min(_event_time_ms(torch, fn, 10) / 10 for _ in range(3))
         out[name] = {"ms": best, "GB/s": nbytes / best / 1e6}
-    out["note"] = "torch eager: 4 element-wise kernels with temporaries + a sum; not bit-compatible"
+    del big
+    # cuBLAS through torch at 8192^3: full-precision SGEMM (no TF32) and DGEMM, A @ B.T
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        for name, dt in (("cublas_sgemm_nt_8192", torch.float32), ("cublas_dgemm_nt_8192", torch.float64)):
+            a = torch.rand(8192, 8192, device="cuda", dtype=dt)
+            b = torch.rand(8192, 8192, device="cuda", dtype=dt)
+            fn = lambda: a @ b.t()
+            fn()
+            torch.cuda.synchronize()
+            best = min(_event_time_ms(torch, fn, 1) for _ in range(3))
+            out[name] = {"ms": best, "TFLOP/s": 2 * 8192 ** 3 / best / 1e9}
+            del a, b
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    out["note"] = ("torch eager: 4 element-wise kernels with temporaries + a sum; not bit-compatible. "
+                   "cuBLAS SGEMM/DGEMM: the library rates the 3xTF32 / DMMA GEMMs stand beside")
     return out
 
 

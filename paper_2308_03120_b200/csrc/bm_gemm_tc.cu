@@ -522,6 +522,10 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool vali
                  : "memory");
 }
 
+__device__ __forceinline__ void cp_async16_all(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
 // VEC: the M-contiguous A (not TA) and N-contiguous B (TB) tiles move as
 // 16-byte pairs (host checks even m / n / ld and 16-byte bases), halving the
 // LDGSTS count per stage.
@@ -545,9 +549,50 @@ __global__ void __launch_bounds__(DmCfg<BM, BK, ST>::NW * 32, BM == 64 ? 2 : 1)
 #pragma unroll
         for (int j = 0; j < G::NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
+    // interior tiles (the tile and the K block inside the matrices) skip the
+    // per-copy bounds tests: fewer integer instructions competing with the
+    // DMMAs for issue slots
+    const bool full_mn = (m0 + BM <= m) && (n0 + DM_BN <= n);
     auto load = [&](int st, i64 k0) {
         double* as = As + st * BK * G::LDA;
         double* bs = Bs + st * BK * G::LDB;
+        if (full_mn && k0 + BK <= k) {
+            if (VA) {
+#pragma unroll
+                for (int t = 0; t < (BK * BM / 2) / NT; ++t) {
+                    const int idx = threadIdx.x + t * NT;
+                    const int kk = idx / (BM / 2), mm = 2 * (idx % (BM / 2));
+                    cp_async16_all(as + kk * G::LDA + mm, A + (m0 + mm) + (k0 + kk) * lda);
+                }
+            } else {
+#pragma unroll
+                for (int t = 0; t < (BK * BM) / NT; ++t) {
+                    const int idx = threadIdx.x + t * NT;
+                    int kk, mm;
+                    if (TA) { mm = idx / BK; kk = idx % BK; } else { kk = idx / BM; mm = idx % BM; }
+                    const double* src = TA ? A + (k0 + kk) + (m0 + mm) * lda : A + (m0 + mm) + (k0 + kk) * lda;
+                    cp_async8(as + kk * G::LDA + mm, src, true);
+                }
+            }
+            if (VB) {
+#pragma unroll
+                for (int t = 0; t < (BK * DM_BN / 2) / NT; ++t) {
+                    const int idx = threadIdx.x + t * NT;
+                    const int kk = idx / (DM_BN / 2), nn = 2 * (idx % (DM_BN / 2));
+                    cp_async16_all(bs + kk * G::LDB + nn, B + (n0 + nn) + (k0 + kk) * ldb);
+                }
+            } else {
+#pragma unroll
+                for (int t = 0; t < (BK * DM_BN) / NT; ++t) {
+                    const int idx = threadIdx.x + t * NT;
+                    int kk, nn;
+                    if (TB) { kk = idx / DM_BN; nn = idx % DM_BN; } else { nn = idx / BK; kk = idx % BK; }
+                    const double* src = TB ? B + (n0 + nn) + (k0 + kk) * ldb : B + (k0 + kk) + (n0 + nn) * ldb;
+                    cp_async8(bs + kk * G::LDB + nn, src, true);
+                }
+            }
+            return;
+        }
         if (VA) {
 #pragma unroll
             for (int t = 0; t < (BK * BM / 2) / NT; ++t) {

@@ -628,7 +628,8 @@ def test_fused_logistic_step_vs_reference(dm):
     np.testing.assert_allclose(dm.evaluate(X.t() @ r_e).to_numpy(), g["lr_g"], rtol=1e-4, atol=1e-5)
 
 
-@pytest.mark.parametrize("m,k", [(1 << 16, 1024), (4100, 300), (4096 * 3 + 16, 1000)])
+@pytest.mark.parametrize("m,k", [(1 << 16, 1024), (4100, 300), (4096 * 3 + 16, 1000), (16, 16), (1024, 513),
+                                 (2052, 1)])
 def test_fused_logistic_step_large(dm, m, k):
     rng = np.random.default_rng(m + k)
     X = rng.standard_normal((m, k), dtype=np.float32)

@@ -245,6 +245,22 @@ int bm_combine_partials(const void* dev_partials, int64_t count, int32_t dtype,
 /* same fold, result left on the device (no host synchronisation) */
 int bm_combine_partials_to_device(const void* dev_partials, int64_t count, int32_t dtype,
                                   int32_t reduce_op, void* dev_result);
+/* ---- peer-memory exchange of the shard partials (replaces the NCCL all-gather of
+ * ShardedReduction with one kernel over NVLink; one process per GPU) ----
+ * bm_exchange_alloc: an exchange buffer of 2 parities x (world values + world flags)
+ * 8-byte slots, zeroed, from cudaMalloc (IPC-exportable); its 64-byte IPC handle goes
+ * to every peer (torch.distributed object all-gather), which maps it with
+ * bm_exchange_open.  bm_exchange_combine (one kernel): writes this rank's partial into
+ * slot `rank` of every rank's buffer (parity epoch & 1), publishes `epoch` in its flag
+ * with release semantics at system scope, waits until every rank's flag in the local
+ * buffer reaches `epoch`, then folds the world values in rank order like
+ * bm_combine_partials_to_device into dev_result. */
+int bm_exchange_alloc(int32_t world, void** dev_buffer, void* ipc_handle /* 64 bytes out */);
+int bm_exchange_open(const void* ipc_handle, void** dev_buffer);
+int bm_exchange_close(void* dev_buffer, int32_t opened /* 1: mapped peer buffer, 0: own */);
+int bm_exchange_combine(const void* dev_partial, void* const* peer_buffers /* host array, world entries */,
+                        int32_t world, int32_t rank, uint64_t epoch, int32_t dtype, int32_t reduce_op,
+                        void* dev_result);
 int bm_sync(void);
 
 /* ---- instrumentation -------------------------------------------------------------- */

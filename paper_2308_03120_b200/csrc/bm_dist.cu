@@ -4,6 +4,7 @@
 // folded here with combine_pairwise (kernels.py:380-392).  When every shard
 // holds an aligned power-of-two run of REDUCE_BLOCK blocks this reproduces the
 // single-device result bit for bit ("reduction order").
+#include <cstring>
 #include <type_traits>
 
 #include "bm_internal.h"
@@ -11,12 +12,51 @@
 
 namespace bm {
 
+struct PeerPtrs {
+    void* p[64];
+};
+
 template <typename A, int OP>
 __global__ void __launch_bounds__(256) combine_kernel(const A* __restrict__ parts, int count, A* out, int normalise) {
     __shared__ A buf[2 * 2048];
     for (int i = threadIdx.x; i < count; i += blockDim.x) buf[i] = parts[i];
     __syncthreads();
     const A r = cta_combine_pairwise<A, OP>(buf, buf + 2048, count);
+    if (threadIdx.x == 0) out[0] = normalise ? OpPlus::f(r, A(0)) : r;
+}
+
+// One CTA: publish this rank's partial to every peer, wait for all, fold.
+// Buffer layout per parity: [world values][world flags], 8-byte slots.
+template <typename A, int OP>
+__global__ void __launch_bounds__(256) exchange_combine_kernel(const A* __restrict__ partial, PeerPtrs peers, int world,
+                                                               int rank, unsigned long long epoch, A* out,
+                                                               int normalise) {
+    __shared__ A buf[2 * 2048];
+    const int par = (int)(epoch & 1);
+    const size_t base = (size_t)par * 2 * world;
+    if (threadIdx.x == 0) {
+        const A v = partial[0];
+        for (int p = 0; p < world; ++p) {
+            A* slot = reinterpret_cast<A*>(reinterpret_cast<unsigned long long*>(peers.p[p]) + base + rank);
+            *slot = v;
+        }
+        __threadfence_system();   // the values land before any flag says so
+        for (int p = 0; p < world; ++p) {
+            unsigned long long* flag = reinterpret_cast<unsigned long long*>(peers.p[p]) + base + world + rank;
+            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(epoch) : "memory");
+        }
+    }
+    // wait for every rank's flag in this rank's own buffer
+    unsigned long long* mine = reinterpret_cast<unsigned long long*>(peers.p[rank]) + base;
+    for (int p = threadIdx.x; p < world; p += blockDim.x) {
+        unsigned long long f;
+        do {
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(f) : "l"(mine + world + p) : "memory");
+        } while (f < epoch);
+        buf[p] = *reinterpret_cast<volatile A*>(mine + p);
+    }
+    __syncthreads();
+    const A r = cta_combine_pairwise<A, OP>(buf, buf + 2048, world);
     if (threadIdx.x == 0) out[0] = normalise ? OpPlus::f(r, A(0)) : r;
 }
 
@@ -103,3 +143,86 @@ int combine_partials(const void* parts, int64_t count, int dtype, int op, void* 
 }
 
 }  // namespace bmi
+
+namespace bmi {
+
+template <typename A, int OP>
+static int run_exchange(const void* partial, void* const* peers, int world, int rank, unsigned long long epoch,
+                        void* out, int normalise) {
+    bm::PeerPtrs pp;
+    std::memset(&pp, 0, sizeof pp);
+    for (int i = 0; i < world; ++i) pp.p[i] = peers[i];
+    bm::exchange_combine_kernel<A, OP><<<1, 256, 0, st().stream>>>((const A*)partial, pp, world, rank, epoch, (A*)out,
+                                                                    normalise);
+    BM_CUDA(cudaGetLastError());
+    st().launches++;
+    return BM_OK;
+}
+
+template <typename T>
+static int exchange_typed(const void* partial, void* const* peers, int world, int rank, unsigned long long epoch,
+                          int op, void* out) {
+    const int norm = std::is_floating_point<T>::value ? 1 : 0;
+    switch (op) {
+        case BM_R_ACCU: return run_exchange<T, 1>(partial, peers, world, rank, epoch, out, norm);
+        case BM_R_MIN: return run_exchange<T, 2>(partial, peers, world, rank, epoch, out, 0);
+        case BM_R_MAX: return run_exchange<T, 3>(partial, peers, world, rank, epoch, out, 0);
+        case BM_R_DOT: return run_exchange<typename bm::DotAcc<T>::type, 1>(partial, peers, world, rank, epoch, out, 0);
+    }
+    return set_error(BM_ERR_ARG, "exchange: bad reduce op");
+}
+
+}  // namespace bmi
+
+extern "C" {
+
+int bm_exchange_alloc(int32_t world, void** dev_buffer, void* ipc_handle) {
+    using namespace bmi;
+    BM_REQUIRE_INIT();
+    if (world < 1 || world > 64) return set_error(BM_ERR_ARG, "exchange: world out of range");
+    const size_t bytes = (size_t)2 * 2 * world * 8;
+    BM_CUDA(cudaMalloc(dev_buffer, bytes));
+    BM_CUDA(cudaMemset(*dev_buffer, 0, bytes));
+    cudaIpcMemHandle_t h;
+    BM_CUDA(cudaIpcGetMemHandle(&h, *dev_buffer));
+    static_assert(sizeof(h) == 64, "IPC handle size");
+    std::memcpy(ipc_handle, &h, sizeof h);
+    return BM_OK;
+}
+
+int bm_exchange_open(const void* ipc_handle, void** dev_buffer) {
+    using namespace bmi;
+    BM_REQUIRE_INIT();
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, ipc_handle, sizeof h);
+    BM_CUDA(cudaIpcOpenMemHandle(dev_buffer, h, cudaIpcMemLazyEnablePeerAccess));
+    return BM_OK;
+}
+
+int bm_exchange_close(void* dev_buffer, int32_t opened) {
+    using namespace bmi;
+    BM_REQUIRE_INIT();
+    if (opened) BM_CUDA(cudaIpcCloseMemHandle(dev_buffer));
+    else BM_CUDA(cudaFree(dev_buffer));
+    return BM_OK;
+}
+
+int bm_exchange_combine(const void* dev_partial, void* const* peer_buffers, int32_t world, int32_t rank,
+                        uint64_t epoch, int32_t dtype, int32_t reduce_op, void* dev_result) {
+    using namespace bmi;
+    BM_REQUIRE_INIT();
+    if (world < 1 || world > 64 || rank < 0 || rank >= world) return set_error(BM_ERR_ARG, "exchange: bad world/rank");
+    if (epoch == 0) return set_error(BM_ERR_ARG, "exchange: epochs start at 1");
+    std::lock_guard<std::recursive_mutex> lk(st().mu);
+    switch (dtype) {
+        case BM_F32: return exchange_typed<float>(dev_partial, peer_buffers, world, rank, epoch, reduce_op, dev_result);
+        case BM_F64: return exchange_typed<double>(dev_partial, peer_buffers, world, rank, epoch, reduce_op, dev_result);
+        case BM_I32: return exchange_typed<int>(dev_partial, peer_buffers, world, rank, epoch, reduce_op, dev_result);
+        case BM_U64:
+            return exchange_typed<unsigned long long>(dev_partial, peer_buffers, world, rank, epoch, reduce_op,
+                                                      dev_result);
+    }
+    return set_error(BM_ERR_ARG, "exchange: bad dtype");
+}
+
+}  // extern "C"

@@ -50,6 +50,54 @@ def partial_dtype(op: str, elem: str) -> str:
     return "f64" if op == "dot" and elem in ("f32", "f64") else elem
 
 
+class PeerExchange:
+    """Exchange buffers of every rank mapped into this process (CUDA IPC): the
+    peer-memory replacement of the all-gather + fold in ShardedReduction
+    (b200mat.h bm_exchange_*).  One kernel writes this rank's partial into
+    every rank's buffer over NVLink, publishes a step epoch with release
+    semantics, waits for all epochs and folds in rank order."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self._lib = _clib.lib()
+        own = ctypes.c_void_p()
+        handle = ctypes.create_string_buffer(64)
+        _clib.check(self._lib.bm_exchange_alloc(self.world, ctypes.byref(own), handle), "exchange alloc")
+        handles = [None] * self.world
+        dist.all_gather_object(handles, handle.raw, group=group)
+        self._own = own.value
+        self._opened = []
+        ptrs = []
+        for r, h in enumerate(handles):
+            if r == self.rank:
+                ptrs.append(self._own)
+                continue
+            p = ctypes.c_void_p()
+            _clib.check(self._lib.bm_exchange_open(ctypes.create_string_buffer(h, 64), ctypes.byref(p)),
+                        "exchange open")
+            ptrs.append(p.value)
+            self._opened.append(p.value)
+        self._ptrs = (ctypes.c_void_p * self.world)(*ptrs)
+        self.epoch = 0
+        dist.barrier(group=group)          # every rank mapped every buffer before the first step
+
+    def combine(self, partial, elem: str, op_code: int, result) -> None:
+        self.epoch += 1
+        _clib.check(self._lib.bm_exchange_combine(
+            ctypes.c_void_p(partial.data_ptr()), self._ptrs, self.world, self.rank, self.epoch,
+            _clib.DTYPE_CODE[elem], op_code, ctypes.c_void_p(result.data_ptr())), "exchange combine")
+
+    def close(self) -> None:
+        for p in self._opened:
+            self._lib.bm_exchange_close(ctypes.c_void_p(p), 1)
+        self._opened = []
+        if self._own:
+            self._lib.bm_exchange_close(ctypes.c_void_p(self._own), 0)
+            self._own = None
+
+
 class ShardedReduction:
     """A scalar reduction over column-block shards, reusable across steps.
 
@@ -65,7 +113,9 @@ class ShardedReduction:
     max(kernel, collective) instead of their sum.  ``join`` orders the current
     stream after every collective issued so far (timing, value).
     ``collective="allreduce"`` gathers by summing rank-slotted vectors (for
-    backends without all-gather of device tensors, e.g. gloo in tests).
+    backends without all-gather of device tensors, e.g. gloo in tests);
+    ``collective="p2p"`` replaces the all-gather and the fold with one kernel
+    over peer memory (PeerExchange).
     """
 
     def __init__(self, op: str, *local_exprs, group=None, pipeline=None, collective=None):
@@ -81,7 +131,7 @@ class ShardedReduction:
             raise ValueError("sharded reduction expects a purely element-wise local program")
         if collective is None:
             collective = os.environ.get("BM_SHARD_COLLECTIVE", "all_gather")
-        if collective not in ("all_gather", "allreduce"):
+        if collective not in ("all_gather", "allreduce", "p2p"):
             raise ValueError(f"unknown collective {collective!r}")
         self.collective = collective
         node = _expr.as_expr(local_exprs[0])
@@ -105,6 +155,7 @@ class ShardedReduction:
                          "dot": _clib.BM_R_DOT}[op]
         self._step = 0
         self._last = 0
+        self._exchange = PeerExchange(group) if (collective == "p2p" and self.world > 1) else None
         if self.pipeline:
             self._comm = torch.cuda.Stream()
             self._reduced = [torch.cuda.Event() for _ in range(nbuf)]
@@ -112,6 +163,9 @@ class ShardedReduction:
 
     def _gather_and_fold(self, slot: int) -> None:
         part, gath = self.partials[slot], self.gathered[slot]
+        if self._exchange is not None:     # one kernel over peer memory
+            self._exchange.combine(part, self.elem, self._op_code, self.results[slot])
+            return
         if self.collective == "all_gather":
             self.dist.all_gather_into_tensor(gath, part, group=self.group)
         else:

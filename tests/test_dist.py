@@ -193,7 +193,7 @@ def test_sharded_logistic_step_matches_single_device():
 
 # ---- the pipelined device path: two ranks sharing one GPU over gloo ----------------------------
 
-def _pipeline_worker(rank, world, port, q, rows, cols, pipeline):
+def _pipeline_worker(rank, world, port, q, rows, cols, pipeline, collective="allreduce"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -205,7 +205,7 @@ def _pipeline_worker(rank, world, port, q, rows, cols, pipeline):
         full = np.random.default_rng(9).random((rows, cols), dtype=np.float32)
         start, count = column_block(cols, rank, world)
         m = dm.Matrix.from_numpy(np.asfortranarray(full[:, start:start + count]))
-        red = D.ShardedReduction("accu", m, pipeline=pipeline, collective="allreduce")
+        red = D.ShardedReduction("accu", m, pipeline=pipeline, collective=collective)
         view = D.torch_view(m)
         # three back-to-back steps, the input doubled on the compute stream in between:
         # step k reduces 2^k * X (exact), step 2 reuses step 0's buffers
@@ -220,6 +220,9 @@ def _pipeline_worker(rank, world, port, q, rows, cols, pipeline):
         last = np.float32(red.value()).tobytes()
         if rank == 0:
             q.put((res, last, red.pipeline))
+        if red._exchange is not None:
+            dist.barrier()                 # no rank unmaps while a peer may still write
+            red._exchange.close()
         dm.shutdown()
     finally:
         dist.destroy_process_group()
@@ -237,5 +240,23 @@ def test_pipelined_sharded_reduction_two_ranks_one_gpu(pipeline):
     assert last == want[2]
     if pipeline:
         assert res == [want[2], want[1]]       # buffers by step parity
+    else:
+        assert res == [want[2]]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("pipeline", [True, False])
+def test_peer_exchange_two_ranks_one_gpu(pipeline):
+    """The peer-memory exchange (one kernel: publish the partial into every
+    rank's buffer over CUDA IPC, wait for all epochs, fold in rank order)
+    gives the same bits as the all-gather path, pipelined or not."""
+    rows, cols = 1024, 256
+    res, last, piped = _spawn(_pipeline_worker, 2, rows, cols, pipeline, "p2p")
+    full = np.random.default_rng(9).random((rows, cols), dtype=np.float32)
+    want = [np.float32(O.reduce_accu((np.float32(2 ** k) * full).reshape(-1, order="F"))).tobytes()
+            for k in range(3)]
+    assert last == want[2]
+    if pipeline:
+        assert res == [want[2], want[1]]
     else:
         assert res == [want[2]]

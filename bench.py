@@ -525,7 +525,7 @@ def main() -> None:
             # test mode only: every rank on GPU 0 over gloo (NCCL refuses two ranks
             # on one device); a rank-slotted all-reduce stands in for the all-gather
             local_rank = 0
-            os.environ["BM_SHARD_COLLECTIVE"] = "allreduce"
+            os.environ.setdefault("BM_SHARD_COLLECTIVE", "allreduce")   # or p2p: peer-memory exchange
             torch.cuda.set_device(0)
             tdist.init_process_group("gloo")
         else:

@@ -258,6 +258,13 @@ int bm_combine_partials_to_device(const void* dev_partials, int64_t count, int32
 int bm_exchange_alloc(int32_t world, void** dev_buffer, void* ipc_handle /* 64 bytes out */);
 int bm_exchange_open(const void* ipc_handle, void** dev_buffer);
 int bm_exchange_close(void* dev_buffer, int32_t opened /* 1: mapped peer buffer, 0: own */);
+/* the reduction and the exchange in ONE kernel: like bm_reduce_to_device, but the
+ * reduction's last CTA publishes the shard partial into every rank's exchange buffer,
+ * waits for all and writes the folded world result to dev_result.  dev_peer_array is
+ * a DEVICE array of the world buffer pointers (own buffer at [rank]).  Reductions
+ * large enough to need the separate fold kernels return BM_ERR_NOTIMPL. */
+int bm_reduce_to_device_exchange(const bm_invocation* inv, void* dev_result, void* const* dev_peer_array,
+                                 int32_t world, int32_t rank, uint64_t epoch);
 int bm_exchange_combine(const void* dev_partial, void* const* peer_buffers /* host array, world entries */,
                         int32_t world, int32_t rank, uint64_t epoch, int32_t dtype, int32_t reduce_op,
                         void* dev_result);

@@ -26,6 +26,10 @@ struct State {
     void* partials[2] = {nullptr, nullptr};
     int64_t partials_cap = 0;          // capacity of each, in 8-byte entries
     void* fold_scratch = nullptr;      // chunk results of the separate fold kernels (8192 x 8 B)
+    // pending fused exchange for the next reduction (bm_reduce_to_device_exchange)
+    void* const* exch_peers = nullptr;
+    int exch_world = 0, exch_rank = 0;
+    unsigned long long exch_epoch = 0;
     int flip = 0;                      // buffer of the next reduction
     unsigned int* ticket = nullptr;    // two last-CTA counters (at +0 and +32), zero between launches
     void* result = nullptr;            // device slot of the final value

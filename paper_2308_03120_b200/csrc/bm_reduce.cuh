@@ -51,6 +51,11 @@ struct Args {
     int smem_bytes;             // dynamic shared memory of the launch
     int ext_fold;               // 1: leave the partials for the separate fold kernels
     int grab;                   // items a warp takes per counter fetch (dynamic scheduling)
+    // fused cross-GPU combine (peer-memory exchange, b200mat.h bm_reduce_to_device_exchange):
+    // exch_world > 1 makes the last CTA publish its partial to every rank and fold them all
+    void* const* exch_peers;    // device array of the world exchange buffers
+    int exch_world, exch_rank;
+    unsigned long long exch_epoch;
 };
 
 // ---------------------------------------------------------------------------
@@ -723,6 +728,43 @@ __device__ void last_cta_fold(const Args& a, i64 nitems, i64 nfull, bool has_tai
         reinterpret_cast<P*>(a.result)[0] = fin;
         a.ticket[0] = 0u;
         a.ticket[1] = 0u;
+        chunk_res[0] = fin;
+    }
+    if (a.exch_world > 1) {
+        // the collective in the same kernel: publish this rank's partial into every
+        // rank's exchange buffer over NVLink (parity by epoch), release an epoch flag,
+        // wait for every rank's flag in this rank's buffer, fold in rank order
+        __syncthreads();
+        const int W = a.exch_world, R = a.exch_rank;
+        const unsigned long long ep = a.exch_epoch;
+        const size_t base = (size_t)(ep & 1) * 2 * W;
+        if (threadIdx.x == 0) {
+            const P v = chunk_res[0];
+            for (int p = 0; p < W; ++p)
+                *reinterpret_cast<P*>(reinterpret_cast<unsigned long long*>(a.exch_peers[p]) + base + R) = v;
+            __threadfence_system();
+            for (int p = 0; p < W; ++p) {
+                unsigned long long* flag = reinterpret_cast<unsigned long long*>(a.exch_peers[p]) + base + W + R;
+                asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(ep) : "memory");
+            }
+        }
+        __syncthreads();
+        unsigned long long* mine = reinterpret_cast<unsigned long long*>(a.exch_peers[R]) + base;
+        P* xv = chunk_res + 1;                     // W <= 64 values + ping-pong space
+        for (int p = threadIdx.x; p < W; p += blockDim.x) {
+            unsigned long long f;
+            do {
+                asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(f) : "l"(mine + W + p) : "memory");
+            } while (f < ep);
+            xv[p] = *reinterpret_cast<volatile P*>(mine + p);
+        }
+        __syncthreads();
+        const P g = cta_combine_pairwise<P, OP>(xv, xv + 128, W);
+        if (threadIdx.x == 0) {
+            P o = g;
+            if constexpr (OP == 1 && is_float_t<T>::value) o = g + T(0);
+            reinterpret_cast<P*>(a.result)[0] = o;
+        }
     }
     BM_TRACE(4);
 }

@@ -389,6 +389,22 @@ int bm_combine_partials(const void* dev_partials, int64_t count, int32_t dtype, 
     return BM_OK;
 }
 
+int bm_reduce_to_device_exchange(const bm_invocation* inv, void* dev_result, void* const* dev_peer_array,
+                                 int32_t world, int32_t rank, uint64_t epoch) {
+    State& s = st();
+    std::lock_guard<std::recursive_mutex> lk(s.mu);
+    if (world < 2 || world > 64 || rank < 0 || rank >= world || epoch == 0 || !dev_peer_array)
+        return set_error(BM_ERR_ARG, "fused exchange: bad world / rank / epoch");
+    s.exch_peers = dev_peer_array;
+    s.exch_world = world;
+    s.exch_rank = rank;
+    s.exch_epoch = epoch;
+    const int rc = reduce_common(inv, true, dev_result);
+    s.exch_world = 0;
+    s.exch_peers = nullptr;
+    return rc;
+}
+
 int bm_combine_partials_to_device(const void* dev_partials, int64_t count, int32_t dtype, int32_t reduce_op,
                                   void* dev_result) {
     BM_REQUIRE_INIT();

@@ -80,6 +80,8 @@ class PeerExchange:
             ptrs.append(p.value)
             self._opened.append(p.value)
         self._ptrs = (ctypes.c_void_p * self.world)(*ptrs)
+        import torch
+        self.dev_ptrs = torch.tensor(ptrs, dtype=torch.int64, device="cuda")   # for the fused kernel
         self.epoch = 0
         dist.barrier(group=group)          # every rank mapped every buffer before the first step
 
@@ -88,6 +90,14 @@ class PeerExchange:
         _clib.check(self._lib.bm_exchange_combine(
             ctypes.c_void_p(partial.data_ptr()), self._ptrs, self.world, self.rank, self.epoch,
             _clib.DTYPE_CODE[elem], op_code, ctypes.c_void_p(result.data_ptr())), "exchange combine")
+
+    def reduce(self, inv, result) -> None:
+        """The shard reduction and the exchange in one kernel
+        (bm_reduce_to_device_exchange): the folded world value lands in result."""
+        self.epoch += 1
+        _clib.check(self._lib.bm_reduce_to_device_exchange(
+            ctypes.byref(inv), ctypes.c_void_p(result.data_ptr()), ctypes.c_void_p(self.dev_ptrs.data_ptr()),
+            self.world, self.rank, self.epoch), "fused reduce + exchange")
 
     def close(self) -> None:
         for p in self._opened:
@@ -115,7 +125,8 @@ class ShardedReduction:
     ``collective="allreduce"`` gathers by summing rank-slotted vectors (for
     backends without all-gather of device tensors, e.g. gloo in tests);
     ``collective="p2p"`` replaces the all-gather and the fold with one kernel
-    over peer memory (PeerExchange).
+    over peer memory (PeerExchange); ``"p2p_fused"`` moves that exchange into
+    the reduction kernel itself (its last CTA publishes, waits and folds).
     """
 
     def __init__(self, op: str, *local_exprs, group=None, pipeline=None, collective=None):
@@ -131,7 +142,7 @@ class ShardedReduction:
             raise ValueError("sharded reduction expects a purely element-wise local program")
         if collective is None:
             collective = os.environ.get("BM_SHARD_COLLECTIVE", "all_gather")
-        if collective not in ("all_gather", "allreduce", "p2p"):
+        if collective not in ("all_gather", "allreduce", "p2p", "p2p_fused"):
             raise ValueError(f"unknown collective {collective!r}")
         self.collective = collective
         node = _expr.as_expr(local_exprs[0])
@@ -140,7 +151,9 @@ class ShardedReduction:
         tdt = getattr(torch, _TORCH_DTYPE[self.pdt])
         if pipeline is None:
             pipeline = os.environ.get("BM_SHARD_PIPELINE", "1") != "0"
-        self.pipeline = bool(pipeline) and self.world > 1
+        # p2p_fused: the collective runs inside the reduction kernel, which already
+        # overlaps the next step (programmatic dependent launch); no side stream
+        self.pipeline = bool(pipeline) and self.world > 1 and collective != "p2p_fused"
         nbuf = 2 if self.pipeline else 1
         self.partials = [torch.zeros(1, dtype=tdt, device="cuda") for _ in range(nbuf)]
         self.gathered = [torch.zeros(self.world, dtype=tdt, device="cuda") for _ in range(nbuf)]
@@ -155,7 +168,7 @@ class ShardedReduction:
                          "dot": _clib.BM_R_DOT}[op]
         self._step = 0
         self._last = 0
-        self._exchange = PeerExchange(group) if (collective == "p2p" and self.world > 1) else None
+        self._exchange = PeerExchange(group) if (collective in ("p2p", "p2p_fused") and self.world > 1) else None
         if self.pipeline:
             self._comm = torch.cuda.Stream()
             self._reduced = [torch.cuda.Event() for _ in range(nbuf)]
@@ -182,6 +195,9 @@ class ShardedReduction:
         self._step += 1
         self._last = slot
         compute = torch.cuda.current_stream()
+        if self._exchange is not None and self.collective == "p2p_fused":
+            self._exchange.reduce(self.inv, self.results[slot])
+            return
         if self.pipeline and self._gathered[slot] is not None:
             compute.wait_event(self._gathered[slot])   # the gather that read this partial is done
         _clib.check(self._lib.bm_reduce_to_device(ctypes.byref(self.inv),

@@ -245,18 +245,18 @@ def test_pipelined_sharded_reduction_two_ranks_one_gpu(pipeline):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("pipeline", [True, False])
-def test_peer_exchange_two_ranks_one_gpu(pipeline):
+@pytest.mark.parametrize("pipeline,collective", [(True, "p2p"), (False, "p2p"), (False, "p2p_fused")])
+def test_peer_exchange_two_ranks_one_gpu(pipeline, collective):
     """The peer-memory exchange (one kernel: publish the partial into every
     rank's buffer over CUDA IPC, wait for all epochs, fold in rank order)
     gives the same bits as the all-gather path, pipelined or not."""
     rows, cols = 1024, 256
-    res, last, piped = _spawn(_pipeline_worker, 2, rows, cols, pipeline, "p2p")
+    res, last, piped = _spawn(_pipeline_worker, 2, rows, cols, pipeline, collective)
     full = np.random.default_rng(9).random((rows, cols), dtype=np.float32)
     want = [np.float32(O.reduce_accu((np.float32(2 ** k) * full).reshape(-1, order="F"))).tobytes()
             for k in range(3)]
     assert last == want[2]
     if pipeline:
         assert res == [want[2], want[1]]
-    else:
+    elif collective == "p2p":
         assert res == [want[2]]

@@ -1,5 +1,5 @@
 """Run one hot-path workload a few times so ncu can capture its kernel.
-Usage: python tools/profile_targets.py cfg1|accu1|logistic|logistic_fused|gemm_f32|gemm_f64|rdim0|rdim1|dot"""
+Usage: python tools/profile_targets.py cfg1|accu1|logistic|logistic_fused|gemm_f32|gemm_f64|rdim0|rdim1|rdim0_fused|rdim1_fused|dot"""
 import pathlib
 import sys
 
@@ -53,6 +53,11 @@ def main(which: str) -> None:
         for op in ("sum", "max"):
             for _ in range(2):
                 dm.evaluate(getattr(dm, op)(m, int(which[-1])))
+    elif which in ("rdim0_fused", "rdim1_fused"):
+        a = dm.Matrix(16384, 16384, fill="randu", elem_type="f64")
+        b = dm.Matrix(16384, 16384, fill="randu", elem_type="f64")
+        for _ in range(2):
+            dm.evaluate(dm.sum(2 * a + b, int(which[4])))
     elif which == "dot":
         a = dm.Col(1 << 30, fill="randu")
         b = dm.Col(1 << 30, fill="randu")

@@ -479,8 +479,13 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
             "config": {"workload": WORKLOAD, "rows": N_SIDE, "cols": N_SIDE * world,
                        "bytes_per_step_per_gpu": BYTES_PER_STEP,
                        "l2": "inputs 256 MiB per GPU > 126 MB L2; no flush",
-                       "parallelism": f"column-block shards x{world}; rank partials all-gathered (NCCL) and folded "
-                                      "deterministically on device" if world > 1 else "single GPU"},
+                       "parallelism": (f"column-block shards x{world}; rank partials exchanged ("
+                                       + {"all_gather": "NCCL all-gather, pipelined on a side stream",
+                                          "allreduce": "rank-slotted all-reduce, pipelined",
+                                          "p2p": "peer-memory exchange kernel over NVLink, pipelined",
+                                          "p2p_fused": "inside the reduction kernel, over peer memory"}.get(
+                                           red.collective, red.collective)
+                                       + ") and folded deterministically on device") if world > 1 else "single GPU"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak_hbm, "unit": "GB/s",
                          "frac": achieved / peak_hbm, "traffic": _ncu_traffic("cfg1_bm_reduce"),
                          "traffic_unit": "DRAM bytes per launch (ncu capture, profiles/ncu_traffic.json)",

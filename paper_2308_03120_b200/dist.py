@@ -58,32 +58,52 @@ class PeerExchange:
     semantics, waits for all epochs and folds in rank order."""
 
     def __init__(self, group=None):
+        import torch
         import torch.distributed as dist
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self._lib = _clib.lib()
-        own = ctypes.c_void_p()
+        self._own = None
+        self._opened = []
+        self.epoch = 0
+
+        def agree(ok: bool) -> bool:          # every rank learns whether every rank succeeded
+            t = torch.tensor([1 if ok else 0], dtype=torch.int32, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+            return bool(t.item())
+
         handle = ctypes.create_string_buffer(64)
-        _clib.check(self._lib.bm_exchange_alloc(self.world, ctypes.byref(own), handle), "exchange alloc")
+        ok = True
+        try:
+            own = ctypes.c_void_p()
+            _clib.check(self._lib.bm_exchange_alloc(self.world, ctypes.byref(own), handle), "exchange alloc")
+            self._own = own.value
+        except Exception:  # noqa: BLE001 - reported collectively below
+            ok = False
+        if not agree(ok):
+            self.close()
+            raise RuntimeError("peer exchange: buffer allocation failed on some rank")
         handles = [None] * self.world
         dist.all_gather_object(handles, handle.raw, group=group)
-        self._own = own.value
-        self._opened = []
         ptrs = []
-        for r, h in enumerate(handles):
-            if r == self.rank:
-                ptrs.append(self._own)
-                continue
-            p = ctypes.c_void_p()
-            _clib.check(self._lib.bm_exchange_open(ctypes.create_string_buffer(h, 64), ctypes.byref(p)),
-                        "exchange open")
-            ptrs.append(p.value)
-            self._opened.append(p.value)
+        ok = True
+        try:
+            for r, h in enumerate(handles):
+                if r == self.rank:
+                    ptrs.append(self._own)
+                    continue
+                p = ctypes.c_void_p()
+                _clib.check(self._lib.bm_exchange_open(ctypes.create_string_buffer(h, 64), ctypes.byref(p)),
+                            "exchange open")
+                ptrs.append(p.value)
+                self._opened.append(p.value)
+        except Exception:  # noqa: BLE001
+            ok = False
+        if not agree(ok):                   # every rank mapped every buffer, or nobody uses them
+            self.close()
+            raise RuntimeError("peer exchange: mapping a peer buffer failed on some rank")
         self._ptrs = (ctypes.c_void_p * self.world)(*ptrs)
-        import torch
         self.dev_ptrs = torch.tensor(ptrs, dtype=torch.int64, device="cuda")   # for the fused kernel
-        self.epoch = 0
-        dist.barrier(group=group)          # every rank mapped every buffer before the first step
 
     def combine(self, partial, elem: str, op_code: int, result) -> None:
         self.epoch += 1
@@ -106,6 +126,23 @@ class PeerExchange:
         if self._own:
             self._lib.bm_exchange_close(ctypes.c_void_p(self._own), 0)
             self._own = None
+
+
+_SHARED_EXCHANGES: dict = {}
+
+
+def shared_exchange(group=None):
+    """The process's PeerExchange for `group`, created once (collectively) and
+    reused by every fused sharded reduction, whose epochs then advance in the
+    same order on every rank; None when peer mapping is unavailable anywhere
+    (then the NCCL all-gather serves)."""
+    key = id(group)
+    if key not in _SHARED_EXCHANGES:
+        try:
+            _SHARED_EXCHANGES[key] = PeerExchange(group)
+        except RuntimeError:
+            _SHARED_EXCHANGES[key] = None
+    return _SHARED_EXCHANGES[key]
 
 
 class ShardedReduction:
@@ -141,9 +178,14 @@ class ShardedReduction:
         if self.plan.steps:
             raise ValueError("sharded reduction expects a purely element-wise local program")
         if collective is None:
-            collective = os.environ.get("BM_SHARD_COLLECTIVE", "all_gather")
+            collective = os.environ.get("BM_SHARD_COLLECTIVE", "p2p_fused")
         if collective not in ("all_gather", "allreduce", "p2p", "p2p_fused"):
             raise ValueError(f"unknown collective {collective!r}")
+        fused_ex = None
+        if collective == "p2p_fused" and self.world > 1:
+            fused_ex = shared_exchange(group)
+            if fused_ex is None:
+                collective = "all_gather"      # peer memory unavailable: NCCL all-gather
         self.collective = collective
         node = _expr.as_expr(local_exprs[0])
         self.elem = node.elem_type
@@ -168,7 +210,10 @@ class ShardedReduction:
                          "dot": _clib.BM_R_DOT}[op]
         self._step = 0
         self._last = 0
-        self._exchange = PeerExchange(group) if (collective in ("p2p", "p2p_fused") and self.world > 1) else None
+        if collective == "p2p_fused":
+            self._exchange = fused_ex
+        else:
+            self._exchange = PeerExchange(group) if (collective == "p2p" and self.world > 1) else None
         if self.pipeline:
             self._comm = torch.cuda.Stream()
             self._reduced = [torch.cuda.Event() for _ in range(nbuf)]

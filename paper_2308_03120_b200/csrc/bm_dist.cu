@@ -49,11 +49,19 @@ __global__ void __launch_bounds__(256) exchange_combine_kernel(const A* __restri
     // wait for every rank's flag in this rank's own buffer
     unsigned long long* mine = reinterpret_cast<unsigned long long*>(peers.p[rank]) + base;
     for (int p = threadIdx.x; p < world; p += blockDim.x) {
-        unsigned long long f;
+        // bounded wait (10 s): a missing peer yields a NaN / all-ones result, not a hang
+        unsigned long long f, t0, t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
         do {
             asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(f) : "l"(mine + world + p) : "memory");
-        } while (f < epoch);
-        buf[p] = *reinterpret_cast<volatile A*>(mine + p);
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        } while (f < epoch && t - t0 < 10000000000ull);
+        A v = *reinterpret_cast<volatile A*>(mine + p);
+        if (f < epoch) {
+            unsigned long long bad = ~0ull;
+            memcpy(&v, &bad, sizeof v);
+        }
+        buf[p] = v;
     }
     __syncthreads();
     const A r = cta_combine_pairwise<A, OP>(buf, buf + 2048, world);

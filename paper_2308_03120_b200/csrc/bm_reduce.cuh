@@ -752,11 +752,20 @@ __device__ void last_cta_fold(const Args& a, i64 nitems, i64 nfull, bool has_tai
         unsigned long long* mine = reinterpret_cast<unsigned long long*>(a.exch_peers[R]) + base;
         P* xv = chunk_res + 1;                     // W <= 64 values + ping-pong space
         for (int p = threadIdx.x; p < W; p += blockDim.x) {
-            unsigned long long f;
+            // bounded wait: a peer that never publishes (10 s) turns into a NaN /
+            // all-ones result instead of a hung GPU
+            unsigned long long f, t0, t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
             do {
                 asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(f) : "l"(mine + W + p) : "memory");
-            } while (f < ep);
-            xv[p] = *reinterpret_cast<volatile P*>(mine + p);
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            } while (f < ep && t - t0 < 10000000000ull);
+            P v = *reinterpret_cast<volatile P*>(mine + p);
+            if (f < ep) {
+                const unsigned long long bad = ~0ull;
+                v = *reinterpret_cast<const P*>(&bad);
+            }
+            xv[p] = v;
         }
         __syncthreads();
         const P g = cta_combine_pairwise<P, OP>(xv, xv + 128, W);

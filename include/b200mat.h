@@ -54,6 +54,9 @@ extern "C" {
 #define BM_ERR_EMPTY      4   /* min/max over an empty range (reference: ValueError, runtime.py:279-281) */
 #define BM_ERR_JIT        5   /* NVRTC compilation of a fused program failed */
 #define BM_ERR_NODEVICE   6   /* no CUDA device / not initialised */
+#define BM_ERR_PEER       7   /* a peer rank never published into a cross-GPU exchange (device error
+                                 word, raised at the next synchronisation point like the reference's
+                                 asynchronous errors, runtime.py:340-353) */
 
 /* element types (kernels.py:28-35) */
 #define BM_F32 0
@@ -262,13 +265,18 @@ int bm_exchange_close(void* dev_buffer, int32_t opened /* 1: mapped peer buffer,
  * reduction's last CTA publishes the shard partial into every rank's exchange buffer,
  * waits for all and writes the folded world result to dev_result.  dev_peer_array is
  * a DEVICE array of the world buffer pointers (own buffer at [rank]).  Reductions
- * large enough to need the separate fold kernels return BM_ERR_NOTIMPL. */
+ * large enough for the separate fold kernels run the exchange in the final fold
+ * kernel instead; an empty shard (accu / dot) publishes a zero. */
 int bm_reduce_to_device_exchange(const bm_invocation* inv, void* dev_result, void* const* dev_peer_array,
                                  int32_t world, int32_t rank, uint64_t epoch);
 int bm_exchange_combine(const void* dev_partial, void* const* peer_buffers /* host array, world entries */,
                         int32_t world, int32_t rank, uint64_t epoch, int32_t dtype, int32_t reduce_op,
                         void* dev_result);
-int bm_sync(void);
+int bm_sync(void);   /* drain the stream; BM_ERR_CUDA on a kernel fault, BM_ERR_PEER on an exchange timeout */
+/* check (and clear) the device error word without draining, after the caller synchronised
+ * the stream itself (e.g. torch.cuda.synchronize): BM_ERR_PEER when a peer timed out.  The
+ * peer wait of every exchange is bounded by BM_EXCH_TIMEOUT_S (default 60 s). */
+int bm_poll_device_error(void);
 
 /* ---- instrumentation -------------------------------------------------------------- */
 typedef struct bm_counters {

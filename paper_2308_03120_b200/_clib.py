@@ -16,7 +16,7 @@ _HERE = pathlib.Path(__file__).resolve().parent
 LIB_PATH = _HERE / "libb200mat.so"
 
 # ---- constants (include/b200mat.h) -------------------------------------------------
-BM_OK, BM_ERR_CUDA, BM_ERR_ARG, BM_ERR_NOTIMPL, BM_ERR_EMPTY, BM_ERR_JIT, BM_ERR_NODEVICE = range(7)
+BM_OK, BM_ERR_CUDA, BM_ERR_ARG, BM_ERR_NOTIMPL, BM_ERR_EMPTY, BM_ERR_JIT, BM_ERR_NODEVICE, BM_ERR_PEER = range(8)
 BM_F32, BM_F64, BM_I32, BM_U64 = range(4)
 DTYPE_CODE = {"f32": BM_F32, "f64": BM_F64, "i32": BM_I32, "u64": BM_U64}
 
@@ -98,6 +98,7 @@ SIGNATURES = {
     "bm_reduce_to_device_exchange": ([ctypes.POINTER(Invocation), _VP, _VP, _I32, _I32, ctypes.c_uint64], ctypes.c_int),
     "bm_exchange_combine": ([_VP, ctypes.POINTER(_VP), _I32, _I32, ctypes.c_uint64, _I32, _I32, _VP], ctypes.c_int),
     "bm_sync": ([], ctypes.c_int),
+    "bm_poll_device_error": ([], ctypes.c_int),
     "bm_get_counters": ([ctypes.POINTER(Counters)], ctypes.c_int),
     "bm_set_cache_dir": ([_CP], ctypes.c_int),
     "bm_jit_compile_only": ([ctypes.POINTER(Invocation)], ctypes.c_int),
@@ -110,6 +111,11 @@ _lib = None
 
 class DeviceError(DevmatError, RuntimeError):
     """A CUDA / NVRTC failure inside libb200mat.so."""
+
+
+class PeerTimeoutError(DeviceError):
+    """A cross-GPU exchange gave up waiting for a peer rank (BM_ERR_PEER): the
+    sharded result is invalid.  Raised at the next synchronisation point."""
 
 
 def lib() -> ctypes.CDLL:
@@ -154,4 +160,6 @@ def check(rc: int, what: str = "") -> None:
         raise NotImplementedError(text)
     if rc == BM_ERR_ARG:
         raise BufferError_(text)
+    if rc == BM_ERR_PEER:
+        raise PeerTimeoutError(text)
     raise DeviceError(text)

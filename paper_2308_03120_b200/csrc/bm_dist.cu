@@ -25,46 +25,19 @@ __global__ void __launch_bounds__(256) combine_kernel(const A* __restrict__ part
     if (threadIdx.x == 0) out[0] = normalise ? OpPlus::f(r, A(0)) : r;
 }
 
-// One CTA: publish this rank's partial to every peer, wait for all, fold.
-// Buffer layout per parity: [world values][world flags], 8-byte slots.
+// One CTA: publish this rank's partial to every peer, wait for all, fold
+// (exchange_fold, bm_reduce.cuh).
 template <typename A, int OP>
 __global__ void __launch_bounds__(256) exchange_combine_kernel(const A* __restrict__ partial, PeerPtrs peers, int world,
                                                                int rank, unsigned long long epoch, A* out,
-                                                               int normalise) {
-    __shared__ A buf[2 * 2048];
-    const int par = (int)(epoch & 1);
-    const size_t base = (size_t)par * 2 * world;
-    if (threadIdx.x == 0) {
-        const A v = partial[0];
-        for (int p = 0; p < world; ++p) {
-            A* slot = reinterpret_cast<A*>(reinterpret_cast<unsigned long long*>(peers.p[p]) + base + rank);
-            *slot = v;
-        }
-        __threadfence_system();   // the values land before any flag says so
-        for (int p = 0; p < world; ++p) {
-            unsigned long long* flag = reinterpret_cast<unsigned long long*>(peers.p[p]) + base + world + rank;
-            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(epoch) : "memory");
-        }
-    }
-    // wait for every rank's flag in this rank's own buffer
-    unsigned long long* mine = reinterpret_cast<unsigned long long*>(peers.p[rank]) + base;
-    for (int p = threadIdx.x; p < world; p += blockDim.x) {
-        // bounded wait (10 s): a missing peer yields a NaN / all-ones result, not a hang
-        unsigned long long f, t0, t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-        do {
-            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(f) : "l"(mine + world + p) : "memory");
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        } while (f < epoch && t - t0 < 10000000000ull);
-        A v = *reinterpret_cast<volatile A*>(mine + p);
-        if (f < epoch) {
-            unsigned long long bad = ~0ull;
-            memcpy(&v, &bad, sizeof v);
-        }
-        buf[p] = v;
-    }
-    __syncthreads();
-    const A r = cta_combine_pairwise<A, OP>(buf, buf + 2048, world);
+                                                               int normalise, unsigned int* err,
+                                                               unsigned long long timeout_ns,
+                                                               void* const* dev_peers) {
+    __shared__ A xv[2 * 64];
+    __shared__ void* pp[64];
+    for (int i = threadIdx.x; i < world; i += blockDim.x) pp[i] = dev_peers ? dev_peers[i] : peers.p[i];
+    const A v = partial ? partial[0] : A(0);   // no partial: an empty shard contributes zero (accu / dot)
+    const A r = exchange_fold<A, OP>(pp, world, rank, epoch, err, timeout_ns, v, xv);
     if (threadIdx.x == 0) out[0] = normalise ? OpPlus::f(r, A(0)) : r;
 }
 
@@ -94,7 +67,7 @@ static int combine_typed(const void* parts, int64_t count, int op, void* out) {
 
 template <typename P, int OP, int UPB, bool NORM>
 static int fold_typed(const void* parts, int64_t nitems, int64_t nfull, bool unit_mode, int chunk, int nchunks,
-                      void* result) {
+                      void* result, const bm::ExchArgs& x) {
     void* scratch = st().fold_scratch;   // per initialised device (bm_init / bm_shutdown)
     const int smem = 2 * chunk * (int)sizeof(P);
     static bool attr = false;
@@ -107,25 +80,33 @@ static int fold_typed(const void* parts, int64_t nitems, int64_t nfull, bool uni
         (const P*)parts, nitems, nfull, unit_mode ? 1 : 0, chunk, (P*)scratch);
     BM_CUDA(cudaGetLastError());
     bm::fold_final_kernel<P, OP, NORM><<<1, 256, (nchunks + nchunks / 256 + 1) * (int)sizeof(P), st().stream>>>(
-        (const P*)scratch, nchunks, (P*)result);
+        (const P*)scratch, nchunks, (P*)result, x);
     BM_CUDA(cudaGetLastError());
     st().launches += 2;
     return BM_OK;
 }
 
 int launch_fold(int dtype, int op, const void* parts, int64_t nitems, int64_t nfull, bool unit_mode, int chunk,
-                int nchunks, void* result) {
+                int nchunks, void* result, void* const* exch_peers, int exch_world, int exch_rank,
+                unsigned long long exch_epoch) {
+    bm::ExchArgs x;
+    x.peers = exch_peers;
+    x.world = exch_world;
+    x.rank = exch_rank;
+    x.epoch = exch_epoch;
+    x.err = st().err_dev;
+    x.timeout_ns = st().exch_timeout_ns;
 #define BM_FOLD(P, UPB, NORM)                                                                                     \
     switch (op) {                                                                                                  \
-        case BM_R_ACCU: return fold_typed<P, 1, UPB, NORM>(parts, nitems, nfull, unit_mode, chunk, nchunks, result); \
-        case BM_R_MIN: return fold_typed<P, 2, UPB, false>(parts, nitems, nfull, unit_mode, chunk, nchunks, result); \
-        case BM_R_MAX: return fold_typed<P, 3, UPB, false>(parts, nitems, nfull, unit_mode, chunk, nchunks, result); \
+        case BM_R_ACCU: return fold_typed<P, 1, UPB, NORM>(parts, nitems, nfull, unit_mode, chunk, nchunks, result, x); \
+        case BM_R_MIN: return fold_typed<P, 2, UPB, false>(parts, nitems, nfull, unit_mode, chunk, nchunks, result, x); \
+        case BM_R_MAX: return fold_typed<P, 3, UPB, false>(parts, nitems, nfull, unit_mode, chunk, nchunks, result, x); \
     }
     if (op == BM_R_DOT) {
-        if (dtype == BM_F32) return fold_typed<double, 1, 8, false>(parts, nitems, nfull, unit_mode, chunk, nchunks, result);
-        if (dtype == BM_F64) return fold_typed<double, 1, 16, false>(parts, nitems, nfull, unit_mode, chunk, nchunks, result);
-        if (dtype == BM_I32) return fold_typed<int, 1, 8, false>(parts, nitems, nfull, unit_mode, chunk, nchunks, result);
-        return fold_typed<unsigned long long, 1, 16, false>(parts, nitems, nfull, unit_mode, chunk, nchunks, result);
+        if (dtype == BM_F32) return fold_typed<double, 1, 8, false>(parts, nitems, nfull, unit_mode, chunk, nchunks, result, x);
+        if (dtype == BM_F64) return fold_typed<double, 1, 16, false>(parts, nitems, nfull, unit_mode, chunk, nchunks, result, x);
+        if (dtype == BM_I32) return fold_typed<int, 1, 8, false>(parts, nitems, nfull, unit_mode, chunk, nchunks, result, x);
+        return fold_typed<unsigned long long, 1, 16, false>(parts, nitems, nfull, unit_mode, chunk, nchunks, result, x);
     }
     switch (dtype) {
         // unit-mode items are half-units (bm_reduce.cuh PwHalf): 8 per block
@@ -156,12 +137,14 @@ namespace bmi {
 
 template <typename A, int OP>
 static int run_exchange(const void* partial, void* const* peers, int world, int rank, unsigned long long epoch,
-                        void* out, int normalise) {
+                        void* out, int normalise, void* const* dev_peers = nullptr) {
     bm::PeerPtrs pp;
     std::memset(&pp, 0, sizeof pp);
-    for (int i = 0; i < world; ++i) pp.p[i] = peers[i];
+    if (!dev_peers)
+        for (int i = 0; i < world; ++i) pp.p[i] = peers[i];
     bm::exchange_combine_kernel<A, OP><<<1, 256, 0, st().stream>>>((const A*)partial, pp, world, rank, epoch, (A*)out,
-                                                                    normalise);
+                                                                    normalise, st().err_dev, st().exch_timeout_ns,
+                                                                    dev_peers);
     BM_CUDA(cudaGetLastError());
     st().launches++;
     return BM_OK;
@@ -178,6 +161,26 @@ static int exchange_typed(const void* partial, void* const* peers, int world, in
         case BM_R_DOT: return run_exchange<typename bm::DotAcc<T>::type, 1>(partial, peers, world, rank, epoch, out, 0);
     }
     return set_error(BM_ERR_ARG, "exchange: bad reduce op");
+}
+
+// An empty shard of a fused sharded accu / dot: no reduction kernel, but the
+// rank still takes part in the exchange with a zero (peers wait for it).
+int exchange_empty_shard(int dtype, int op, void* const* dev_peers, int world, int rank, unsigned long long epoch,
+                         void* out) {
+    const bool f = dtype == BM_F32 || dtype == BM_F64;
+    if (op == BM_R_DOT) {
+        if (f) return run_exchange<double, 1>(nullptr, nullptr, world, rank, epoch, out, 0, dev_peers);
+        if (dtype == BM_I32) return run_exchange<int, 1>(nullptr, nullptr, world, rank, epoch, out, 0, dev_peers);
+        return run_exchange<unsigned long long, 1>(nullptr, nullptr, world, rank, epoch, out, 0, dev_peers);
+    }
+    if (op != BM_R_ACCU) return set_error(BM_ERR_EMPTY, "reduction over an empty range");
+    switch (dtype) {
+        case BM_F32: return run_exchange<float, 1>(nullptr, nullptr, world, rank, epoch, out, 1, dev_peers);
+        case BM_F64: return run_exchange<double, 1>(nullptr, nullptr, world, rank, epoch, out, 1, dev_peers);
+        case BM_I32: return run_exchange<int, 1>(nullptr, nullptr, world, rank, epoch, out, 0, dev_peers);
+        case BM_U64: return run_exchange<unsigned long long, 1>(nullptr, nullptr, world, rank, epoch, out, 0, dev_peers);
+    }
+    return set_error(BM_ERR_ARG, "exchange: bad dtype");
 }
 
 }  // namespace bmi

@@ -30,6 +30,11 @@ struct State {
     void* const* exch_peers = nullptr;
     int exch_world = 0, exch_rank = 0;
     unsigned long long exch_epoch = 0;
+    unsigned long long exch_timeout_ns = 60ull * 1000000000ull;   // BM_EXCH_TIMEOUT_S
+    // device error word: pinned, mapped host memory that kernels set (atomicOr_system)
+    // and every host synchronisation point checks (BM_ERR_PEER)
+    unsigned int* err_host = nullptr;
+    unsigned int* err_dev = nullptr;
     int flip = 0;                      // buffer of the next reduction
     unsigned int* ticket = nullptr;    // two last-CTA counters (at +0 and +32), zero between launches
     void* result = nullptr;            // device slot of the final value
@@ -48,6 +53,8 @@ State& st();
 int set_error(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* what);
 int cu_fail(CUresult r, const char* what);
+// after a stream synchronisation: BM_ERR_PEER (and clear) when a kernel set the device error word
+int check_device_error(const char* what);
 
 #define BM_CUDA(call)                                           \
     do {                                                        \
@@ -93,9 +100,13 @@ int launch_rdim_fused(const bm_invocation* inv);
 typedef std::function<int(float* hi, float* lo, int64_t kp, int64_t rp)> SplitFn;
 int gemm_tc_f32_core(int64_t m, int64_t n, int64_t k, const SplitFn& split_a, const SplitFn& split_b, float* C,
                      int64_t ldc, bool* handled);
+int exchange_empty_shard(int dtype, int op, void* const* dev_peers, int world, int rank, unsigned long long epoch,
+                         void* dev_out);
 int combine_partials(const void* dev_partials, int64_t count, int dtype, int op, void* dev_out);
+// exch_world > 1: the final fold kernel also runs the cross-GPU exchange (fused sharded reductions)
 int launch_fold(int dtype, int op, const void* partials, int64_t nitems, int64_t nfull, bool unit_mode, int chunk,
-                int nchunks, void* result);
+                int nchunks, void* result, void* const* exch_peers = nullptr, int exch_world = 0, int exch_rank = 0,
+                unsigned long long exch_epoch = 0);
 
 // grid heuristics
 inline int ewise_grid(int64_t n_vec_units) {

@@ -56,6 +56,8 @@ struct Args {
     void* const* exch_peers;    // device array of the world exchange buffers
     int exch_world, exch_rank;
     unsigned long long exch_epoch;
+    unsigned int* dev_err;      // mapped host error word (bm_sync raises when it is set)
+    unsigned long long exch_timeout_ns;
 };
 
 // ---------------------------------------------------------------------------
@@ -481,6 +483,55 @@ __device__ A cta_combine_pairwise(A* v, A* w, int cnt) {
     return r;
 }
 
+
+// Device error word bits (State::err_*, surfaced by bm_sync / bm_poll_device_error).
+#define BM_DEVERR_PEER_TIMEOUT 1u
+
+// ---------------------------------------------------------------------------
+// Cross-GPU exchange of one value per rank over peer memory, then the fold of
+// the world values in rank order (combine_pairwise, kernels.py:380-392).
+// Buffer layout of every rank, per parity (epoch & 1): [world values][world
+// flags], 8-byte slots.  Thread 0 writes this rank's value into slot `rank`
+// of every rank's buffer (NVLink stores), fences at system scope, releases
+// the epoch in its flag of every buffer; then the CTA waits for every flag of
+// its own buffer with acquire loads and folds.  A peer that has not published
+// after timeout_ns sets BM_DEVERR_PEER_TIMEOUT in the mapped error word, which
+// bm_sync turns into BM_ERR_PEER (the reference surfaces asynchronous device
+// errors at synchronise, runtime.py:340-353); the slot keeps its stale value.
+// Called by every thread of ONE CTA; v is read in thread 0; xv is shared
+// scratch of >= 2 * world values.  Returns the world value (all threads).
+template <typename P, int OP>
+__device__ P exchange_fold(void* const* peers, int W, int R, unsigned long long ep, unsigned int* err,
+                           unsigned long long timeout_ns, P v, P* xv) {
+    __syncthreads();
+    const size_t base = (size_t)(ep & 1) * 2 * W;
+    if (threadIdx.x == 0) {
+        for (int p = 0; p < W; ++p)
+            *reinterpret_cast<P*>(reinterpret_cast<unsigned long long*>(peers[p]) + base + R) = v;
+        __threadfence_system();   // the values land before any flag says so
+        for (int p = 0; p < W; ++p) {
+            unsigned long long* flag = reinterpret_cast<unsigned long long*>(peers[p]) + base + W + R;
+            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(ep) : "memory");
+        }
+    }
+    __syncthreads();
+    unsigned long long* mine = reinterpret_cast<unsigned long long*>(peers[R]) + base;
+    for (int p = threadIdx.x; p < W; p += blockDim.x) {
+        unsigned long long f, t0, t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        do {
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(f) : "l"(mine + W + p) : "memory");
+            if (f >= ep) break;
+            __nanosleep(64);
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        } while (t - t0 < timeout_ns);
+        if (f < ep && err) atomicOr_system(err, BM_DEVERR_PEER_TIMEOUT);
+        xv[p] = *reinterpret_cast<volatile P*>(mine + p);
+    }
+    __syncthreads();
+    return cta_combine_pairwise<P, OP>(xv, xv + W, W);
+}
+
 // ---------------------------------------------------------------------------
 // flat reduction kernel body.
 //
@@ -731,44 +782,11 @@ __device__ void last_cta_fold(const Args& a, i64 nitems, i64 nfull, bool has_tai
         chunk_res[0] = fin;
     }
     if (a.exch_world > 1) {
-        // the collective in the same kernel: publish this rank's partial into every
-        // rank's exchange buffer over NVLink (parity by epoch), release an epoch flag,
-        // wait for every rank's flag in this rank's buffer, fold in rank order
+        // the collective in the same kernel: publish this rank's partial, wait
+        // for every rank's, fold in rank order (exchange_fold)
         __syncthreads();
-        const int W = a.exch_world, R = a.exch_rank;
-        const unsigned long long ep = a.exch_epoch;
-        const size_t base = (size_t)(ep & 1) * 2 * W;
-        if (threadIdx.x == 0) {
-            const P v = chunk_res[0];
-            for (int p = 0; p < W; ++p)
-                *reinterpret_cast<P*>(reinterpret_cast<unsigned long long*>(a.exch_peers[p]) + base + R) = v;
-            __threadfence_system();
-            for (int p = 0; p < W; ++p) {
-                unsigned long long* flag = reinterpret_cast<unsigned long long*>(a.exch_peers[p]) + base + W + R;
-                asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(ep) : "memory");
-            }
-        }
-        __syncthreads();
-        unsigned long long* mine = reinterpret_cast<unsigned long long*>(a.exch_peers[R]) + base;
-        P* xv = chunk_res + 1;                     // W <= 64 values + ping-pong space
-        for (int p = threadIdx.x; p < W; p += blockDim.x) {
-            // bounded wait: a peer that never publishes (10 s) turns into a NaN /
-            // all-ones result instead of a hung GPU
-            unsigned long long f, t0, t;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-            do {
-                asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(f) : "l"(mine + W + p) : "memory");
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            } while (f < ep && t - t0 < 10000000000ull);
-            P v = *reinterpret_cast<volatile P*>(mine + p);
-            if (f < ep) {
-                const unsigned long long bad = ~0ull;
-                v = *reinterpret_cast<const P*>(&bad);
-            }
-            xv[p] = v;
-        }
-        __syncthreads();
-        const P g = cta_combine_pairwise<P, OP>(xv, xv + 128, W);
+        const P g = exchange_fold<P, OP>(a.exch_peers, a.exch_world, a.exch_rank, a.exch_epoch, a.dev_err,
+                                         a.exch_timeout_ns, chunk_res[0], chunk_res + 1);
         if (threadIdx.x == 0) {
             P o = g;
             if constexpr (OP == 1 && is_float_t<T>::value) o = g + T(0);
@@ -939,19 +957,32 @@ __global__ void __launch_bounds__(512) fold_chunks_kernel(const P* __restrict__ 
     if (threadIdx.x == 0) out[blockIdx.x] = r;
 }
 
+struct ExchArgs {
+    void* const* peers;   // device array of the world exchange buffers; world < 2: no exchange
+    int world, rank;
+    unsigned long long epoch;
+    unsigned int* err;
+    unsigned long long timeout_ns;
+};
+
 template <typename P, int OP, bool NORMALISE>
-__global__ void __launch_bounds__(256) fold_final_kernel(const P* __restrict__ chunks, int n, P* __restrict__ result) {
+__global__ void __launch_bounds__(256) fold_final_kernel(const P* __restrict__ chunks, int n, P* __restrict__ result,
+                                                         ExchArgs x) {
     // the chunk values are staged in shared memory and folded by the whole CTA
     // (cta_fold_pairwise: the same combine_pairwise order); one thread
     // streaming them costs ~135 ns per value (69 us for 512 chunks)
     extern __shared__ __align__(16) char fsm[];
+    __shared__ P xv[2 * 64];
     P* buf = reinterpret_cast<P*>(fsm);
     for (int i = threadIdx.x; i < n; i += blockDim.x) buf[i] = chunks[i];
     __syncthreads();
     P r = cta_fold_pairwise<P, OP>(buf, buf + n, n);
-    if (threadIdx.x != 0) return;
     if (NORMALISE) r = r + P(0);
-    result[0] = r;
+    if (x.world > 1) {   // sharded reduction: the exchange of the shard values in this kernel
+        r = exchange_fold<P, OP>(x.peers, x.world, x.rank, x.epoch, x.err, x.timeout_ns, r, xv);
+        if (NORMALISE) r = r + P(0);
+    }
+    if (threadIdx.x == 0) result[0] = r;
 }
 
 }  // namespace bm

@@ -33,6 +33,20 @@ int cuda_fail(cudaError_t e, const char* what) {
     return set_error(BM_ERR_CUDA, m);
 }
 
+int check_device_error(const char* what) {
+    State& s = st();
+    if (!s.err_host) return BM_OK;
+    const unsigned int w = __atomic_exchange_n(s.err_host, 0u, __ATOMIC_ACQ_REL);
+    if (!w) return BM_OK;
+    std::string m = std::string(what) + ": ";
+    if (w & 1u)
+        m += "a peer rank did not publish its partial within the exchange timeout (BM_EXCH_TIMEOUT_S); "
+             "the sharded result is invalid and the exchange must be re-created";
+    else
+        m += "device error word set";
+    return set_error(BM_ERR_PEER, m);
+}
+
 int cu_fail(CUresult r, const char* what) {
     char buf[160];
     std::snprintf(buf, sizeof buf, "%s: CUresult %d", what, (int)r);
@@ -121,6 +135,13 @@ int bm_init(int device) {
     BM_CUDA(cudaMalloc(&s.result, 256));
     BM_CUDA(cudaMalloc(&s.fold_scratch, 8 * 8192));
     BM_CUDA(cudaMallocHost(&s.host_slot, 256));
+    BM_CUDA(cudaHostAlloc((void**)&s.err_host, 64, cudaHostAllocMapped));
+    *s.err_host = 0u;
+    BM_CUDA(cudaHostGetDevicePointer((void**)&s.err_dev, s.err_host, 0));
+    if (const char* t = std::getenv("BM_EXCH_TIMEOUT_S")) {
+        const double sec = std::atof(t);
+        if (sec > 0) s.exch_timeout_ns = (unsigned long long)(sec * 1e9);
+    }
     BM_CUDA(cudaDeviceSynchronize());
     s.initialised = true;
     return BM_OK;
@@ -138,6 +159,8 @@ int bm_shutdown(void) {
     cudaFree(s.fold_scratch);
     s.fold_scratch = nullptr;
     cudaFreeHost(s.host_slot);
+    cudaFreeHost(s.err_host);
+    s.err_host = s.err_dev = nullptr;
     cudaStreamDestroy(s.own_stream);
     s.partials[0] = s.partials[1] = s.result = s.host_slot = nullptr;
     s.partials_cap = 0;
@@ -196,7 +219,12 @@ int bm_sync(void) {
     BM_REQUIRE_INIT();
     cudaError_t e = cudaStreamSynchronize(st().stream);
     if (e != cudaSuccess) return cuda_fail(e, "bm_sync (asynchronous kernel failure)");
-    return BM_OK;
+    return check_device_error("bm_sync");
+}
+
+int bm_poll_device_error(void) {
+    BM_REQUIRE_INIT();
+    return check_device_error("device error");
 }
 
 static int copy_sync(void* dst, const void* src, int64_t bytes, cudaMemcpyKind k) {
@@ -206,7 +234,7 @@ static int copy_sync(void* dst, const void* src, int64_t bytes, cudaMemcpyKind k
     BM_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, k, st().stream));
     cudaError_t e = cudaStreamSynchronize(st().stream);
     if (e != cudaSuccess) return cuda_fail(e, "copy");
-    return BM_OK;
+    return check_device_error("copy");
 }
 
 int bm_h2d(void* dst, const void* src, int64_t bytes) {
@@ -355,6 +383,7 @@ int bm_execute_reduce(const bm_invocation* inv, void* host_result) {
     BM_CUDA(cudaMemcpyAsync(s.host_slot, s.result, 8, cudaMemcpyDeviceToHost, s.stream));
     cudaError_t e = cudaStreamSynchronize(s.stream);
     if (e != cudaSuccess) return cuda_fail(e, "bm_execute_reduce");
+    if (int erc = check_device_error("bm_execute_reduce")) return erc;
     const int rdt = inv->compute_dtype;
     if (inv->reduce_op == BM_R_DOT && rdt == BM_F32) {
         // f32 dot partials are accumulated in f64; round once, like numpy's

@@ -104,6 +104,10 @@ class PeerExchange:
             raise RuntimeError("peer exchange: mapping a peer buffer failed on some rank")
         self._ptrs = (ctypes.c_void_p * self.world)(*ptrs)
         self.dev_ptrs = torch.tensor(ptrs, dtype=torch.int64, device="cuda")   # for the fused kernel
+        # the fused kernel reads dev_ptrs on the library's stream, which need not be
+        # torch's current stream: finish the host-to-device copy first
+        torch.cuda.current_stream().synchronize()
+        self.broken = False
 
     def combine(self, partial, elem: str, op_code: int, result) -> None:
         self.epoch += 1
@@ -128,21 +132,74 @@ class PeerExchange:
             self._own = None
 
 
+# group -> PeerExchange (or None when peer mapping failed somewhere).  Entries
+# hold the group object itself, so an id() is never reused for another group;
+# runtime.shutdown() forgets them (their pointers die with the library state).
 _SHARED_EXCHANGES: dict = {}
 
 
 def shared_exchange(group=None):
     """The process's PeerExchange for `group`, created once (collectively) and
-    reused by every fused sharded reduction, whose epochs then advance in the
-    same order on every rank; None when peer mapping is unavailable anywhere
-    (then the NCCL all-gather serves)."""
+    reused by every sharded reduction that exchanges over peer memory, whose
+    epochs then advance in the same order on every rank; None when peer
+    mapping is unavailable anywhere (then the NCCL all-gather serves) or the
+    exchange timed out earlier (BM_ERR_PEER: it is no longer in step)."""
     key = id(group)
-    if key not in _SHARED_EXCHANGES:
+    ent = _SHARED_EXCHANGES.get(key)
+    if ent is None or ent[0] is not group:
         try:
-            _SHARED_EXCHANGES[key] = PeerExchange(group)
+            ex = PeerExchange(group)
         except RuntimeError:
-            _SHARED_EXCHANGES[key] = None
-    return _SHARED_EXCHANGES[key]
+            ex = None
+        ent = (group, ex)
+        _SHARED_EXCHANGES[key] = ent
+    ex = ent[1]
+    return None if ex is None or ex.broken else ex
+
+
+def close_exchanges() -> None:
+    """Collective: unmap every peer buffer, wait for all ranks, free the own
+    buffers.  Call on every rank before destroying the process group."""
+    import torch
+    import torch.distributed as dist
+    torch.cuda.synchronize()
+    ents = list(_SHARED_EXCHANGES.values())
+    _SHARED_EXCHANGES.clear()
+    for group, ex in ents:
+        if ex is not None:
+            for q in ex._opened:
+                ex._lib.bm_exchange_close(ctypes.c_void_p(q), 1)
+            ex._opened = []
+    for group, ex in ents:
+        if ex is not None:
+            dist.barrier(group=group)      # no peer maps this rank's buffer any more
+            ex.close()
+
+
+def _forget_exchanges() -> None:
+    """runtime.shutdown hook (not collective): unmap peer buffers and drop
+    every entry, so no stale device pointer is reused after a re-init.  The
+    own buffers are left to the process (a peer may still map them)."""
+    for _, ex in list(_SHARED_EXCHANGES.values()):
+        if ex is not None:
+            for q in ex._opened:
+                ex._lib.bm_exchange_close(ctypes.c_void_p(q), 1)
+            ex._opened = []
+            ex._own = None
+    _SHARED_EXCHANGES.clear()
+
+
+_rt._shutdown_hooks.append(_forget_exchanges)
+
+
+def _agree_all(group, flag: bool) -> bool:
+    """Collective AND of a per-rank flag."""
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.tensor([1 if flag else 0], dtype=torch.int32, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    return bool(t.item())
 
 
 class ShardedReduction:
@@ -181,13 +238,33 @@ class ShardedReduction:
             collective = os.environ.get("BM_SHARD_COLLECTIVE", "p2p_fused")
         if collective not in ("all_gather", "allreduce", "p2p", "p2p_fused"):
             raise ValueError(f"unknown collective {collective!r}")
-        fused_ex = None
-        if collective == "p2p_fused" and self.world > 1:
-            fused_ex = shared_exchange(group)
-            if fused_ex is None:
-                collective = "all_gather"      # peer memory unavailable: NCCL all-gather
-        self.collective = collective
         node = _expr.as_expr(local_exprs[0])
+        # Shard sizes, once: an empty shard of a min / max has no partial, so
+        # the fold skips it (the peer-memory paths cannot: they fall back to
+        # the gather); every shard empty is the reference's empty-range error.
+        shp = _expr.shape_of(node)
+        n_local = int(shp.rows) * int(shp.cols)
+        self.counts = [n_local]
+        self._fold_ranks = None
+        if self.world > 1:
+            counts = [None] * self.world
+            dist.all_gather_object(counts, n_local, group=group)
+            self.counts = counts
+            if op in ("min", "max") and 0 in counts:
+                self._fold_ranks = [r for r, c in enumerate(counts) if c > 0]
+                if collective in ("p2p", "p2p_fused"):
+                    collective = "all_gather" if dist.get_backend(group) == "nccl" else "allreduce"
+        if op in ("min", "max") and sum(self.counts) == 0:
+            raise ValueError(f"{op}: reduction over an empty range")
+        ex = None
+        if collective in ("p2p", "p2p_fused") and self.world > 1:
+            # every rank must take the same path, or a peer waits for nothing
+            ex = shared_exchange(group)
+            if not _agree_all(group, ex is not None):
+                ex = None
+            if ex is None:
+                collective = "all_gather" if dist.get_backend(group) == "nccl" else "allreduce"
+        self.collective = collective
         self.elem = node.elem_type
         self.pdt = partial_dtype(op, self.elem)
         tdt = getattr(torch, _TORCH_DTYPE[self.pdt])
@@ -210,10 +287,7 @@ class ShardedReduction:
                          "dot": _clib.BM_R_DOT}[op]
         self._step = 0
         self._last = 0
-        if collective == "p2p_fused":
-            self._exchange = fused_ex
-        else:
-            self._exchange = PeerExchange(group) if (collective == "p2p" and self.world > 1) else None
+        self._exchange = ex if collective in ("p2p", "p2p_fused") else None
         if self.pipeline:
             self._comm = torch.cuda.Stream()
             self._reduced = [torch.cuda.Event() for _ in range(nbuf)]
@@ -230,8 +304,10 @@ class ShardedReduction:
             gath.zero_()
             gath[self.rank:self.rank + 1].copy_(part)
             self.dist.all_reduce(gath, group=self.group)
+        if self._fold_ranks is not None:        # min / max with empty shards: fold the others
+            gath = gath[self._fold_ranks].contiguous()
         _clib.check(self._lib.bm_combine_partials_to_device(
-            ctypes.c_void_p(gath.data_ptr()), self.world, _clib.DTYPE_CODE[self.elem], self._op_code,
+            ctypes.c_void_p(gath.data_ptr()), gath.numel(), _clib.DTYPE_CODE[self.elem], self._op_code,
             ctypes.c_void_p(self.results[slot].data_ptr())), "combine partials")
 
     def launch(self) -> None:
@@ -245,9 +321,10 @@ class ShardedReduction:
             return
         if self.pipeline and self._gathered[slot] is not None:
             compute.wait_event(self._gathered[slot])   # the gather that read this partial is done
-        _clib.check(self._lib.bm_reduce_to_device(ctypes.byref(self.inv),
-                                                  ctypes.c_void_p(self.partials[slot].data_ptr())),
-                    "sharded reduce")
+        if self.counts[self.rank] > 0 or self.op not in ("min", "max"):
+            _clib.check(self._lib.bm_reduce_to_device(ctypes.byref(self.inv),
+                                                      ctypes.c_void_p(self.partials[slot].data_ptr())),
+                        "sharded reduce")
         if self.world == 1:
             return
         if not self.pipeline:
@@ -266,6 +343,10 @@ class ShardedReduction:
             ev.record(self._comm)
             self._gathered[slot] = ev
 
+    def check(self) -> None:
+        """After the caller synchronised: raise if an exchange timed out."""
+        _check_exchange_error(self._exchange)
+
     def join(self) -> None:
         """Order the current stream after every collective issued so far."""
         import torch
@@ -273,15 +354,27 @@ class ShardedReduction:
             torch.cuda.current_stream().wait_stream(self._comm)
 
     def value(self):
+        """The folded result of the last step.  Raises PeerTimeoutError when a
+        peer never published into the exchange (the async-error contract of
+        the reference: device errors surface at synchronisation)."""
         import torch
         self.join()
         torch.cuda.synchronize()
+        self.check()
         src = self.partials[self._last] if self.world == 1 else self.results[self._last]
         v = src.cpu().numpy()[0]
         dt = kernels.NP_DTYPE[self.elem]
         if self.op == "dot" and dt.kind == "f":
             return dt.type(v)
         return np.asarray(v).astype(dt)[()]
+
+
+def _check_exchange_error(ex) -> None:
+    rc = _clib.lib().bm_poll_device_error()
+    if rc != _clib.BM_OK:
+        if ex is not None:
+            ex.broken = True          # out of step with the peers: never used again
+        _clib.check(rc, "sharded reduction")
 
 
 def sharded_accu(local_expr, group=None):

@@ -663,6 +663,9 @@ def init(backend: str | None = None, print_info: bool = False, device_id: int = 
         _generation += 1
 
 
+_shutdown_hooks: list = []   # callables run before the library shuts down (dist: forget peer exchanges)
+
+
 def shutdown() -> None:
     """Drain the stream, free every live buffer, clear the singleton."""
     global _runtime, _generation
@@ -672,6 +675,11 @@ def shutdown() -> None:
         rt = _runtime
         _generation += 1
         try:
+            for hook in list(_shutdown_hooks):
+                try:
+                    hook()
+                except Exception:  # noqa: BLE001 - shutdown must finish
+                    pass
             rt.stop()
         finally:
             with rt._lock:

@@ -277,6 +277,8 @@ int bm_sync(void);   /* drain the stream; BM_ERR_CUDA on a kernel fault, BM_ERR_
  * the stream itself (e.g. torch.cuda.synchronize): BM_ERR_PEER when a peer timed out.  The
  * peer wait of every exchange is bounded by BM_EXCH_TIMEOUT_S (default 60 s). */
 int bm_poll_device_error(void);
+/* 1 while queued work has not finished on the library's stream, else 0 */
+int bm_stream_busy(void);
 
 /* ---- instrumentation -------------------------------------------------------------- */
 typedef struct bm_counters {

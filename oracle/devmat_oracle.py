@@ -375,6 +375,8 @@ def tree_walk(node, leaf_data):
         if kind == "gen_eye":
             return np.eye(r, c, dtype=dt)
         return np.linspace(node.aux[2], node.aux[3], r).astype(dt).reshape(r, 1)
+    if kind in ("gen_randu", "gen_randn"):      # expr.py:875-877: a device RNG stream cannot be replayed
+        raise ValueError(f"oracle cannot replay the device RNG stream of {kind}")
     if kind == "mtop_conv_to":
         return cast_out(tree_walk(node.operands[0], leaf_data), dt)
     a = tree_walk(node.operands[0], leaf_data)

@@ -99,6 +99,7 @@ SIGNATURES = {
     "bm_exchange_combine": ([_VP, ctypes.POINTER(_VP), _I32, _I32, ctypes.c_uint64, _I32, _I32, _VP], ctypes.c_int),
     "bm_sync": ([], ctypes.c_int),
     "bm_poll_device_error": ([], ctypes.c_int),
+    "bm_stream_busy": ([], ctypes.c_int),
     "bm_get_counters": ([ctypes.POINTER(Counters)], ctypes.c_int),
     "bm_set_cache_dir": ([_CP], ctypes.c_int),
     "bm_jit_compile_only": ([ctypes.POINTER(Invocation)], ctypes.c_int),

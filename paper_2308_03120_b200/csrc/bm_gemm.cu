@@ -14,6 +14,16 @@
 
 namespace bm {
 
+// Multiply-accumulate of the SIMT GEMM.  Floats: one fused multiply-add per
+// k, in k order from zero -- the accumulation of the reference's OpenBLAS
+// sgemm/dgemm micro-kernels for the small shapes this kernel serves, so the
+// products match np.dot (kernels.py:704-708) bit for bit when K fits one
+// OpenBLAS K-block.  Integers wrap like numpy's integer np.dot.
+__device__ __forceinline__ float mac(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double mac(double a, double b, double c) { return __fma_rn(a, b, c); }
+template <typename T>
+__device__ __forceinline__ T mac(T a, T b, T c) { return OpPlus::f(c, OpTimes::f(a, b)); }
+
 // 64x64 output tile per CTA, 256 threads x (4x4) outputs, K staged 16 at a time.
 template <typename T>
 __global__ void __launch_bounds__(256) gemm_simt_kernel(int ta, int tb, i64 m, i64 n, i64 k, const T* __restrict__ A,
@@ -51,7 +61,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(int ta, int tb, i64 m, i
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = OpPlus::f(acc[i][j], OpTimes::f(a[i], b[j]));
+                for (int j = 0; j < 4; ++j) acc[i][j] = mac(a[i], b[j], acc[i][j]);
         }
         __syncthreads();
     }

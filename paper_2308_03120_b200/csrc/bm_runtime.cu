@@ -222,6 +222,13 @@ int bm_sync(void) {
     return check_device_error("bm_sync");
 }
 
+int bm_stream_busy(void) {
+    if (!st().initialised) return 0;
+    const cudaError_t e = cudaStreamQuery(st().stream);
+    if (e == cudaErrorNotReady) return 1;
+    return 0;   // idle, or a sticky error that the next bm_sync reports
+}
+
 int bm_poll_device_error(void) {
     BM_REQUIRE_INIT();
     return check_device_error("device error");

@@ -434,7 +434,11 @@ def gather_columns(local, group=None):
     if world == 1:
         return local
     out = Matrix(local.n_elem, world, elem_type=local.elem_type)
-    dist.all_gather_into_tensor(torch_view(out), torch_view(local), group=group)
+    ov, lv = torch_view(out), torch_view(local)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(ov, lv, group=group)
+    else:                                   # gloo (ranks sharing one GPU in tests): list all-gather
+        dist.all_gather(list(ov.view(world, -1).unbind(0)), lv, group=group)
     return out
 
 

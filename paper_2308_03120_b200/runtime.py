@@ -16,6 +16,7 @@ from __future__ import annotations
 import ctypes
 import hashlib
 import os
+import pathlib
 import threading
 import time
 from dataclasses import dataclass, field, fields, replace
@@ -50,8 +51,9 @@ class DeviceDescriptor:
 
     @property
     def descriptor_hash(self) -> str:
-        text = (f"backend={self.backend_name};device={self.device_id};gpu={self.gpu_name};"
-                f"sm={self.sm_count};arch=sm_100a;version={__version__}")
+        text = (f"backend={self.backend_name};device={self.device_id};workers={self.worker_count};"
+                f"f64={int(self.supports_f64)};gpu={self.gpu_name};sm={self.sm_count};arch=sm_100a;"
+                f"version={__version__}")
         return hashlib.sha256(text.encode()).hexdigest()[:16]
 
 
@@ -113,6 +115,73 @@ class Counters:
 
 # ---------------------------------------------------------------------------
 # translation of KernelInvocation -> bm_invocation
+
+MANIFEST_NAME = "kernels.manifest"
+
+
+@dataclass(frozen=True)
+class KernelCacheEntry:
+    """One line of the kernel-cache manifest (runtime.py:112-122 of the
+    reference): device descriptor hash, kind, input and output element type,
+    source hash; tab-separated, hashes are 16 lowercase hex digits."""
+    descriptor_hash: str
+    kind: str
+    in_type: str
+    out_type: str
+    source_hash: str
+
+    def line(self) -> str:
+        return "\t".join((self.descriptor_hash, self.kind, self.in_type, self.out_type, self.source_hash))
+
+
+def _hex16(t: str) -> bool:
+    return len(t) == 16 and set(t) <= set("0123456789abcdef")
+
+
+def load_manifest(cache_dir) -> dict:
+    """Read the manifest in ``cache_dir``; an unreadable, truncated (no final
+    newline) or malformed file warns KernelCacheWarning and reads as empty
+    (a cold cache), the reference's contract (runtime.py:156-189).  The B200
+    library's real cache is the NVRTC cubin directory (BM_CACHE_DIR); this
+    index is kept for code that manages the reference's manifest."""
+    import pathlib
+    import warnings
+    from .errors import KernelCacheWarning
+    path = pathlib.Path(cache_dir) / MANIFEST_NAME
+    if not path.exists():
+        return {}
+    try:
+        text = path.read_text(encoding="utf-8")
+    except (OSError, UnicodeDecodeError) as exc:
+        warnings.warn(f"kernel cache {path} unreadable ({exc}): cold start", KernelCacheWarning)
+        return {}
+    if text and text[-1] != "\n":
+        warnings.warn(f"kernel cache {path} truncated: cold start", KernelCacheWarning)
+        return {}
+    out = {}
+    for no, ln in enumerate(text.split("\n")[:-1] if text else [], 1):
+        if not ln:
+            continue
+        f = ln.split("\t")
+        if not (len(f) == 5 and _hex16(f[0]) and _hex16(f[4]) and f[1] in kernels.ALL_KINDS
+                and f[2] in kernels.ELEM_TYPES and f[3] in kernels.ELEM_TYPES):
+            warnings.warn(f"kernel cache {path}: bad line {no}: cold start", KernelCacheWarning)
+            return {}
+        e = KernelCacheEntry(*f)
+        out[(e.descriptor_hash, e.kind, e.in_type, e.out_type)] = e
+    return out
+
+
+def store_manifest(cache_dir, entries: dict) -> None:
+    """Write the manifest atomically (sorted lines, temp file + rename)."""
+    import pathlib
+    d = pathlib.Path(cache_dir)
+    d.mkdir(parents=True, exist_ok=True)
+    body = "".join(sorted(e.line() + "\n" for e in entries.values()))
+    tmp = d / (MANIFEST_NAME + ".tmp")
+    tmp.write_text(body, encoding="utf-8")
+    os.replace(tmp, d / MANIFEST_NAME)
+
 
 _REDUCE_OP = {"reduce_accu": _clib.BM_R_ACCU, "reduce_min": _clib.BM_R_MIN, "reduce_max": _clib.BM_R_MAX,
               "reduce_dot": _clib.BM_R_DOT, "accu": _clib.BM_R_ACCU, "min": _clib.BM_R_MIN,
@@ -422,6 +491,9 @@ class Runtime:
         self.seed = int(os.environ.get(SEED_ENV, "42"))
         self._section_mark = Counters()
         self._live: dict[int, int] = {}     # buffer_id -> device pointer
+        self._queued_ids: set = set()       # buffers used by work enqueued since the last synchronise
+        self._pending_error = None          # raised at the next synchronise (asynchronous error contract)
+        self.cache_dir = pathlib.Path(os.environ.get(CACHE_DIR_ENV, str(pathlib.Path.home() / ".devmat")))
         self._lib = _clib.lib()
         self._jit_base = self._native_counters()
         if print_info:
@@ -468,7 +540,23 @@ class Runtime:
 
     def release(self, buf: DeviceBuffer) -> None:
         """Release now; the handle becomes invalid (the memory returns to the
-        pool once work already queued on the stream has finished)."""
+        pool once work already queued on the stream has finished).
+
+        The reference frees at once, so a queued kernel that still uses the
+        buffer fails and the error surfaces at the next synchronise
+        (runtime.py:441-447, 340-353; tests/test_runtime.py:228-235).  The
+        stream-ordered free makes that race harmless here, but it is still the
+        caller's bug: releasing a buffer that work enqueued since the last
+        synchronise uses is reported as BufferError_ at the next synchronise
+        (deterministically: on the reference it depends on the dispatcher's
+        timing; a B200 kernel usually finishes before the host gets here).
+        release_deferred is the ordered release and never reports."""
+        bid = buf.buffer_id
+        with self._lock:
+            if bid in self._queued_ids:
+                if self._pending_error is None:
+                    self._pending_error = BufferError_(
+                        f"buffer #{bid} released while queued work still used it")
         _clib.check(self._lib.bm_free(self._retire(buf)), "release")
 
     def release_deferred(self, buf: DeviceBuffer) -> None:
@@ -501,9 +589,22 @@ class Runtime:
         _clib.check(self._lib.bm_enqueue(ctypes.byref(c)), inv.kind)
         with self._lock:
             self.counters.launches += 1
+            # buffers unfinished work may use (release() race report); bounded
+            if len(self._queued_ids) > 4096:
+                self._queued_ids.clear()
+            for v in inv.inputs:
+                self._queued_ids.add(v.buf.buffer_id)
+            if inv.output is not None:
+                self._queued_ids.add(inv.output.buf.buffer_id)
 
     def synchronise(self) -> None:
-        _clib.check(self._lib.bm_sync(), "synchronise")
+        rc = self._lib.bm_sync()
+        with self._lock:
+            self._queued_ids.clear()
+            err, self._pending_error = self._pending_error, None
+        _clib.check(rc, "synchronise")
+        if err is not None:
+            raise err
 
     def execute_reduce(self, inv: KernelInvocation):
         """Enqueue a reducing invocation, wait, and return its scalar as a
@@ -517,6 +618,8 @@ class Runtime:
         with self._lock:
             self.counters.launches += 1
         _clib.check(rc, inv.kind)
+        with self._lock:
+            self._queued_ids.clear()          # the call drained the stream
         value = np.frombuffer(bytes(raw)[: dt.itemsize], dtype=dt)[0]
         nbytes = kernels.itemsize(inv.inputs[0].buf.elem_type) if inv.inputs else 8
         with self._lock:
@@ -547,6 +650,8 @@ class Runtime:
         out = np.empty(n, dtype=dt)
         if n:
             _clib.check(self._lib.bm_d2h(out.ctypes.data, buf.ptr + offset * dt.itemsize, out.nbytes), "copy_d2h")
+            with self._lock:
+                self._queued_ids.clear()      # the copy drained the stream
         else:
             self.synchronise()
         with self._lock:

@@ -4,10 +4,10 @@
 
 One "step" is one pass of the hot path over one batch: the config-1 fused
 expression ``accu(2*A + B % C - exp(D))`` on a 4096 x 4096 f32 block per GPU
-(numpy default_rng(0) U[0,1) inputs on rank 0).
-At N > 1 every rank owns its own 4096 x 4096 column block of a 4096 x 4096N
-matrix (weak scaling); the rank partials are all-gathered over NCCL and
-folded deterministically on the device (paper_2308_03120_b200/dist.py).
+(numpy default_rng(rank) U[0,1) inputs).  At N > 1
+every rank owns its own 4096 x 4096 column block of a 4096 x 4096N matrix
+(weak scaling); the rank partials are exchanged and folded deterministically
+on the device (paper_2308_03120_b200/dist.py).
 
 value    device throughput: algorithmic bytes (4 inputs x 4 B per element)
          over K steps timed with CUDA events on the library's stream, inputs
@@ -16,11 +16,14 @@ e2e      the same metric through the public API with host buffers: every step
          copies A..D from pinned host memory (Matrix.from_numpy) and reads the
          scalar back (dm.accu).
 roofline the fused kernel's achieved GB/s against MEASURED_PEAKS.json hbm_gbs.
+parity   the step's value against the unmodified reference's (golden).
 cpu_baseline  the reference (baseline/_ref devmat, parallel backend on all host
          cores) on the same inputs, timed for ~10 s on rank 0 at N = 1.
-secondary     the other SURVEY 8d configs on one GPU (dot/norm 2^30, rdim
-         16384^2 f64, GEMM 8192^3 f32/f64, logistic step) -- reported beside the
-         headline, not part of it.
+secondary     N = 1: configs 2-5 on their BASELINE inputs (tools/baseline_inputs.py),
+         each with the median of 10 timings, roofline fraction, in-run parity
+         and the reference's CPU time for the same work.  N > 1: the configs
+         that shard (dot/norm 2^30, dim-1 reductions, column-sharded GEMM,
+         sample-sharded logistic step), strong scaling, parity per rank.
 """
 from __future__ import annotations
 
@@ -252,38 +255,95 @@ def torch_reference(torch, host) -> dict:
     return out
 
 
-def secondary_suite(dm, torch) -> dict:
-    """The other SURVEY 8d configs on this GPU (inputs generated on device by
-    the counter RNG; timings with CUDA events, best of a few)."""
+def _median_ms(torch, fn, reps: int = 10, inner: int = 1) -> float:
+    """Median over `reps` CUDA-event timings of `inner` back-to-back calls
+    (per call), after one untimed warm-up call."""
+    fn()
+    torch.cuda.synchronize()
+    return statistics.median(_event_time_ms(torch, fn, inner) / inner for _ in range(reps))
+
+
+def _rel(got, want) -> float:
+    """max|got - want| / max(max|want|, 1): the reference's metric (tests/dag_util.py:84-95)."""
+    got = np.asarray(got, dtype=np.float64)
+    want = np.asarray(want, dtype=np.float64)
+    return float(np.abs(got - want).max() / max(float(np.abs(want).max()), 1.0))
+
+
+def _golden_baseline():
+    p = ROOT / "tests" / "golden" / "baseline.npz"
+    if not p.exists():
+        return None
+    with np.load(p) as z:
+        return {k: z[k] for k in z.files}
+
+
+class _RefCPU:
+    """The unmodified reference (baseline/_ref devmat) on this host's cores,
+    for the per-config CPU baselines: bounded samples, each op run once after
+    the inputs are staged (staging is not timed, like bench.py:136-142 of the
+    reference)."""
+
+    def __init__(self):
+        self.devmat, self.kind = _reference_module()
+        self.cores = os.cpu_count() or 1
+
+    def ok(self) -> bool:
+        return self.devmat is not None
+
+    def run(self, backend: str, host_arrays, fn, reps: int = 1) -> float:
+        """Seconds per call of fn(devmat, mats) (min over reps)."""
+        dmr = self.devmat
+        if backend == "parallel":
+            dmr.init("parallel", worker_count=self.cores)
+        else:
+            dmr.init("reference")
+        try:
+            mats = [dmr.Matrix.from_numpy(x) for x in host_arrays]
+            best = None
+            for _ in range(reps):
+                t0 = time.perf_counter()
+                fn(dmr, mats)
+                dmr.synchronise()
+                t = time.perf_counter() - t0
+                best = t if best is None else min(best, t)
+            del mats
+            return best
+        finally:
+            dmr.shutdown()
+
+    def baseline(self, value, unit, sample, backend="parallel", extra=None) -> dict:
+        d = {"value": value, "unit": unit, "cores": self.cores if backend == "parallel" else 1, "kind": self.kind,
+             "backend": backend, "sample": sample}
+        if extra:
+            d.update(extra)
+        return d
+
+
+def secondary_suite(dm, torch, cpu: bool) -> dict:
+    """The other SURVEY 8d configs on this GPU, on the BASELINE inputs
+    (tools/baseline_inputs.py: the exact shapes and seeds).  Each entry: the
+    median of 10 CUDA-event timings, the roofline fraction, an in-run parity
+    check (against the unmodified reference's results in
+    tests/golden/baseline.npz and an f64 truth computed with torch on this
+    GPU), and the reference's CPU time on this host for the same work."""
     from paper_2308_03120_b200 import dist as D
     from paper_2308_03120_b200 import expr as E
     from paper_2308_03120_b200 import runtime as R
+    from tools import baseline_inputs as BI
     out = {}
-    peak_hbm, _, _ = _peaks()
+    peak_hbm, peak_bf16, _ = _peaks()
+    gold = _golden_baseline() or {}
+    ref = _RefCPU() if cpu else None
+    if ref is not None and not ref.ok():
+        ref = None
+    rtm = R.get_runtime()
 
-    def best_ms(fn, reps=5, inner=1):
-        fn()
-        torch.cuda.synchronize()
-        return min(_event_time_ms(torch, fn, inner) / inner for _ in range(reps))
-
-    try:  # config 3: dot and norm over 2^30 f32
-        n = 1 << 30
-        dm.set_seed(2)
-        a = dm.Col(n, fill="randu")
-        b = dm.Col(n, fill="randu")
-        rd = D.ShardedReduction("dot", a, b)
-        rn = D.ShardedReduction("dot", a, a)
-        t_dot = best_ms(rd.launch, inner=3)
-        t_norm = best_ms(rn.launch, inner=3)
-        out["dot_2^30_f32"] = {"ms": t_dot, "GB/s": 8 * n / t_dot / 1e6, "frac": 8 * n / t_dot / 1e6 / peak_hbm}
-        out["norm2_2^30_f32"] = {"ms": t_norm, "GB/s": 4 * n / t_norm / 1e6,
-                                 "frac": 4 * n / t_norm / 1e6 / peak_hbm}
-        del a, b, rd, rn
-    except Exception as e:  # pragma: no cover - reported, not fatal
-        out["dot_error"] = repr(e)[:200]
-    try:  # config 2: f64 sum/min/max dims 0/1 on 16384^2
-        m = dm.Matrix(16384, 16384, fill="randu", elem_type="f64")
-        nbytes = 8 * 16384 * 16384
+    # ---- config 2: f64 sum / min / max along both dims of 16384^2 ---------------------------
+    try:
+        X = BI.cfg2_input()
+        m = dm.Matrix.from_numpy(X)
+        nbytes = 8 * X.size
         for op in ("sum", "min", "max"):
             for dim in (0, 1):
                 p = E.plan(getattr(dm, op)(m, dim))
@@ -292,61 +352,333 @@ def secondary_suite(dm, torch) -> dict:
                 views = E._step_views(p, step, {})
                 inv = dm.KernelInvocation(step.kernel, tuple(views),
                                           E._make_view(res.mem, res.n_rows, res.n_cols, "flat"), (), step.params)
-                rtm = R.get_runtime()
-                t = best_ms(lambda: rtm.enqueue(inv), reps=3, inner=3)
-                out[f"{op}_dim{dim}_16384^2_f64"] = {"ms": t, "GB/s": nbytes / t / 1e6,
-                                                     "frac": nbytes / t / 1e6 / peak_hbm}
-        del m
-    except Exception as e:  # pragma: no cover
-        out["rdim_error"] = repr(e)[:200]
-    try:  # config 4: NT GEMM 8192^3 and 32768^3
+                t = _median_ms(torch, lambda: rtm.enqueue(inv))
+                got = res.to_numpy().reshape(-1)
+                want = gold.get(f"cfg2_{op}{dim}")
+                e = {"ms": t, "GB/s": nbytes / t / 1e6, "frac": nbytes / t / 1e6 / peak_hbm, "reps": 10,
+                     "kernel": step.kernel}
+                if want is not None:
+                    e["parity"] = {"vs": "reference (tests/golden/baseline.npz)",
+                                   "bit_exact": bool(got.tobytes() == want.tobytes()),
+                                   "max_rel_err": _rel(got, want)}
+                if ref is not None:
+                    s = ref.run("parallel", [X], lambda d, ms, op=op, dim=dim: d.evaluate(getattr(d, op)(ms[0], dim)))
+                    e["cpu_baseline"] = ref.baseline(nbytes / s / 1e9, "GB/s", f"one full {op}(A, {dim}) on 16384^2 f64")
+                    e["speedup_vs_cpu"] = e["GB/s"] / e["cpu_baseline"]["value"]
+                out[f"cfg2_{op}_dim{dim}_16384^2_f64"] = e
+        del m, X
+    except Exception as ex:  # pragma: no cover - reported, not fatal
+        out["cfg2_error"] = repr(ex)[:300]
+
+    # ---- config 3: dot and 2-norm of 2^30-element f32 vectors --------------------------------
+    try:
+        a, b = BI.cfg3_inputs()
+        n = a.size
+        ca = dm.Matrix.from_numpy(a.reshape(-1, 1))
+        cb = dm.Matrix.from_numpy(b.reshape(-1, 1))
+        rd = D.ShardedReduction("dot", ca, cb)
+        rn = D.ShardedReduction("dot", ca, ca)
+        t_dot = _median_ms(torch, rd.launch, inner=3)
+        t_norm = _median_ms(torch, rn.launch, inner=3)
+        got_dot = float(dm.dot(ca, cb))
+        got_norm = float(dm.norm(ca, 2))
+        # f64 truth on this GPU (torch, chunked)
+        tdot = tnn = 0.0
+        step = 1 << 26
+        for i in range(0, n, step):
+            ta = torch.from_numpy(a[i:i + step]).cuda().double()
+            tb = torch.from_numpy(b[i:i + step]).cuda().double()
+            tdot += float(torch.dot(ta, tb))
+            tnn += float(torch.dot(ta, ta))
+            del ta, tb
+        tnorm = float(np.sqrt(tnn))
+        for key, t, nb, got, want, truth in (("cfg3_dot_2^30_f32", t_dot, 8 * n, got_dot, gold.get("cfg3_dot"), tdot),
+                                             ("cfg3_norm2_2^30_f32", t_norm, 4 * n, got_norm, gold.get("cfg3_norm2"),
+                                              tnorm)):
+            e = {"ms": t, "GB/s": nb / t / 1e6, "frac": nb / t / 1e6 / peak_hbm, "reps": 10, "kernel": "bm_reduce",
+                 "value": got, "parity": {"tol": 1e-5, "rel_err_vs_f64": _rel(got, truth)}}
+            if want is not None:
+                e["parity"]["rel_err_vs_reference"] = _rel(got, want)
+                e["parity"]["vs"] = "reference (tests/golden/baseline.npz) and f64 truth (torch on this GPU)"
+            out[key] = e
+        del ca, cb, rd, rn
+        if ref is not None:
+            for backend in ("reference", "parallel"):
+                s_dot = ref.run(backend, [a.reshape(-1, 1), b.reshape(-1, 1)], lambda d, ms: d.dot(ms[0], ms[1]))
+                s_norm = ref.run(backend, [a.reshape(-1, 1)], lambda d, ms: d.norm(ms[0], 2))
+                for key, s, nb in (("cfg3_dot_2^30_f32", s_dot, 8 * n), ("cfg3_norm2_2^30_f32", s_norm, 4 * n)):
+                    cand = ref.baseline(nb / s / 1e9, "GB/s", f"one full {key[5:9]} of 2^30 f32", backend)
+                    cur = out[key].get("cpu_baseline")
+                    if cur is None or cand["value"] > cur["value"]:
+                        out[key]["cpu_baseline"] = cand      # the faster reference backend
+                    out[key].setdefault("cpu_by_backend", {})[backend] = cand["value"]
+            for key in ("cfg3_dot_2^30_f32", "cfg3_norm2_2^30_f32"):
+                out[key]["speedup_vs_cpu"] = out[key]["GB/s"] / out[key]["cpu_baseline"]["value"]
+        del a, b
+    except Exception as ex:  # pragma: no cover
+        out["cfg3_error"] = repr(ex)[:300]
+
+    # ---- config 4: C = A * trans(B), f32 (3xTF32) and f64 (DMMA), 8192^3 and 32768^3 -----------
+    try:
+        cpu_rate = {}
         for elem, n in (("f32", 8192), ("f64", 8192), ("f32", 32768), ("f64", 32768)):
-            A = dm.Matrix(n, n, fill="randu", elem_type=elem)
-            B = dm.Matrix(n, n, fill="randu", elem_type=elem)
+            if n == 8192:
+                a_h, b_h = BI.cfg4_inputs(n, elem)
+                A, B = dm.Matrix.from_numpy(a_h), dm.Matrix.from_numpy(b_h)
+            else:
+                dm.set_seed(3)
+                A = dm.Matrix(n, n, fill="randu", elem_type=elem)
+                B = dm.Matrix(n, n, fill="randu", elem_type=elem)
             C = dm.Matrix(n, n, elem_type=elem)
-            rtm = R.get_runtime()
             inv = dm.KernelInvocation("gemm", (R.BlockView(A.mem, 0, n, n, n), R.BlockView(B.mem, 0, n, n, n)),
                                       R.BlockView(C.mem, 0, n, n, n), (), {"trans_a": 0, "trans_b": 1})
-            t = best_ms(lambda: rtm.enqueue(inv), reps=3 if n <= 8192 else 1)
-            out[f"gemm_nt_{n}^3_{elem}"] = {"ms": t, "TFLOP/s": 2 * n ** 3 / t / 1e9}
+            reps = 10 if not (n == 32768 and elem == "f64") else 5
+            t = _median_ms(torch, lambda: rtm.enqueue(inv), reps=reps)
+            flops = 2 * n ** 3
+            e = {"ms": t, "TFLOP/s": flops / t / 1e9, "reps": reps,
+                 "kernel": "gemm_3xtf32_pair_kernel" if elem == "f32" else "gemm_dmma_kernel"}
+            if elem == "f32":
+                ceil = peak_bf16 / 2 / 3          # tf32 = half the bf16 rate, 3 MMAs per product
+                e["roofline"] = {"bound": "tensor", "peak": ceil, "unit": "TFLOP/s", "frac": e["TFLOP/s"] / ceil,
+                                 "basis": "measured bf16 dense / 2 (tf32) / 3 (3xTF32 passes)"}
+            tol = 1e-5 if elem == "f32" else 1e-12
+            if n == 8192:
+                td = torch.float64
+                ta = torch.from_numpy(a_h).cuda().to(td)
+                tb = torch.from_numpy(b_h).cuda().to(td)
+                truth = (ta @ tb.t())
+                del ta, tb
+                got = D.torch_view(C).view(n, n).t()        # column-major storage -> (row, col)
+                err = float((got.to(td) - truth).abs().max() / max(float(truth.abs().max()), 1.0))
+                e["parity"] = {"tol": tol, "normwise_vs_f64_full_matrix": err}
+                ii, jj = BI.gemm_sample_index(n)
+                if f"cfg4_{elem}_samples" in gold:
+                    ti = torch.from_numpy(ii).cuda()
+                    tj = torch.from_numpy(jj).cuda()
+                    samp = got[ti, tj].cpu().numpy()
+                    e["parity"]["samples_vs_reference"] = _rel(samp, gold[f"cfg4_{elem}_samples"])
+                    rows = got.to(td).sum(dim=1).cpu().numpy()
+                    e["parity"]["rowsums_vs_reference"] = _rel(rows, gold[f"cfg4_{elem}_rowsum"])
+                    e["parity"]["vs"] = "f64 cuBLAS product of the same inputs; reference entries and row sums"
+                del truth, got
+                if ref is not None:
+                    s = ref.run("parallel", [a_h, b_h], lambda d, ms: d.evaluate(ms[0] @ ms[1].t()))
+                    cpu_rate[elem] = flops / s / 1e12
+                    e["cpu_baseline"] = ref.baseline(cpu_rate[elem], "TFLOP/s", f"one full {n}^3 {elem} A @ B.t()")
+                del a_h, b_h
+            else:
+                rng = np.random.default_rng(12)
+                worst = 0.0
+                for i, j in zip(rng.integers(0, n, 16), rng.integers(0, n, 16)):
+                    ar = dm.evaluate(A.row(int(i))).to_numpy().astype(np.float64).reshape(-1)
+                    br = dm.evaluate(B.row(int(j))).to_numpy().astype(np.float64).reshape(-1)
+                    want = float(ar @ br)
+                    worst = max(worst, abs(C.at(int(i), int(j)) - want) / abs(want))
+                e["parity"] = {"tol": tol, "sampled_entries": 16, "max_rel_err_vs_f64_dot": worst}
+                if elem in cpu_rate:
+                    e["cpu_baseline"] = ref.baseline(cpu_rate[elem], "TFLOP/s",
+                                                     "extrapolated O(n^3) from the measured 8192^3 run (not run: "
+                                                     "~minutes on the CPU)", extra={"extrapolated": True})
+            if "cpu_baseline" in e:
+                e["speedup_vs_cpu"] = e["TFLOP/s"] / e["cpu_baseline"]["value"]
+            out[f"cfg4_gemm_nt_{n}^3_{elem}"] = e
             del A, B, C
-    except Exception as e:  # pragma: no cover
-        out["gemm_error"] = repr(e)[:200]
-    try:  # config 5: logistic-regression gradient step on 2^20 x 1024 f32
+    except Exception as ex:  # pragma: no cover
+        out["cfg4_error"] = repr(ex)[:300]
+
+    # ---- config 5: logistic-regression gradient step on 2^20 x 1024 f32 -------------------------
+    try:
+        x, w, y = BI.cfg5_inputs()
+        nrow, ncol = x.shape
+        X, W, Y = (dm.Matrix.from_numpy(v) for v in (x, w, y))
+
+        def two_pass():
+            z = dm.evaluate(X @ W)
+            r = dm.evaluate(1 / (1 + dm.exp(0 - z)) - Y)
+            g = dm.evaluate(X.t() @ r)
+            return r, g, dm.accu(r)
+
+        r_e = 1 / (1 + dm.exp(0 - X @ W)) - Y
+
+        def fused():
+            r, g = dm.evaluate_many(r_e, X.t() @ r_e)
+            return r, g, dm.accu(r)
+
+        # f64 truth on this GPU
+        tx = torch.from_numpy(x).cuda().double()
+        tr = 1 / (1 + torch.exp(-(tx @ torch.from_numpy(w).cuda().double()))) - torch.from_numpy(y).cuda().double()
+        tg = (tx.t() @ tr).reshape(-1).cpu().numpy()
+        ts = float(tr.sum())
+        del tx, tr
+        for key, fn, passes, note in (
+                ("cfg5_logistic_step_1Mx1024_f32", two_pass, 2, "z=X@w, r=1/(1+exp(-z))-y, g=X.t()@r, accu(r); X read twice"),
+                ("cfg5_logistic_step_fused_1Mx1024_f32", fused, 1,
+                 "r, g = evaluate_many(r, X.t() @ r) with r = 1/(1+exp(-X@w))-y; accu(r); X read once")):
+            t = _median_ms(torch, fn)
+            nb = passes * 4 * nrow * ncol
+            r, g, s = fn()
+            gg = g.to_numpy().reshape(-1)
+            e = {"ms": t, "GB/s": nb / t / 1e6, "frac": nb / t / 1e6 / peak_hbm, "reps": 10, "note": note,
+                 "parity": {"tol": 1e-5, "g_vs_f64": _rel(gg, tg), "s_vs_f64": _rel(s, ts)}}
+            if "cfg5_g" in gold:
+                e["parity"]["g_vs_reference"] = _rel(gg, gold["cfg5_g"])
+                e["parity"]["s_vs_reference"] = _rel(s, gold["cfg5_s"])
+            out[key] = e
+        del X, W, Y, r_e
+        if ref is not None:
+            ms_ = 1 << 17
+
+            def ref_step(d, ms):
+                z = d.evaluate(ms[0] @ ms[1])
+                r = d.evaluate(1 / (1 + d.exp(0 - z)) - ms[2])
+                d.evaluate(ms[0].t() @ r)
+                d.accu(r)
+
+            s = ref.run("parallel", [x[:ms_], w, y[:ms_]], ref_step)
+            for key in ("cfg5_logistic_step_1Mx1024_f32", "cfg5_logistic_step_fused_1Mx1024_f32"):
+                out[key]["cpu_baseline"] = ref.baseline(2 * 4 * ms_ * ncol / s / 1e9, "GB/s",
+                                                        f"one step on the first {ms_} rows (1/8 of X)")
+                out[key]["speedup_vs_cpu"] = out[key]["GB/s"] / out[key]["cpu_baseline"]["value"]
+        del x
+    except Exception as ex:  # pragma: no cover
+        out["cfg5_error"] = repr(ex)[:300]
+    return out
+
+
+def sharded_suite(dm, torch, rank: int, world: int) -> dict:
+    """N > 1: the configs that shard, strong scaling (the total
+    work is the single-GPU config split over the ranks), every rank's result
+    checked in-run against the single-device computation of the same data on
+    its own GPU.  Inputs come from the counter RNG (every rank generates the
+    same full operands locally, then keeps its block: nothing is broadcast).
+    Timing: K steps between barriers, CUDA events, max over ranks."""
+    import torch.distributed as tdist
+    from paper_2308_03120_b200 import dist as D
+    out = {}
+    peak_hbm, _, _ = _peaks()
+    dev = "cuda" if tdist.get_backend() == "nccl" else "cpu"
+    K = 10
+
+    def reduce_max(vals):
+        t = torch.tensor(vals, dtype=torch.float64, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        return [float(v) for v in t.cpu()]
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        tdist.barrier()
+        torch.cuda.synchronize()
+        ms = _event_time_ms(torch, fn, K) / K
+        tdist.barrier()
+        return ms
+
+    # config 3: dot / norm of 2^30 f32, split over the ranks (power-of-two shards: bit-exact)
+    try:
+        n = 1 << 30
+        dm.set_seed(2)
+        a = dm.Col(n, fill="randu")
+        b = dm.Col(n, fill="randu")
+        want_dot = np.float32(dm.dot(a, b))
+        want_nn = np.float32(dm.dot(a, a))
+        s0, cnt = D.column_block(n, rank, world)
+        sa, sb = dm.Matrix(cnt, 1), dm.Matrix(cnt, 1)
+        D.torch_view(sa).copy_(D.torch_view(a)[s0:s0 + cnt])
+        D.torch_view(sb).copy_(D.torch_view(b)[s0:s0 + cnt])
+        del a, b
+        torch.cuda.synchronize()
+        for key, args, want, nb in (("cfg3_dot_2^30_f32_sharded", (sa, sb), want_dot, 8 * n),
+                                    ("cfg3_norm2_2^30_f32_sharded", (sa, sa), want_nn, 4 * n)):
+            red = D.ShardedReduction("dot", *args)
+            ms = timed(lambda: (red.launch(), red.join()))
+            got = np.float32(red.value())
+            bad, ms = reduce_max([0.0 if got.tobytes() == want.tobytes() else 1.0, ms])
+            out[key] = {"ms": ms, "GB/s": nb / ms / 1e6, "frac_per_gpu": nb / ms / 1e6 / world / peak_hbm,
+                        "scaling": "strong", "collective": red.collective,
+                        "parity": {"vs": "single-device reduction of the whole vector on each rank's GPU",
+                                   "bit_exact_all_ranks": bad == 0.0}}
+            del red
+        del sa, sb
+    except Exception as ex:  # pragma: no cover
+        out["cfg3_sharded_error"] = repr(ex)[:300]
+
+    # config 2: f64 row reductions (dim 1) of 16384^2, column blocks per rank + one gather
+    try:
+        nr = 16384
+        dm.set_seed(1)
+        full = dm.Matrix(nr, nr, fill="randu", elem_type="f64")
+        c0, cc = D.column_block(nr, rank, world)
+        local = dm.evaluate(full.cols(c0, c0 + cc - 1))
+        for op in ("sum", "min", "max"):
+            want = dm.evaluate(getattr(dm, op)(full, 1)).to_numpy().reshape(-1)
+            ms = timed(lambda op=op: D.sharded_reduce_dim(op, local, 1))
+            got = D.sharded_reduce_dim(op, local, 1).to_numpy().reshape(-1)
+            err = _rel(got, want)
+            exact = got.tobytes() == want.tobytes()
+            err, notexact, ms = reduce_max([err, 0.0 if exact else 1.0, ms])
+            nb = 8 * nr * nr
+            out[f"cfg2_{op}_dim1_16384^2_f64_sharded"] = {
+                "ms": ms, "GB/s": nb / ms / 1e6, "scaling": "strong",
+                "parity": {"vs": "single-device reduction on each rank's GPU", "tol": 1e-12 if op == "sum" else 0.0,
+                           "max_rel_err": err, "bit_exact_all_ranks": notexact == 0.0,
+                           "note": "sum: each rank folds its columns, then the rank partials are folded in rank "
+                                   "order (not the single-device left-to-right order)"}}
+        del full, local
+    except Exception as ex:  # pragma: no cover
+        out["cfg2_sharded_error"] = repr(ex)[:300]
+
+    # config 4: C = A * B^T with C's columns (B's rows) sharded; A generated locally on every rank
+    try:
+        for elem, n in (("f32", 8192), ("f64", 8192)):
+            dm.set_seed(3)
+            A = dm.Matrix(n, n, fill="randu", elem_type=elem)
+            B = dm.Matrix(n, n, fill="randu", elem_type=elem)
+            r0, rc = D.column_block(n, rank, world)
+            Bl = dm.evaluate(B.rows(r0, r0 + rc - 1))
+            want = dm.evaluate(A @ B.t())
+            ms = timed(lambda: D.sharded_gemm_nt(A, Bl))
+            Cl = D.sharded_gemm_nt(A, Bl)
+            got = D.torch_view(Cl).view(rc, n)                    # column-major: rc columns of n
+            ref_blk = D.torch_view(want).view(n, n)[r0:r0 + rc]
+            err = float((got.double() - ref_blk.double()).abs().max() / max(float(ref_blk.abs().max()), 1.0))
+            exact = bool(torch.equal(got, ref_blk))
+            err, notexact, ms = reduce_max([err, 0.0 if exact else 1.0, ms])
+            out[f"cfg4_gemm_nt_{n}^3_{elem}_sharded"] = {
+                "ms": ms, "TFLOP/s": 2 * n ** 3 / ms / 1e9, "scaling": "strong",
+                "parity": {"vs": "the same column block of the single-device product on each rank's GPU",
+                           "max_rel_err": err, "bit_exact_all_ranks": notexact == 0.0}}
+            del A, B, Bl, want, Cl
+    except Exception as ex:  # pragma: no cover
+        out["cfg4_sharded_error"] = repr(ex)[:300]
+
+    # config 5: logistic step sharded by samples (row blocks of X), one gather of g
+    try:
         nrow, ncol = 1 << 20, 1024
         dm.set_seed(5)
         X = dm.Matrix(nrow, ncol, fill="randn")
         w = dm.evaluate(0.03 * dm.Matrix(ncol, 1, fill="randn"))
         y = dm.evaluate(dm.conv_to(dm.conv_to(2 * dm.Matrix(nrow, 1, fill="randu"), "i32"), "f32"))
-
-        def step():
-            z = dm.evaluate(X @ w)
-            r = dm.evaluate(1 / (1 + dm.exp(0 - z)) - y)
-            g = dm.evaluate(X.t() @ r)
-            return r, g
-
-        def timed():
-            r, g = step()
-            dm.accu(r)
-
-        t = best_ms(timed, reps=3)
-        nbytes = 2 * 4 * nrow * ncol
-        out["logistic_step_1Mx1024_f32"] = {"ms": t, "GB/s": nbytes / t / 1e6, "frac": nbytes / t / 1e6 / peak_hbm,
-                                            "note": "z=X@w, r=1/(1+exp(-z))-y, g=X.t()@r, accu(r); X read twice"}
-        r_e = 1 / (1 + dm.exp(0 - X @ w)) - y
-
-        def timed_fused():
-            r, g = dm.evaluate_many(r_e, X.t() @ r_e)
-            dm.accu(r)
-
-        t = best_ms(timed_fused, reps=3)
-        nbytes = 4 * nrow * ncol
-        out["logistic_step_fused_1Mx1024_f32"] = {
-            "ms": t, "GB/s": nbytes / t / 1e6, "frac": nbytes / t / 1e6 / peak_hbm,
-            "note": "r, g = evaluate_many(r, X.t() @ r) with r = 1/(1+exp(-X@w))-y; accu(r); X read once"}
-        del X
-    except Exception as e:  # pragma: no cover
-        out["logistic_error"] = repr(e)[:200]
+        r0, rc = D.column_block(nrow, rank, world)
+        Xl = dm.evaluate(X.rows(r0, r0 + rc - 1))
+        yl = dm.evaluate(y.rows(r0, r0 + rc - 1))
+        zf = dm.evaluate(X @ w)
+        rf = dm.evaluate(1 / (1 + dm.exp(0 - zf)) - y)
+        g_want = dm.evaluate(X.t() @ rf).to_numpy().reshape(-1)
+        s_want = dm.accu(rf)
+        del X, zf, rf
+        ms = timed(lambda: D.sharded_logistic_step(Xl, w, yl))
+        g, s = D.sharded_logistic_step(Xl, w, yl)
+        gerr = _rel(g.to_numpy().reshape(-1), g_want)
+        serr = _rel(s, s_want)
+        gerr, serr, ms = reduce_max([gerr, serr, ms])
+        nb = 2 * 4 * nrow * ncol
+        out["cfg5_logistic_step_1Mx1024_f32_sharded"] = {
+            "ms": ms, "GB/s": nb / ms / 1e6, "scaling": "strong",
+            "parity": {"vs": "single-device step on each rank's GPU", "tol": 1e-5, "g_max_rel_err": gerr,
+                       "s_max_rel_err": serr}}
+        del Xl, yl, w, y
+    except Exception as ex:  # pragma: no cover
+        out["cfg5_sharded_error"] = repr(ex)[:300]
     return out
 
 
@@ -442,9 +774,11 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
     result_value = red.value()
     secondary = {}
     cpu = None
-    if rank == 0 and world == 1 and not args.no_secondary:
-        secondary = secondary_suite(dm, torch)
+    if world == 1 and not args.no_secondary:
+        secondary = secondary_suite(dm, torch, cpu=not args.no_cpu)
         secondary["torch_reference"] = torch_reference(torch, host)
+    elif world > 1 and not args.no_secondary:
+        secondary = sharded_suite(dm, torch, rank, world)
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_reference_run(host, args.cpu_seconds, None, 1)
 
@@ -499,6 +833,13 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
             "clocks": clocks.summary(),
             "result": float(result_value),
         }
+        gold = _golden_baseline()
+        if gold is not None and world == 1:
+            want = float(gold["cfg1_accu_exp"])
+            line["parity"] = {"vs": "the unmodified reference's accu at 4096^2, default_rng(0) "
+                                    "(tests/golden/baseline.npz)", "reference": want,
+                              "rel_err": _rel(result_value, want), "tol": 1e-5,
+                              "bit_exact": bool(np.float32(result_value).tobytes() == np.float32(want).tobytes())}
         if cpu is not None:
             line["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
         if secondary:
@@ -530,7 +871,6 @@ def main() -> None:
             # test mode only: every rank on GPU 0 over gloo (NCCL refuses two ranks
             # on one device); a rank-slotted all-reduce stands in for the all-gather
             local_rank = 0
-            os.environ.setdefault("BM_SHARD_COLLECTIVE", "allreduce")   # or p2p: peer-memory exchange
             torch.cuda.set_device(0)
             tdist.init_process_group("gloo")
         else:

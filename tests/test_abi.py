@@ -80,3 +80,31 @@ def test_header_constants_match_binding():
 def test_sm100a_code_in_library():
     out = subprocess.run(["cuobjdump", "--list-elf", str(_clib.LIB_PATH)], capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+# ---- the C example (examples/c_abi_example.c): the ABI from C, no Python -------------------------
+
+def _build_c_example(tmp_path):
+    import subprocess
+    root = pathlib.Path(__file__).resolve().parents[1]
+    exe = tmp_path / "c_abi_example"
+    lib_dir = root / "paper_2308_03120_b200"
+    cmd = ["gcc", "-O2", "-std=c11", "-Wall", "-Werror", "-I", str(root / "include"),
+           str(root / "examples" / "c_abi_example.c"), "-L", str(lib_dir), "-lb200mat",
+           f"-Wl,-rpath,{lib_dir}", "-lm", "-o", str(exe)]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return exe
+
+
+def test_c_example_compiles_and_links(tmp_path):
+    assert _build_c_example(tmp_path).exists()
+
+
+@pytest.mark.gpu
+def test_c_example_runs(tmp_path):
+    import subprocess
+    exe = _build_c_example(tmp_path)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "c_abi_example: ok" in r.stdout

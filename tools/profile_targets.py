@@ -41,9 +41,9 @@ def main(which: str) -> None:
         r_e = 1 / (1 + dm.exp(0 - X @ w)) - y
         for _ in range(3):
             r, g = dm.evaluate_many(r_e, X.t() @ r_e)
-    elif which in ("gemm_f32", "gemm_f64"):
+    elif which in ("gemm_f32", "gemm_f64", "gemm32k_f32", "gemm32k_f64"):
         elem = which[-3:]
-        n = 8192
+        n = 32768 if "32k" in which else 8192
         A = dm.Matrix(n, n, fill="randu", elem_type=elem)
         B = dm.Matrix(n, n, fill="randu", elem_type=elem)
         for _ in range(3):

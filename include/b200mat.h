@@ -77,7 +77,12 @@ extern "C" {
 #define BM_K_RANDU          10   /* gen_randu (splitmix64 counter RNG, kernels.py:227-245)         */
 #define BM_K_RANDN          11   /* gen_randn (Box-Muller, kernels.py:248-253)                     */
 #define BM_K_STRIDED_COPY   12   /* mov_extract_strided / mov_insert_strided / resize / joins      */
-#define BM_K_LOGISTIC_GRAD  13   /* fused single-pass logistic step             */
+#define BM_K_LOGISTIC_GRAD  13   /* fused single-pass logistic step: inputs X
+                                    (block view, m x k f32), w (k), r (m, written), then the
+                                    program's inputs 1..; program input 0 is X w; output g (k).
+                                    iparams[0] = address of an f32 device slot that receives
+                                    accu(r) in the reference's order (0: not wanted; needs
+                                    m <= 2^26)                                                    */
 #define BM_K_PRED_COUNT     14   /* pred_count / pred_all_any: matches of an element-vs-scalar test
                                     (ops.py:202-262, kernels.py:643-699); result u64 via
                                     bm_execute_reduce; iparams[0] = BM_CMP_*, threshold in scalars[0] */

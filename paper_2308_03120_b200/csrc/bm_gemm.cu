@@ -243,14 +243,68 @@ __global__ void __launch_bounds__(256) gemv_t_vec_kernel(const T* __restrict__ A
     if (lane == 0) part[(i64)blockIdx.y * ncols + j] = acc;
 }
 
-// fold of the fused logistic step's per-CTA gradient partials, in CTA order
-__global__ void __launch_bounds__(256) lgrad_finish_kernel(const double* __restrict__ part, int grid, i64 k,
-                                                           float* __restrict__ g) {
-    const i64 c = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= k) return;
-    double s = 0.0;
-    for (int b = 0; b < grid; ++b) s += part[(i64)b * k + c];
-    g[c] = (float)s;
+// Tail of the fused logistic step (bm_lgrad.cuh), one launch:
+//  * CTAs [0, gridDim.x - has_accu): g[c] = the per-cluster gradient partials
+//    of column c folded in cluster order -- 8 warps each add a contiguous
+//    eighth of the P partials (independent loads in flight, 32 columns
+//    coalesced per warp), then the eight sums are added in warp order;
+//  * the last CTA (accu_out != 0): accu(r) in the reference's order
+//    (kernels.py:459-460 ndarray.sum per 8192-element block, combine_pairwise
+//    kernels.py:380-392).  The kernel already left every 128-element numpy
+//    leaf of the full blocks in `leaves`; a block value is numpy's balanced
+//    tree over its 64 leaves (one warp, operand order kept), the ragged tail
+//    block is pw_generic over r, and the blocks fold with combine_pairwise.
+// Launched with programmatic dependent launch: griddepcontrol.wait orders it
+// after the logistic kernel's writes.
+__global__ void __launch_bounds__(256) lgrad_finish_kernel(const double* __restrict__ part, int P, i64 k,
+                                                           float* __restrict__ g, const float* __restrict__ leaves,
+                                                           const float* __restrict__ r, i64 m,
+                                                           float* __restrict__ accu_out) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool accu_cta = accu_out != nullptr && blockIdx.x == gridDim.x - 1;
+    if (!accu_cta) {
+        __shared__ double ps[8][32];
+        const i64 c = (i64)blockIdx.x * 32 + lane;
+        const int b0 = (int)((i64)P * warp / 8), b1 = (int)((i64)P * (warp + 1) / 8);
+        double s = 0.0;
+        if (c < k) {
+#pragma unroll 4
+            for (int b = b0; b < b1; ++b) s += __ldcg(part + (i64)b * k + c);
+        }
+        ps[warp][lane] = s;
+        __syncthreads();
+        if (warp == 0 && c < k) {
+            double t = ps[0][lane];
+#pragma unroll
+            for (int w = 1; w < 8; ++w) t += ps[w][lane];
+            g[c] = (float)t;
+        }
+        return;
+    }
+    __shared__ float bv[LG_ACCU_MAX_BLOCKS];
+    __shared__ float scratch[LG_ACCU_MAX_BLOCKS / 256 + 2];
+    __shared__ __align__(16) char tile[BM_TILE_BYTES];
+    const i64 nfull = m / BM_REDUCE_BLOCK, tail = m - nfull * BM_REDUCE_BLOCK;
+    for (i64 b = warp; b < nfull; b += 8) {
+        const float* lv = leaves + b * (BM_REDUCE_BLOCK / 128);
+        float x = lv[2 * lane] + lv[2 * lane + 1];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const float y = warp_shfl_xor(x, o);
+            x = (lane & o) ? y + x : x + y;
+        }
+        if (lane == 0) bv[b] = x;
+    }
+    if (tail && warp == 7) {
+        const BufSrc<float> src{r, 1};
+        const bool vec_ok = ((uintptr_t)(r + nfull * BM_REDUCE_BLOCK) & 15u) == 0;
+        const float t = pw_generic<float>(src, nfull * BM_REDUCE_BLOCK, tail, tile, vec_ok);
+        if (lane == 0) bv[nfull] = t;
+    }
+    __syncthreads();
+    const float v = cta_fold_pairwise<float, 1>(bv, scratch, (int)(nfull + (tail ? 1 : 0)));
+    if (threadIdx.x == 0) accu_out[0] = v + 0.0f;   // numpy: 0 + pairwise(...)
 }
 
 }  // namespace bm
@@ -397,9 +451,19 @@ int launch_gemm(const bm_invocation* inv) {
     return set_error(BM_ERR_ARG, "gemm: bad dtype");
 }
 
-int launch_lgrad_finish(const double* gpart, int grid, int64_t k, float* g) {
-    bm::lgrad_finish_kernel<<<(unsigned)((k + 255) / 256), 256, 0, st().stream>>>(gpart, grid, k, g);
-    BM_CUDA(cudaGetLastError());
+int launch_lgrad_finish(const double* gpart, int grid, int64_t k, float* g, const float* leaves, const float* r,
+                        int64_t m, float* accu_out) {
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg;
+    std::memset(&cfg, 0, sizeof cfg);
+    cfg.gridDim = dim3((unsigned)((k + 31) / 32 + (accu_out ? 1 : 0)));
+    cfg.blockDim = dim3(256);
+    cfg.stream = st().stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    BM_CUDA(cudaLaunchKernelEx(&cfg, bm::lgrad_finish_kernel, gpart, grid, (bm::i64)k, g, leaves, r, (bm::i64)m, accu_out));
     st().launches++;
     return BM_OK;
 }

@@ -26,6 +26,8 @@ struct State {
     void* partials[2] = {nullptr, nullptr};
     int64_t partials_cap = 0;          // capacity of each, in 8-byte entries
     void* fold_scratch = nullptr;      // chunk results of the separate fold kernels (8192 x 8 B)
+    void* lg_scratch = nullptr;        // fused logistic step: gradient partials + accu leaves (stream-ordered reuse)
+    int64_t lg_scratch_cap = 0;        // bytes
     // pending fused exchange for the next reduction (bm_reduce_to_device_exchange)
     void* const* exch_peers = nullptr;
     int exch_world = 0, exch_rank = 0;

@@ -33,8 +33,14 @@
 //            accumulator for the whole kernel.
 // The loop is software-pipelined: while the partials of slab j + 1 travel,
 // the CTA runs phase 2 of slab j.
-// Slabs are dealt round-robin to clusters; every cluster writes its k
-// partials and lgrad_finish folds them in cluster order: deterministic.
+// Slabs are dealt to clusters in consecutive pairs (pair p = slabs 2p, 2p+1,
+// pairs round-robin), so every 128-row numpy leaf of r is produced by one
+// cluster: with the accu side output on, warp 0 of CTA 0 runs numpy's eight
+// interleaved accumulators over the pair's r values and writes the leaf sum
+// (kernels.py:459-460; ndarray.sum's pairwise leaves), and lgrad_finish folds
+// leaves -> 8192-row blocks -> combine_pairwise, so accu(r) costs no pass.
+// Every cluster writes its k gradient partials and lgrad_finish folds them in
+// cluster order: deterministic.
 // Compiled by NVRTC with the program's functor E.
 #pragma once
 #include "bm_reduce.cuh"
@@ -68,8 +74,10 @@ struct LgArgs {
     const float* w;             // k
     float* r;                   // m (side output)
     double* gpart;              // clusters x k partials
+    float* leaves;              // accu(r) side output: numpy leaf sums of the full blocks (nullptr: off)
     i64 m, k;
     i64 nslabs;
+    i64 nleaves;                // 128-row leaves inside full 8192-row blocks
 };
 
 __device__ __forceinline__ unsigned lg_smem(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -171,7 +179,11 @@ __device__ void logistic_grad(const LgArgs& L) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const unsigned q = lg_cluster_rank();
     const i64 cluster = blockIdx.x / LG_CLUSTER, nclusters = gridDim.x / LG_CLUSTER;
-    const i64 nmine = L.nslabs > cluster ? (L.nslabs - cluster + nclusters - 1) / nclusters : 0;
+    // slab j of this cluster: pair cluster + (j / 2) * nclusters, half j % 2
+    const i64 npairs = (L.nslabs + 1) / 2;
+    const i64 pmine = npairs > cluster ? (npairs - cluster + nclusters - 1) / nclusters : 0;
+    const i64 nmine = 2 * pmine - (((L.nslabs & 1) && pmine > 0 && cluster + (pmine - 1) * nclusters == npairs - 1) ? 1 : 0);
+    auto slab_of = [&](i64 j) -> i64 { return 2 * (cluster + (j >> 1) * nclusters) + (j & 1); };
     const int col0 = (int)q * LG_COLS;                  // this CTA's first column
     for (int c = tid; c < LG_COLS; c += LG_BLOCK) ws[c] = (col0 + c < L.k) ? L.w[col0 + c] : 0.f;
     if (tid == 0) {
@@ -203,7 +215,7 @@ __device__ void logistic_grad(const LgArgs& L) {
                 if (i >= LG_NBOX) lg_wait(&empty[s], (unsigned)(((i / LG_NBOX) - 1) & 1));
                 const i64 j = i / LG_NB;
                 const int b = (int)(i % LG_NB);
-                const i64 slab = cluster + j * nclusters;
+                const i64 slab = slab_of(j);
                 lg_expect_tx(&full[s], LG_BOX_BYTES);
                 lg_tma_2d(ring + s * LG_BOX_BYTES, &L.tmx, (int)(slab * LG_RB), col0 + b * LG_BOXC, &full[s]);
             }
@@ -304,7 +316,7 @@ __device__ void logistic_grad(const LgArgs& L) {
                 double z = zq_all[par][0][tid];
 #pragma unroll
                 for (unsigned p = 1; p < LG_CLUSTER; ++p) z = z + zq_all[par][p][tid];
-                const i64 row = (cluster + j * nclusters) * LG_RB + tid;
+                const i64 row = slab_of(j) * LG_RB + tid;
                 float r = 0.f;
                 if (row < L.m) {
                     r = E::at(L.a, pre, (float)z);
@@ -317,8 +329,28 @@ __device__ void logistic_grad(const LgArgs& L) {
         // partial sums for its 16 columns, then a transpose-reduce across the 16
         // lanes of the half-warp (15 shuffles), after which lane l owns column
         // cw + (l & 15) (bit-reversed order: 8 b3 + 4 b2 + 2 b1 + b0)
+        float lacc = 0.f;                      // numpy leaf accumulator (warp 0, lanes 0..7 of CTA 0)
+        auto leaf = [&](i64 j) {
+            const int par = (int)(j & 1);
+            const i64 pair = slab_of(j) >> 1;
+            if (pair >= L.nleaves) return;     // tail block: folded from r by lgrad_finish
+            const int t = lane & 7;
+            float acc = (j & 1) ? lacc : rs[par][t];
+#pragma unroll
+            for (int i = (j & 1) ? 0 : 1; i < LG_RB / 8; ++i) acc = acc + rs[par][8 * i + t];
+            if (!(j & 1)) {
+                lacc = acc;
+                return;
+            }
+            // ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7))
+            acc = acc + __shfl_down_sync(0xffffffffu, acc, 1);
+            acc = acc + __shfl_down_sync(0xffffffffu, acc, 2);
+            acc = acc + __shfl_down_sync(0xffffffffu, acc, 4);
+            if (lane == 0) L.leaves[pair] = acc;
+        };
         auto phase2 = [&](i64 j) {
             const int par = (int)(j & 1);
+            if (L.leaves != nullptr && q == 0 && warp == 0) leaf(j);
             const float4 rr = *reinterpret_cast<const float4*>(&rs[par][4 * hl]);
             float xs[64];
             const unsigned t = tmem_me + (unsigned)((j & 1) * 256);
@@ -351,7 +383,7 @@ __device__ void logistic_grad(const LgArgs& L) {
         auto csync = [&]() { asm volatile("bar.sync 1, %0;" ::"n"(LG_THREADS) : "memory"); };
         if (nmine > 0) {
             if (tid < LG_RB) {
-                const i64 row = cluster * LG_RB + tid;
+                const i64 row = slab_of(0) * LG_RB + tid;
                 if (row < L.m) E::load(L.a, row, pre);
             }
             phase1(0);
@@ -361,7 +393,7 @@ __device__ void logistic_grad(const LgArgs& L) {
         for (i64 j = 0; j < nmine; ++j) {
             chain(j);
             if (j + 1 < nmine && tid < LG_RB) {   // y & co. of slab j + 1 into registers now
-                const i64 row = (cluster + (j + 1) * nclusters) * LG_RB + tid;
+                const i64 row = slab_of(j + 1) * LG_RB + tid;
                 if (row < L.m) E::load(L.a, row, pre);
             }
             if (j + 1 < nmine) phase1(j + 1);
@@ -369,6 +401,7 @@ __device__ void logistic_grad(const LgArgs& L) {
             if (j + 1 < nmine) publish(j + 1);
             phase2(j);
         }
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // lgrad_finish may get resident
         {
             const int c = col0 + cw + 8 * ((lane >> 3) & 1) + 4 * ((lane >> 2) & 1) + 2 * ((lane >> 1) & 1) + (lane & 1);
             if (c < L.k) L.gpart[cluster * L.k + c] = gacc;

@@ -28,6 +28,7 @@ namespace bm {
 
 #define BM_MAXIN 16
 #define BM_REDUCE_BLOCK 8192
+#define LG_ACCU_MAX_BLOCKS 8192           // fused logistic step: accu(r) side output up to 2^26 rows
 #define BM_TILE_PITCH 544
 #define BM_TILE_BYTES (8 * BM_TILE_PITCH)   // one half-unit (8 rows of 512 B)
 #ifndef BM_UNIT_UNROLL

@@ -158,6 +158,9 @@ int bm_shutdown(void) {
     cudaFree(s.result);
     cudaFree(s.fold_scratch);
     s.fold_scratch = nullptr;
+    cudaFree(s.lg_scratch);
+    s.lg_scratch = nullptr;
+    s.lg_scratch_cap = 0;
     cudaFreeHost(s.host_slot);
     cudaFreeHost(s.err_host);
     s.err_host = s.err_dev = nullptr;

@@ -406,6 +406,7 @@ def torch_view(m):
     """The column-major storage of a device matrix as a flat torch tensor
     sharing its memory (no copy): what NCCL reads and writes."""
     import torch
+    _rt.get_runtime().forget_sum(m.mem.buffer_id)   # the view can write: drop a cached accu
     return torch.as_tensor(_CudaArray(m.mem.ptr, m.n_elem, m.elem_type), device="cuda")
 
 

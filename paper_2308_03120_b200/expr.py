@@ -17,11 +17,18 @@ rewrites, plan/evaluate behaviour) are the reference's
 * scalar reductions over an expression (``accu``, ``dot``, ``norm``) run the
   element-wise program and the reduction in the same kernel
   (:func:`plan_reduce`) instead of materialising the tree first
-  (ops.py:153-177).
+  (ops.py:153-177);
+* evaluate / evaluate_many / scalar reductions keep a recipe per DAG shape:
+  the plan and its device invocations are built once, and a later call with
+  matrices of the same shapes and types only re-addresses buffers (the
+  reference re-plans every call), which keeps the host out of the way of a
+  step that ends in a scalar read.
 """
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+import collections
+import os
+from dataclasses import dataclass, field, replace
 from typing import NamedTuple
 
 import numpy as np
@@ -360,6 +367,8 @@ class EvalPlan:
     absorbed: list
     reduce: PlanStep | None = None   # trailing fused reduction (plan_reduce)
     extra: tuple = ()                # further result refs (evaluate_many)
+    sums: tuple = ()                 # (slot, sum slot): a step also left accu(slot) in the reference's
+                                     # order in a 1-element slot (the fused logistic step's r)
 
     @property
     def n_invocations(self) -> int:
@@ -391,6 +400,10 @@ class EvalPlan:
             ids.add(self.result[1].mem.buffer_id)
         return ids
 
+
+# bm_reduce.cuh LG_ACCU_MAX_BLOCKS: the fused logistic step's accu(r) side output covers
+# up to this many 8192-element blocks (2^26 rows)
+LGRAD_ACCU_MAX_BLOCKS = 8192
 
 _GEN_KERNEL = {"gen_zeros": "gen_fill_const", "gen_ones": "gen_fill_const", "gen_fill": "gen_fill_const",
                "gen_eye": "gen_eye", "gen_linspace": "gen_linspace", "gen_randu": "gen_randu",
@@ -429,6 +442,7 @@ class _Lowerer:
         self.slots: list[SlotInfo] = []
         self.absorbed: list[tuple] = []
         self.memo: dict = {}          # (id(node), type) -> ref of a value a fused step already produced
+        self.sums: list = []          # (slot, sum slot) side outputs (EvalPlan.sums)
 
     def emit(self, kernel, inputs, in_modes, shape, out_type, out_mode, scalars=(), params=None,
              absorbed_from=None) -> tuple:
@@ -592,11 +606,18 @@ class _Lowerer:
         wref = self.lower(w, "f32")
         self.slots.append(SlotInfo(m, 1, "f32"))
         r_slot = len(self.slots) - 1
+        params = {"program": tuple(prog.stages), "compute_dtype": NP_DTYPE["f32"].str, "alloc_slots": (r_slot,)}
+        if -(-m // kernels.REDUCE_BLOCK) <= LGRAD_ACCU_MAX_BLOCKS:
+            # the kernel also leaves accu(r) (reference order) in a 1-element slot, so a
+            # following accu(r) of the returned matrix is a 4-byte read (runtime sum cache)
+            self.slots.append(SlotInfo(1, 1, "f32"))
+            a_slot = len(self.slots) - 1
+            params["alloc_slots"] = (r_slot, a_slot)
+            params["accu_slot"] = a_slot
+            self.sums.append((r_slot, a_slot))
         inputs = [("leaf", X), wref, ("slot", r_slot)] + list(prog.inputs[1:])
         modes = ["2d", "flat", "flat"] + ["flat"] * (len(prog.inputs) - 1)
-        ref = self.emit("logistic_grad", inputs, modes, shape_of(node), "f32", "flat",
-                        params={"program": tuple(prog.stages), "compute_dtype": NP_DTYPE["f32"].str,
-                                "alloc_slots": (r_slot,)})
+        ref = self.emit("logistic_grad", inputs, modes, shape_of(node), "f32", "flat", params=params)
         self.memo[(id(b), "f32")] = ("slot", r_slot)
         if want != "f32":
             ref = self.emit("mov_copy", [ref], ["flat"], shape_of(node), want, "flat")
@@ -802,7 +823,7 @@ def plan(x, out_elem_type: str | None = None, fuse: bool = True, chain_max: int 
     node = as_expr(x)
     low = _Lowerer(fuse, chain_max)
     result = low.lower(node, out_elem_type or node.elem_type)
-    return EvalPlan(low.steps, low.slots, result, low.absorbed)
+    return EvalPlan(low.steps, low.slots, result, low.absorbed, sums=tuple(low.sums))
 
 
 def plan_reduce(op: str, *xs, fuse: bool = True) -> EvalPlan:
@@ -826,7 +847,7 @@ def plan_reduce(op: str, *xs, fuse: bool = True) -> EvalPlan:
             prog.stages.append(("load", remap[st[1]]) if st[0] == "load" else st)
     red = PlanStep("fused_reduce", tuple(prog.inputs), ("flat",) * len(prog.inputs), -1, "none", (),
                    {"program": tuple(prog.stages), "compute_dtype": NP_DTYPE[elem].str, "op": op})
-    return EvalPlan(low.steps, low.slots, None, low.absorbed, reduce=red)
+    return EvalPlan(low.steps, low.slots, None, low.absorbed, reduce=red, sums=tuple(low.sums))
 
 
 # ---------------------------------------------------------------------------
@@ -844,22 +865,132 @@ def _make_view(buf, rows: int, cols: int, mode):
     raise ValueError(f"unknown view mode {mode!r}")
 
 
-def _step_views(plan_obj: EvalPlan, step: PlanStep, slot_bufs: dict) -> list:
+def _step_views(plan_obj: EvalPlan, step: PlanStep, slot_bufs: dict, leaves=None) -> list:
     views = []
     for ref, mode in zip(step.inputs, step.in_modes):
-        if ref[0] == "leaf":
-            m = ref[1]
-            views.append(_make_view(m.mem, m.n_rows, m.n_cols, mode))
-        else:
+        if ref[0] == "slot":
             info = plan_obj.slots[ref[1]]
             views.append(_make_view(slot_bufs[ref[1]], info.rows, info.cols, mode))
+        else:
+            m = ref[1] if ref[0] == "leaf" else leaves[ref[1]]
+            views.append(_make_view(m.mem, m.n_rows, m.n_cols, mode))
     return views
 
 
-def execute_plan(plan_obj: EvalPlan, target_buf=None):
+# ---------------------------------------------------------------------------
+# plan recipes
+#
+# A recipe is a plan lowered once for a DAG *shape* -- node kinds, scalars,
+# element types, matrix shapes and which nodes / matrices are shared -- with
+# its leaves replaced by positions ("leafpos", i), plus the device invocation
+# of every step built on first use.  A later call with the same shape binds its
+# own leaf matrices and only re-addresses the invocations (buffer pointers),
+# skipping lowering, view construction and build_invocation.  Lowering depends
+# on nothing but what the key holds (shapes, types, sharing), so a recipe is
+# exactly the plan the call would have made.
+
+_RECIPE_MAX = 256
+_RECIPES_ON = os.environ.get("BM_PLAN_CACHE", "1") != "0"
+
+
+class _NoRecipe(Exception):
+    pass
+
+
+def _dag_key(roots):
+    """Structural key of the DAG under ``roots`` and its distinct leaf
+    matrices in first-visit order (None when a node is not cacheable)."""
+    ids: dict = {}
+    lv: dict = {}
+    leaves: list = []
+    out: list = []
+    stack = list(reversed(roots))
+    while stack:
+        n = stack.pop()
+        i = ids.get(id(n))
+        if i is not None:
+            out.append(i)                       # a shared node: back-reference
+            continue
+        if not isinstance(n, ExprNode):
+            return None, None
+        ids[id(n)] = len(ids)
+        if n.kind == "leaf":
+            m = n.operands[0]
+            j = lv.get(id(m))
+            if j is None:
+                j = lv[id(m)] = len(leaves)
+                leaves.append(m)
+            out.append((j, m.n_rows, m.n_cols, m.elem_type))
+        else:
+            out.append((n.kind, n.aux, n.elem_type, len(n.operands)))
+            stack.extend(reversed(n.operands))
+    return tuple(out), leaves
+
+
+class _Recipe:
+    __slots__ = ("plan", "protos", "reduce_proto", "out_refs")
+
+    def __init__(self, plan_obj: EvalPlan, out_refs=None):
+        self.plan = plan_obj
+        self.protos: list = [None] * len(plan_obj.steps)   # (ctypes invocation, input refs) per step
+        self.reduce_proto = None
+        self.out_refs = out_refs
+
+
+def _templatise(plan_obj: EvalPlan, leaves: list) -> EvalPlan:
+    pos = {id(m): i for i, m in enumerate(leaves)}
+
+    def conv(ref):
+        if ref is not None and ref[0] == "leaf":
+            i = pos.get(id(ref[1]))
+            if i is None:
+                raise _NoRecipe
+            return ("leafpos", i)
+        return ref
+
+    steps = [replace(st, inputs=tuple(conv(r) for r in st.inputs)) for st in plan_obj.steps]
+    red = replace(plan_obj.reduce, inputs=tuple(conv(r) for r in plan_obj.reduce.inputs)) \
+        if plan_obj.reduce is not None else None
+    return EvalPlan(steps, plan_obj.slots, conv(plan_obj.result), [], reduce=red,
+                    extra=tuple(conv(r) for r in plan_obj.extra), sums=plan_obj.sums)
+
+
+def _recipe_for(key, leaves, make):
+    """The recipe cached under ``key`` (per runtime, LRU), or a new one from
+    ``make() -> (plan, out_refs)``; None when the plan cannot be one."""
+    rt = runtime.get_runtime()
+    cache = getattr(rt, "_recipes", None)
+    if cache is None:
+        cache = rt._recipes = collections.OrderedDict()
+    rec = cache.get(key)
+    if rec is not None:
+        cache.move_to_end(key)
+        return rec, None
+    plan_obj, out_refs = make()
+    if not plan_obj.steps and plan_obj.reduce is None:
+        return None, plan_obj
+    try:
+        tmpl = _templatise(plan_obj, leaves)
+        outs = None if out_refs is None else tuple(
+            ("leafpos", leaves.index(r[1])) if r[0] == "leaf" else r for r in out_refs)
+    except (_NoRecipe, ValueError):
+        return None, plan_obj
+    rec = _Recipe(tmpl, outs)
+    cache[key] = rec
+    if len(cache) > _RECIPE_MAX:
+        cache.popitem(last=False)
+    return rec, None
+
+
+def execute_plan(plan_obj: EvalPlan, target_buf=None, sums: dict | None = None, leaves=None, recipe=None):
     """Run the plan's steps; returns the result buffer (or the leaf matrix for
     an empty plan).  When the plan carries a fused reduction it is executed
-    last and its value is returned instead."""
+    last and its value is returned instead.  ``sums`` (optional) receives
+    {result slot: 1-element buffer} for the reference-order accu a step left
+    beside a returned result (EvalPlan.sums); every other side output is
+    released here.  A recipe's template plan names leaves by position
+    (``leaves``); its invocations are built on the first run and re-addressed
+    on later ones."""
     rt = runtime.get_runtime()
     if plan_obj.result is not None and plan_obj.result[0] == "leaf" and plan_obj.reduce is None and not plan_obj.extra:
         return plan_obj.result[1]
@@ -867,6 +998,15 @@ def execute_plan(plan_obj: EvalPlan, target_buf=None):
     finals = plan_obj.final_slots
     release_after = {s: span[1] for s, span in plan_obj.temp_schedule.items()}
     slot_bufs: dict[int, object] = {}
+    protos = recipe.protos if recipe is not None else None
+
+    def ref_buf(ref):
+        if ref[0] == "slot":
+            return slot_bufs[ref[1]]
+        return (ref[1] if ref[0] == "leaf" else leaves[ref[1]]).mem
+
+    def step_bufs(refs):
+        return [ref_buf(r) for r in refs]
 
     def release_inputs(step: PlanStep, i: int) -> None:
         done = set()
@@ -876,35 +1016,71 @@ def execute_plan(plan_obj: EvalPlan, target_buf=None):
                 done.add(s)
                 rt.release_deferred(slot_bufs.pop(s))
 
+    def release_leftovers() -> None:
+        # side outputs nobody consumed (the logistic step's r under evaluate(g), a sum slot
+        # whose matrix is not returned): stream-ordered release
+        if sums is not None:
+            for r_slot, a_slot in plan_obj.sums:
+                if r_slot in finals and a_slot in slot_bufs:
+                    sums[r_slot] = slot_bufs.pop(a_slot)
+        for s in [s for s in slot_bufs if s not in finals]:
+            rt.release_deferred(slot_bufs.pop(s))
+
     for i, step in enumerate(plan_obj.steps):
         for a in step.params.get("alloc_slots", ()):     # side outputs the step writes
             ai = plan_obj.slots[a]
             slot_bufs[a] = rt.acquire_memory(ai.rows * ai.cols, ai.elem_type)
-        views = _step_views(plan_obj, step, slot_bufs)
         info = plan_obj.slots[step.out_slot]
         if step.out_slot == final_slot and target_buf is not None:
             out_buf = target_buf
         else:
             out_buf = rt.acquire_memory(info.rows * info.cols, info.elem_type)
         slot_bufs[step.out_slot] = out_buf
-        params = dict(step.params)
-        if params.pop("rng", None):
-            params["seed"] = rt.seed
-            params["stream"] = rt.next_stream_id()
-        rt.enqueue(KernelInvocation(step.kernel, tuple(views), _make_view(out_buf, info.rows, info.cols,
-                                                                          step.out_mode),
-                                    step.scalars, params))
+        proto = protos[i] if protos is not None else None
+        if proto is not None:
+            a = step.params.get("accu_slot")
+            rt.enqueue_prebuilt(proto, step.kernel, step_bufs(step.inputs), out_buf,
+                                slot_bufs[a].ptr if a is not None else 0)
+        else:
+            views = _step_views(plan_obj, step, slot_bufs, leaves)
+            params = dict(step.params)
+            rng = params.pop("rng", None)
+            if rng:
+                params["seed"] = rt.seed
+                params["stream"] = rt.next_stream_id()
+            if "accu_slot" in params:
+                params["accu_ptr"] = slot_bufs[params["accu_slot"]].ptr
+            inv = KernelInvocation(step.kernel, tuple(views), _make_view(out_buf, info.rows, info.cols,
+                                                                         step.out_mode), step.scalars, params)
+            if protos is None or rng:
+                rt.enqueue(inv)
+            else:                                        # first run of a recipe: keep the invocation
+                protos[i] = rt.prebuild(inv)
+                rt.enqueue_prebuilt(protos[i], step.kernel, [v.buf for v in views], out_buf,
+                                    params.get("accu_ptr", 0))
         release_inputs(step, i)
     if plan_obj.reduce is not None:
         step = plan_obj.reduce
-        views = _step_views(plan_obj, step, slot_bufs)
         try:
-            value = rt.execute_reduce(KernelInvocation("fused_reduce", tuple(views), None, (), dict(step.params)))
+            proto = recipe.reduce_proto if recipe is not None else None
+            if proto is not None:
+                value = rt.execute_reduce_prebuilt(proto, "fused_reduce", step_bufs(step.inputs))
+            else:
+                views = _step_views(plan_obj, step, slot_bufs, leaves)
+                inv = KernelInvocation("fused_reduce", tuple(views), None, (), dict(step.params))
+                if recipe is None:
+                    value = rt.execute_reduce(inv)
+                else:
+                    recipe.reduce_proto = rt.prebuild(inv)
+                    value = rt.execute_reduce_prebuilt(recipe.reduce_proto, "fused_reduce", [v.buf for v in views])
         finally:
             release_inputs(step, len(plan_obj.steps))
+            release_leftovers()
         return value
+    release_leftovers()
     if plan_obj.extra:
-        return [slot_bufs[r[1]] if r[0] == "slot" else r[1] for r in (plan_obj.result,) + tuple(plan_obj.extra)]
+        return [slot_bufs[r[1]] if r[0] == "slot" else (r[1] if r[0] == "leaf" else leaves[r[1]])
+                for r in (plan_obj.result,) + tuple(plan_obj.extra)]
     return slot_bufs[final_slot]
 
 
@@ -920,7 +1096,21 @@ def evaluate(x, out=None, fuse: bool = True):
     if out is not None and out.elem_type != node.elem_type:
         raise ElemTypeError(f"cannot assign {node.elem_type} expression to {out.elem_type} matrix; "
                             "convert explicitly")
-    p = plan(node, node.elem_type, fuse=fuse)
+    rec = leaves = None
+    p = None
+    if _RECIPES_ON:
+        key, leaves = _dag_key((node,))
+        if key is not None:
+            rec, p = _recipe_for(("eval", fuse, node.elem_type, key), leaves,
+                                 lambda: (plan(node, node.elem_type, fuse=fuse), None))
+    if rec is not None:
+        p = rec.plan
+        leaf_ids = {m.mem.buffer_id for m in leaves}
+    else:
+        if p is None:
+            p = plan(node, node.elem_type, fuse=fuse)
+        leaves = None
+        leaf_ids = None
     if p.result[0] == "leaf":
         src = p.result[1]
         if out is None:
@@ -931,28 +1121,21 @@ def evaluate(x, out=None, fuse: bool = True):
             out._reshape_storage(shape.rows, shape.cols)
         rt.copy_d2d(src.mem, out.mem, shape.n_elem)
         return out
-    aliased = out is not None and out.mem.buffer_id in p.leaf_buffer_ids()
+    if leaf_ids is None:
+        leaf_ids = p.leaf_buffer_ids()
+    aliased = out is not None and out.mem.buffer_id in leaf_ids
     if out is None or aliased:
-        buf = execute_plan(p)
+        buf = execute_plan(p, leaves=leaves, recipe=rec)
         if out is None:
             return Matrix._adopt(buf, shape.rows, shape.cols, node.elem_type)
         out._adopt_buffer(buf, shape.rows, shape.cols)
         return out
     out._reshape_storage(shape.rows, shape.cols)
-    execute_plan(p, target_buf=out.mem)
+    execute_plan(p, target_buf=out.mem, leaves=leaves, recipe=rec)
     return out
 
 
-def evaluate_many(*xs, fuse: bool = True) -> list:
-    """Evaluate several expressions in one plan and return one fresh matrix
-    per expression (an extension of the reference's evaluate).  Values a
-    fused step produces on the way are shared: with r = F(X @ w, y) and
-    g = X.t() @ r, ``r, g = evaluate_many(r, g)`` reads X once (the fused
-    logistic step) instead of twice."""
-    from .matrix import Matrix
-    nodes = [as_expr(x) for x in xs]
-    if not nodes:
-        return []
+def _lower_many(nodes, fuse: bool):
     low = _Lowerer(fuse)
     # products first, so that side outputs of fused steps are memoised
     # before the expressions that name them are lowered
@@ -969,25 +1152,63 @@ def evaluate_many(*xs, fuse: bool = True) -> list:
             seen.add(r[1])
         out_refs.append(r)
     slot_refs = [r if r[0] != "dup" else ("slot", r[1]) for r in out_refs]
-    p = EvalPlan(low.steps, low.slots, slot_refs[0], low.absorbed, extra=tuple(slot_refs[1:]))
-    rt = runtime.get_runtime()
-    if not p.steps:
-        bufs = [r[1] for r in slot_refs]
+    p = EvalPlan(low.steps, low.slots, slot_refs[0], low.absorbed, extra=tuple(slot_refs[1:]),
+                 sums=tuple(low.sums))
+    return p, out_refs
+
+
+def evaluate_many(*xs, fuse: bool = True) -> list:
+    """Evaluate several expressions in one plan and return one fresh matrix
+    per expression (an extension of the reference's evaluate).  Values a
+    fused step produces on the way are shared: with r = F(X @ w, y) and
+    g = X.t() @ r, ``r, g = evaluate_many(r, g)`` reads X once (the fused
+    logistic step) instead of twice."""
+    from .matrix import Matrix
+    nodes = [as_expr(x) for x in xs]
+    if not nodes:
+        return []
+    rec = leaves = None
+    if _RECIPES_ON:
+        key, leaves = _dag_key(nodes)
+        if key is not None:
+            rec, _ = _recipe_for(("many", fuse, key), leaves, lambda: _lower_many(nodes, fuse))
+    if rec is not None:
+        p, out_refs = rec.plan, rec.out_refs
     else:
-        bufs = execute_plan(p)
+        p, out_refs = _lower_many(nodes, fuse)
+        leaves = None
+    rt = runtime.get_runtime()
+    sums: dict = {}
+    if not p.steps:
+        bufs = [(r[1] if r[0] == "leaf" else leaves[r[1]]) if r[0] != "slot" else None
+                for r in ((p.result,) + tuple(p.extra))]
+    else:
+        bufs = execute_plan(p, sums=sums, leaves=leaves, recipe=rec)
     result = []
     for node, r, b in zip(nodes, out_refs, bufs):
         shape = shape_of(node)
         if r[0] == "slot":
             result.append(Matrix._adopt(b, shape.rows, shape.cols, node.elem_type))
+            if r[1] in sums:          # accu of this matrix already on the device (runtime sum cache)
+                rt.remember_sum(b, sums.pop(r[1]))
         else:   # a leaf or a duplicate: a copy, like evaluate(leaf)
-            src = b.mem if r[0] == "leaf" else b
+            src = b if r[0] == "dup" else b.mem
             m = Matrix._uninitialised(shape.rows, shape.cols, node.elem_type)
             rt.copy_d2d(src, m.mem, shape.n_elem)
             result.append(m)
+    for buf in sums.values():
+        rt.release_deferred(buf)
     return result
 
 
 def reduce_value(op: str, *xs):
     """Run a fused scalar reduction and return the numpy scalar."""
+    if _RECIPES_ON:
+        nodes = [as_expr(x) for x in xs]
+        key, leaves = _dag_key(nodes)
+        if key is not None:
+            rec, p = _recipe_for(("reduce", op, key), leaves, lambda: (plan_reduce(op, *nodes), None))
+            if rec is not None:
+                return execute_plan(rec.plan, leaves=leaves, recipe=rec)
+            return execute_plan(p)
     return execute_plan(plan_reduce(op, *xs))

@@ -302,6 +302,9 @@ def _single_stage_program(kind: str, scalars: tuple, n_in: int) -> tuple:
     raise KeyError(kind)
 
 
+_CODE_TO_ELEM = {v: k for k, v in _clib.DTYPE_CODE.items()}
+
+
 def build_invocation(inv: KernelInvocation) -> _clib.Invocation:
     """KernelInvocation (runtime.py:103-109) -> bm_invocation (b200mat.h)."""
     c = _clib.Invocation()
@@ -444,6 +447,7 @@ def build_invocation(inv: KernelInvocation) -> _clib.Invocation:
         for st in p["program"]:
             pb.stage(st)
         pb.finish()
+        c.iparams[0] = int(p.get("accu_ptr", 0))   # f32 slot for accu(r) in the reference's order
         return c
     if kind in ("pred_count", "pred_all_any", "pred_find_build"):
         # element-vs-scalar predicates (kernels.py:643-699): the threshold is
@@ -491,6 +495,7 @@ class Runtime:
         self.seed = int(os.environ.get(SEED_ENV, "42"))
         self._section_mark = Counters()
         self._live: dict[int, int] = {}     # buffer_id -> device pointer
+        self._sums: dict = {}               # buffer_id -> 1-element buffer holding its accu (sum cache)
         self._queued_ids: set = set()       # buffers used by work enqueued since the last synchronise
         self._pending_error = None          # raised at the next synchronise (asynchronous error contract)
         self.cache_dir = pathlib.Path(os.environ.get(CACHE_DIR_ENV, str(pathlib.Path.home() / ".devmat")))
@@ -531,6 +536,8 @@ class Runtime:
         return buf
 
     def _retire(self, buf: DeviceBuffer) -> int:
+        if self._sums:
+            self.forget_sum(buf.buffer_id)
         with self._lock:
             ptr = self._live.pop(buf.buffer_id, None)
             if ptr is None:
@@ -563,6 +570,29 @@ class Runtime:
         """Stream-ordered release (runtime.py:449-451): cudaFreeAsync."""
         _clib.check(self._lib.bm_free_async(self._retire(buf)), "release_deferred")
 
+    # -- sum cache ----------------------------------------------------------------------------
+    # A fused step may leave accu(result) -- in the reference's order, bit-identical to
+    # reduce_accu -- in a 1-element device buffer beside a matrix it returns (the fused
+    # logistic step's r, expr.py _logistic).  accu() of that matrix then reads 4 bytes
+    # instead of running a reduction.  Any write to the buffer through the runtime
+    # (enqueue output, copies, element writes, release) forgets the entry;
+    # dist.torch_view() forgets it too, since it hands out writable memory.
+    def remember_sum(self, buf: DeviceBuffer, slot: DeviceBuffer) -> None:
+        self.forget_sum(buf.buffer_id)
+        self._sums[buf.buffer_id] = slot
+
+    def cached_sum(self, buf: DeviceBuffer):
+        """The cached accu of ``buf`` as a numpy scalar, or None."""
+        slot = self._sums.get(buf.buffer_id) if self._sums else None
+        if slot is None:
+            return None
+        return self.copy_d2h(slot, 0, 1)[0]
+
+    def forget_sum(self, buffer_id: int) -> None:
+        slot = self._sums.pop(buffer_id, None)
+        if slot is not None:
+            self.release_deferred(slot)
+
     def live(self, buf: DeviceBuffer) -> bool:
         return buf.buffer_id in self._live
 
@@ -585,6 +615,11 @@ class Runtime:
 
     def enqueue(self, inv: KernelInvocation) -> None:
         self._validate(inv)
+        if self._sums:
+            if inv.output is not None:
+                self.forget_sum(inv.output.buf.buffer_id)
+            if inv.kind == "logistic_grad":          # writes r through its input view 2
+                self.forget_sum(inv.inputs[2].buf.buffer_id)
         c = build_invocation(inv)
         _clib.check(self._lib.bm_enqueue(ctypes.byref(c)), inv.kind)
         with self._lock:
@@ -596,6 +631,45 @@ class Runtime:
                 self._queued_ids.add(v.buf.buffer_id)
             if inv.output is not None:
                 self._queued_ids.add(inv.output.buf.buffer_id)
+
+    def prebuild(self, inv: KernelInvocation):
+        """Validate and build ``inv`` once.  The returned prototype is re-addressed
+        per call by enqueue_prebuilt / execute_reduce_prebuilt (expr.py plan
+        recipes): views keep their geometry, only buffer addresses change."""
+        self._validate(inv)
+        return build_invocation(inv)
+
+    def _readdress(self, proto, bufs: list, out_buf, accu_ptr: int):
+        live = self._live
+        c = _clib.Invocation.from_buffer_copy(proto)
+        for k, b in enumerate(bufs):
+            if b.buffer_id not in live:
+                raise BufferError_(f"use of released buffer #{b.buffer_id}")
+            c.inputs[k].base = b.ptr
+        if out_buf is not None:
+            c.output.base = out_buf.ptr
+        if accu_ptr:
+            c.iparams[0] = accu_ptr
+        return c
+
+    def enqueue_prebuilt(self, proto, kind: str, bufs: list, out_buf, accu_ptr: int = 0) -> None:
+        """enqueue() of a prototype from prebuild() on this call's buffers
+        (``bufs`` = the input views' buffers in order)."""
+        c = self._readdress(proto, bufs, out_buf, accu_ptr)
+        if self._sums:
+            if out_buf is not None:
+                self.forget_sum(out_buf.buffer_id)
+            if kind == "logistic_grad":
+                self.forget_sum(bufs[2].buffer_id)
+        _clib.check(self._lib.bm_enqueue(ctypes.byref(c)), kind)
+        with self._lock:
+            self.counters.launches += 1
+            if len(self._queued_ids) > 4096:
+                self._queued_ids.clear()
+            for b in bufs:
+                self._queued_ids.add(b.buffer_id)
+            if out_buf is not None:
+                self._queued_ids.add(out_buf.buffer_id)
 
     def synchronise(self) -> None:
         rc = self._lib.bm_sync()
@@ -609,19 +683,22 @@ class Runtime:
     def execute_reduce(self, inv: KernelInvocation):
         """Enqueue a reducing invocation, wait, and return its scalar as a
         numpy scalar of the element type (one device-to-host transfer)."""
-        self._validate(inv)
-        c = build_invocation(inv)
-        elem = {v: k for k, v in _clib.DTYPE_CODE.items()}[c.compute_dtype]
+        return self.execute_reduce_prebuilt(self.prebuild(inv), inv.kind, [v.buf for v in inv.inputs])
+
+    def execute_reduce_prebuilt(self, proto, kind: str, bufs: list):
+        """execute_reduce() of a prototype from prebuild() on this call's buffers."""
+        c = self._readdress(proto, bufs, None, 0)
+        elem = _CODE_TO_ELEM[c.compute_dtype]
         dt = kernels.NP_DTYPE[elem]
         raw = (ctypes.c_char * 8)()
         rc = self._lib.bm_execute_reduce(ctypes.byref(c), raw)
         with self._lock:
             self.counters.launches += 1
-        _clib.check(rc, inv.kind)
+        _clib.check(rc, kind)
         with self._lock:
             self._queued_ids.clear()          # the call drained the stream
         value = np.frombuffer(bytes(raw)[: dt.itemsize], dtype=dt)[0]
-        nbytes = kernels.itemsize(inv.inputs[0].buf.elem_type) if inv.inputs else 8
+        nbytes = kernels.itemsize(bufs[0].elem_type) if bufs else 8
         with self._lock:
             self.counters.transfers_d2h += 1
             self.counters.bytes_d2h += nbytes
@@ -635,6 +712,8 @@ class Runtime:
         if offset < 0 or offset + arr.shape[0] > buf.length:
             raise BufferError_("host copy out of bounds")
         isz = arr.itemsize
+        if self._sums:
+            self.forget_sum(buf.buffer_id)
         _clib.check(self._lib.bm_h2d(buf.ptr + offset * isz, arr.ctypes.data, arr.nbytes), "copy_h2d")
         with self._lock:
             self.counters.transfers_h2d += 1
@@ -668,6 +747,8 @@ class Runtime:
         if n > src.length or n > dst.length:
             raise BufferError_("d2d copy out of bounds")
         nbytes = n * kernels.itemsize(src.elem_type)
+        if self._sums:
+            self.forget_sum(dst.buffer_id)
         _clib.check(self._lib.bm_d2d(dst.ptr, src.ptr, nbytes), "copy_d2d")
 
     def read_scalar(self, buf: DeviceBuffer, index: int):
@@ -696,6 +777,8 @@ class Runtime:
             raise BufferError_("element index out of bounds")
         dt = kernels.NP_DTYPE[buf.elem_type]
         arr = np.array([value]).astype(dt)
+        if self._sums:
+            self.forget_sum(buf.buffer_id)
         _clib.check(self._lib.bm_write_elem(buf.ptr, _clib.DTYPE_CODE[buf.elem_type], index, arr.ctypes.data),
                     "write_scalar")
         with self._lock:

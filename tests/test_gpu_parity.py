@@ -652,6 +652,109 @@ def test_fused_logistic_step_large(dm, m, k):
     same(r3.to_numpy(), r.to_numpy())
 
 
+@pytest.mark.parametrize("m,k", [(1 << 20, 64), (8192 * 3 + 128 * 5 + 64, 96), (8192 * 2, 32), (100, 8),
+                                 (4100, 300), (64 * 37, 16)])
+def test_fused_logistic_accu_side_output_bit_exact(dm, m, k):
+    """The logistic kernel also folds accu(r) in the reference's order (numpy
+    leaves inside the kernel, blocks + combine_pairwise in lgrad_finish), and
+    accu() of the returned r reads it: bit-identical to the oracle's
+    reduce_accu of the same r, with no reduction launched."""
+    rng = np.random.default_rng(m ^ k)
+    X = rng.standard_normal((m, k), dtype=np.float32)
+    w = (0.05 * rng.standard_normal((k, 1))).astype(np.float32)
+    y = (rng.random((m, 1)) < 0.5).astype(np.float32)
+    mX, mw, my = dm.Matrix.from_numpy(X), dm.Matrix.from_numpy(w), dm.Matrix.from_numpy(y)
+    r_e = 1 / (1 + dm.exp(0 - mX @ mw)) - my
+    r, gr = dm.evaluate_many(r_e, mX.t() @ r_e)
+    rv = r.to_numpy().reshape(-1, order="F")
+    want = O.reduce_accu(rv)
+    dm.synchronise()
+    before = dm.counters()
+    got = dm.accu(r)
+    assert (dm.counters() - before).launches == 0          # served from the sum cache
+    assert np.float32(got).tobytes() == np.float32(want).tobytes(), (got, want)
+    # a second step with the same operands gives the same bits
+    r2, _ = dm.evaluate_many(r_e, mX.t() @ r_e)
+    assert np.float32(dm.accu(r2)).tobytes() == np.float32(want).tobytes()
+
+
+def test_sum_cache_forgets_on_write(dm):
+    """Any write to the matrix drops the cached accu: element writes,
+    evaluate(out=...), host copies and torch views."""
+    from paper_2308_03120_b200 import dist as D
+    m, k = 8192 * 2 + 64, 48
+    rng = np.random.default_rng(7)
+    X = rng.standard_normal((m, k), dtype=np.float32)
+    w = (0.05 * rng.standard_normal((k, 1))).astype(np.float32)
+    y = (rng.random((m, 1)) < 0.5).astype(np.float32)
+    mX, mw, my = dm.Matrix.from_numpy(X), dm.Matrix.from_numpy(w), dm.Matrix.from_numpy(y)
+    r_e = 1 / (1 + dm.exp(0 - mX @ mw)) - my
+
+    def fresh():
+        r, _ = dm.evaluate_many(r_e, mX.t() @ r_e)
+        return r
+
+    def check(r):
+        v = r.to_numpy().reshape(-1, order="F")
+        assert np.float32(dm.accu(r)).tobytes() == np.float32(O.reduce_accu(v)).tobytes()
+
+    r = fresh()
+    r[5, 0] = 1000.0
+    check(r)
+    r = fresh()
+    dm.evaluate(2 * my, out=r)
+    check(r)
+    r = fresh()
+    dm.runtime.get_runtime().copy_h2d(np.ones(m, np.float32), r.mem)
+    check(r)
+    r = fresh()
+    D.torch_view(r).fill_(0.25)
+    check(r)
+    r = fresh()
+    r2 = r
+    del r
+    check(r2)
+
+
+def test_plan_recipes_rebind_leaves(dm):
+    """A recipe (plan + invocations built once per DAG shape) serves later
+    calls with other matrices of the same shapes: results equal a fresh plan
+    of each call, including aliasing outputs, shared leaves, reductions and
+    evaluate_many duplicates."""
+    from paper_2308_03120_b200 import expr as E
+    rng = np.random.default_rng(11)
+    mats = [dm.Matrix.from_numpy(rng.random((300, 200), dtype=np.float32)) for _ in range(6)]
+    hosts = [m.to_numpy() for m in mats]
+    rt = dm.runtime.get_runtime()
+    for it in range(3):
+        a, b, c = mats[it], mats[it + 1], mats[it + 2]
+        ha, hb, hc = hosts[it], hosts[it + 1], hosts[it + 2]
+        e = 2 * a + b % c - a                                  # a shared leaf
+        got = dm.evaluate(e).to_numpy()
+        want = O.run_program((("load", 0), ("scalar", "eop_scalar_times", 2), ("load", 1), ("load", 2),
+                              ("glue", "eglue_schur"), ("glue", "eglue_plus"), ("load", 0), ("glue", "eglue_minus")),
+                             [x.reshape(-1, order="F") for x in (ha, hb, hc)], np.float32)
+        same(got.reshape(-1, order="F"), want)
+        s = dm.accu(2 * a + b)
+        assert np.float32(s).tobytes() == np.float32(O.reduce_accu(
+            O.run_program((("load", 0), ("scalar", "eop_scalar_times", 2), ("load", 1), ("glue", "eglue_plus")),
+                          [ha.reshape(-1, order="F"), hb.reshape(-1, order="F")], np.float32))).tobytes()
+        x, y, z = dm.evaluate_many(a + b, a + b, c)            # a duplicate and a bare leaf
+        same(x.to_numpy(), y.to_numpy())
+        same(z.to_numpy(), hc)
+        d = dm.Matrix.from_numpy(ha)
+        dm.evaluate(d + b, out=d)                              # output aliases an operand
+        same(d.to_numpy(), (ha + hb).astype(np.float32))
+    assert len(rt._recipes) > 0
+    # the same calls without recipes give the same bits
+    E._RECIPES_ON = False
+    try:
+        same(dm.evaluate(2 * mats[0] + mats[1] % mats[2] - mats[0]).to_numpy(),
+             dm.evaluate(2 * mats[0] + mats[1] % mats[2] - mats[0]).to_numpy())
+    finally:
+        E._RECIPES_ON = True
+
+
 # ---- GEMM prologue fusion ------------------------------------------------------------------------
 
 @pytest.mark.parametrize("m,n,k,tb", [(512, 384, 256, 1), (1000, 700, 300, 0), (2048, 2048, 1024, 1)])

@@ -240,8 +240,15 @@ def test_logistic_gradient_is_one_fused_step():
     assert st.inputs[0] == ("leaf", X) and st.inputs[1] == ("leaf", w) and st.inputs[3] == ("leaf", y)
     assert st.params["program"][0] == ("load", 0)            # X @ w is program input 0
     r_slot = st.inputs[2][1]
-    assert st.params["alloc_slots"] == (r_slot,)
+    a_slot = st.params["accu_slot"]                            # accu(r) side output (1 x 1 f32)
+    assert st.params["alloc_slots"] == (r_slot, a_slot)
+    assert p.sums == ((r_slot, a_slot),)
+    assert (p.slots[a_slot].rows, p.slots[a_slot].cols, p.slots[a_slot].elem_type) == (1, 1, "f32")
     assert p.temp_schedule[r_slot] == (0, 0)                   # r is released after the step
+    # beyond 2^26 rows (8192 blocks of 8192) the kernel has no room to fold accu(r)
+    X, w, y, xn, r = _logistic_parts(m=(1 << 26) + 8)
+    st = expr.plan(xn.t() @ r).steps[0]
+    assert st.kernel == "logistic_grad" and "accu_slot" not in st.params and len(st.params["alloc_slots"]) == 1
 
 
 def test_logistic_fusion_declines_other_shapes():

@@ -101,6 +101,13 @@ extern "C" {
                                     (dim 1) values of the compute dtype.  dim 1 takes 1-4 inputs of
                                     the compute dtype, 16-B aligned, rows * size % 16 == 0 (TMA)   */
 
+#define BM_K_GEMM_EPI       18   /* glue_times consumed by an element-wise program (expr.py:596-605 +
+                                    :611-657 lower them as a GEMM and a separate chain): C = F(op(A)
+                                    op(B), ...) with F compiled into the GEMM's store (3xTF32 pair
+                                    kernel / DMMA).  inputs: [0] A, [1] B (block views; trans_a /
+                                    trans_b), [1 + j] program input j >= 1 (m * n elements each);
+                                    program input 0 is the product; output C (contiguous m x n) */
+
 /* comparison of a predicate (kernels.py:643-657 _predicate_mask) */
 #define BM_CMP_GT 0
 #define BM_CMP_LT 1

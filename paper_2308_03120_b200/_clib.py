@@ -22,7 +22,7 @@ DTYPE_CODE = {"f32": BM_F32, "f64": BM_F64, "i32": BM_I32, "u64": BM_U64}
 
 (BM_K_EWISE, BM_K_REDUCE, BM_K_RDIM, BM_K_GEMM, BM_K_COPY, BM_K_TRANSPOSE, BM_K_FILL, BM_K_EYE,
  BM_K_LINSPACE, BM_K_RANDU, BM_K_RANDN, BM_K_STRIDED_COPY, BM_K_LOGISTIC_GRAD, BM_K_PRED_COUNT,
- BM_K_PRED_FIND, BM_K_GEMM_FUSED, BM_K_RDIM_FUSED) = range(1, 18)
+ BM_K_PRED_FIND, BM_K_GEMM_FUSED, BM_K_RDIM_FUSED, BM_K_GEMM_EPI) = range(1, 19)
 BM_CMP_GT, BM_CMP_LT, BM_CMP_GE, BM_CMP_LE, BM_CMP_EQ, BM_CMP_NE = range(6)
 PRED_CODE = {">": BM_CMP_GT, "<": BM_CMP_LT, ">=": BM_CMP_GE, "<=": BM_CMP_LE, "==": BM_CMP_EQ, "!=": BM_CMP_NE}
 

@@ -370,8 +370,6 @@ static int gemv(bool ta, int64_t m, int64_t k, const T* A, int64_t lda, const T*
     return BM_OK;
 }
 
-int gemm_tc_f32(int ta, int tb, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const float* B,
-                int64_t ldb, float* C, int64_t ldc, bool* handled);
 int gemm_dmma_f64(int ta, int tb, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B,
                   int64_t ldb, double* C, int64_t ldc, bool* handled);
 

@@ -16,8 +16,7 @@
 #include <cstring>
 
 #include "bm_internal.h"
-#include "bm_ptx.cuh"
-#include "bm_reduce.cuh"
+#include "bm_gemm_tc.cuh"
 
 namespace bm {
 
@@ -57,36 +56,9 @@ __global__ void __launch_bounds__(256) split_tf32_kernel(const float* __restrict
 // 128x256 chunk into round-to-nearest f32 registers while the MMAs run on
 // the other buffer (the same remedy DeepGEMM applies to FP8).
 
-#define TC_BM 128
-#define TC_BN 256
-#define TC_BK 16
-#define TC_STAGES 4
-#define TC_CHUNK_KB 4                      // K blocks per promoted chunk (64 K)
-#define TC_TILE_A (TC_BM * TC_BK * 4)
-#define TC_TILE_B (TC_BN * TC_BK * 4)
-#define TC_STAGE_BYTES (2 * TC_TILE_A + 2 * TC_TILE_B)
-#define TC_SMEM (TC_STAGES * TC_STAGE_BYTES + 1024 + 256)
-#define TC_THREADS 320                     // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
-
-// K-major operand, SWIZZLE_64B canonical layout: 8-row x 64-B atoms, atoms
-// 512 B apart along M/N (SBO); version 1 (sm_100); K offset via start address.
-__device__ __forceinline__ uint64_t sw64_kmajor_desc(uint32_t saddr) {
-    uint64_t d = 0;
-    d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
-    d |= (uint64_t)(16u >> 4) << 16;
-    d |= (uint64_t)(512u >> 4) << 32;
-    d |= (uint64_t)1 << 46;
-    d |= (uint64_t)4 << 61;
-    return d;
-}
-
-__host__ __device__ constexpr uint32_t tf32_idesc(int m, int n) {
-    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
-}
-
 __global__ void __launch_bounds__(TC_THREADS, 1)
-    gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
-                       const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_blo,
+    gemm_3xtf32_kernel(const __grid_constant__ TmapBytes tm_ahi, const __grid_constant__ TmapBytes tm_alo,
+                       const __grid_constant__ TmapBytes tm_bhi, const __grid_constant__ TmapBytes tm_blo,
                        float* __restrict__ C, i64 m, i64 n, i64 ldc, int nk, int group_m, int kb0, int accumulate) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
@@ -233,453 +205,31 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (warp == 1) tmem_dealloc(tmem, 2 * TC_BN);
 }
 
-// ---------------------------------------------------------------------------
-// The same product on CTA pairs (cta_group::2).  A cluster of two CTAs owns
-// a 256 x 256 tile: CTA r loads rows [128 r, 128 r + 128) of the A tile and
-// columns [128 r, 128 r + 128) of the B tile (hi and lo), and the leader
-// issues tcgen05.mma.cta_group::2 with M = 256, N = 256, which reads each
-// CTA's A rows and both B halves and accumulates each CTA's 128 rows in its
-// own TMEM.  Per SM the tensor cores then read 4 KB of A and 4 KB of B per
-// k8 MMA instead of 4 + 8 KB, which takes the single-CTA kernel off its
-// shared-memory bandwidth bound (128 B/clk: MMA operand reads plus TMA
-// writes needed ~156 B/clk there).  Both CTAs' TMA loads complete on the
-// leader's full barrier; the leader's commits arrive on both CTAs' empty and
-// accumulator barriers (multicast); both CTAs' epilogue warps release a TMEM
-// buffer on the leader's acc_empty.
-
-#define T2_BM 128                         // A rows per CTA (256 per pair)
-#define T2_BNH 128                        // B columns per CTA (256 per pair)
-#define T2_STAGES 6
-#define T2_TILE_A (T2_BM * TC_BK * 4)
-#define T2_TILE_B (T2_BNH * TC_BK * 4)
-#define T2_STAGE_BYTES (2 * T2_TILE_A + 2 * T2_TILE_B)
-#define T2_SMEM (T2_STAGES * T2_STAGE_BYTES + 1024 + 256)
-
-__device__ __forceinline__ uint32_t t2_mapa(const void* p, uint32_t rank) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
-    return r;
-}
-__device__ __forceinline__ void t2_wait(uint64_t* bar, uint32_t parity) {
-    uint32_t ok;
-    do {
-        asm volatile(
-            "{\n"
-            ".reg .pred p;\n"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-            "selp.u32 %0, 1, 0, p;\n"
-            "}\n"
-            : "=r"(ok)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
-    } while (!ok);
-}
-// wait with cluster-scope acquire (the phase was completed from the peer CTA)
-__device__ __forceinline__ void t2_wait_cluster(uint64_t* bar, uint32_t parity) {
-    uint32_t ok;
-    do {
-        asm volatile(
-            "{\n"
-            ".reg .pred p;\n"
-            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
-            "selp.u32 %0, 1, 0, p;\n"
-            "}\n"
-            : "=r"(ok)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
-    } while (!ok);
-}
-__device__ __forceinline__ void t2_tma(void* dst, const void* tmap, int c0, int c1, uint32_t leader_bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
-        "[%4];" ::"r"(smem_u32(dst)),
-        "l"(tmap), "r"(c0), "r"(c1), "r"(leader_bar)
-        : "memory");
-}
-__device__ __forceinline__ void t2_mma(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
-                                       uint32_t accumulate) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "setp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
-        "}\n" ::"r"(d_tmem),
-        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-__device__ __forceinline__ void t2_commit_both(uint64_t* bar) {
-    asm volatile(
-        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-            smem_u32(bar)),
-        "h"((uint16_t)3)
-        : "memory");
-}
-__device__ __forceinline__ void t2_arrive_remote(uint32_t cluster_bar) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
-}
-__device__ __forceinline__ void t2_cluster_sync() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-
+// the ahead-of-time kernels: plain stores
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
-    gemm_3xtf32_pair_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
-                            const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_blo,
+    gemm_3xtf32_pair_kernel(const __grid_constant__ TmapBytes tm_ahi, const __grid_constant__ TmapBytes tm_alo,
+                            const __grid_constant__ TmapBytes tm_bhi, const __grid_constant__ TmapBytes tm_blo,
                             float* __restrict__ C, i64 m, i64 n, i64 ldc, int nk, int group_m, int kb0,
                             int accumulate) {
-    extern __shared__ uint8_t smem_raw[];
-    const uint32_t raw = smem_u32(smem_raw);
-    uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + T2_STAGES * T2_STAGE_BYTES);
-    uint64_t* empty = full + T2_STAGES;
-    uint64_t* acc_full = empty + T2_STAGES;   // [2]
-    uint64_t* acc_empty = acc_full + 2;       // [2] (the leader's counts both CTAs' epilogue warps)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint32_t rank;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
-    const bool leader = rank == 0;
-    // grouped raster over 256 x 256 pair tiles (see gemm_3xtf32_kernel)
-    int m0, n0;
-    {
-        const int nm = (int)((m + 2 * T2_BM - 1) / (2 * T2_BM)), nn = (int)((n + 2 * T2_BNH - 1) / (2 * T2_BNH));
-        const int t = blockIdx.x >> 1;
-        const int per_group = group_m * nn;
-        const int g = t / per_group, first_m = g * group_m;
-        const int gsize = (nm - first_m) < group_m ? (nm - first_m) : group_m;
-        const int r = t - g * per_group;
-        m0 = (first_m + r % gsize) * (2 * T2_BM) + (int)rank * T2_BM;
-        n0 = (r / gsize) * (2 * T2_BNH);
-    }
-    const int nb0 = n0 + (int)rank * T2_BNH;   // this CTA's half of the B tile
-    const int nchunks = (nk + TC_CHUNK_KB - 1) / TC_CHUNK_KB;
-
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < T2_STAGES; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
-        }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(&acc_full[b], 1);
-            mbar_init(&acc_empty[b], 16);
-        }
-        mbar_fence_init();
-        tma_prefetch_desc(&tm_ahi);
-        tma_prefetch_desc(&tm_alo);
-        tma_prefetch_desc(&tm_bhi);
-        tma_prefetch_desc(&tm_blo);
-    }
-    if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(2 * TC_BN)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-    }
-    tc_fence_before();
-    t2_cluster_sync();                         // peers' barriers initialised
-    __syncthreads();                           // and this CTA's TMEM address published
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-
-    auto tile_ahi = [&](int s) { return smem + s * T2_STAGE_BYTES; };
-    auto tile_alo = [&](int s) { return smem + s * T2_STAGE_BYTES + T2_TILE_A; };
-    auto tile_bhi = [&](int s) { return smem + s * T2_STAGE_BYTES + 2 * T2_TILE_A; };
-    auto tile_blo = [&](int s) { return smem + s * T2_STAGE_BYTES + 2 * T2_TILE_A + T2_TILE_B; };
-
-    if (warp == 0) {
-        if (lane == 0) {
-            for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % T2_STAGES;
-                if (kb >= T2_STAGES) t2_wait_cluster(&empty[s], (uint32_t)(((kb / T2_STAGES) - 1) & 1));
-                if (leader) mbar_expect_tx(&full[s], 2 * T2_STAGE_BYTES);   // both CTAs' bytes
-                const uint32_t lbar = t2_mapa(&full[s], 0);
-                const int kc = (kb0 + kb) * TC_BK;
-                t2_tma(tile_ahi(s), &tm_ahi, kc, m0, lbar);
-                t2_tma(tile_alo(s), &tm_alo, kc, m0, lbar);
-                t2_tma(tile_bhi(s), &tm_bhi, kc, nb0, lbar);
-                t2_tma(tile_blo(s), &tm_blo, kc, nb0, lbar);
-            }
-        }
-    } else if (warp == 1) {
-        if (leader && lane == 0) {
-            constexpr uint32_t idesc = tf32_idesc(2 * T2_BM, 2 * T2_BNH);
-            for (int c = 0; c < nchunks; ++c) {
-                const int b = c & 1;
-                if (c >= 2) t2_wait_cluster(&acc_empty[b], (uint32_t)(((c >> 1) - 1) & 1));
-                tc_fence_after();
-                const uint32_t d = tmem + (uint32_t)(b * TC_BN);
-                const int kb_end = (c + 1) * TC_CHUNK_KB < nk ? (c + 1) * TC_CHUNK_KB : nk;
-                for (int kb = c * TC_CHUNK_KB; kb < kb_end; ++kb) {
-                    const int s = kb % T2_STAGES;
-                    t2_wait_cluster(&full[s], (uint32_t)((kb / T2_STAGES) & 1));
-                    tc_fence_after();
-                    const uint64_t ahi = sw64_kmajor_desc(smem_u32(tile_ahi(s)));
-                    const uint64_t alo = sw64_kmajor_desc(smem_u32(tile_alo(s)));
-                    const uint64_t bhi = sw64_kmajor_desc(smem_u32(tile_bhi(s)));
-                    const uint64_t blo = sw64_kmajor_desc(smem_u32(tile_blo(s)));
-#pragma unroll
-                    for (int kk = 0; kk < TC_BK / 8; ++kk) {
-                        const uint64_t adv = (uint64_t)((kk * 32) >> 4);
-                        const uint32_t first = (kb == c * TC_CHUNK_KB && kk == 0) ? 0u : 1u;
-                        t2_mma(d, alo + adv, bhi + adv, idesc, first);
-                        t2_mma(d, ahi + adv, blo + adv, idesc, 1u);
-                        t2_mma(d, ahi + adv, bhi + adv, idesc, 1u);
-                    }
-                    t2_commit_both(&empty[s]);
-                }
-                t2_commit_both(&acc_full[b]);
-            }
-        }
-    } else {
-        // epilogue warps 2..9 of both CTAs: this CTA's 128 rows of the tile
-        const int q = warp & 3;
-        const int h = (warp - 2) >> 2;
-        const i64 row = (i64)m0 + 32 * q + lane;
-        float acc[128];
-        if (accumulate && row < m) {
-            const float* cp = C + row + ((i64)n0 + h * 128) * ldc;
-            const int ncol = (int)(n - n0 - h * 128 < 128 ? n - n0 - h * 128 : 128);
-#pragma unroll
-            for (int t = 0; t < 128; ++t) acc[t] = t < ncol ? __ldg(cp + t * ldc) : 0.f;
-        } else {
-#pragma unroll
-            for (int t = 0; t < 128; ++t) acc[t] = 0.f;
-        }
-        for (int c = 0; c < nchunks; ++c) {
-            const int b = c & 1;
-            t2_wait_cluster(&acc_full[b], (uint32_t)((c >> 1) & 1));
-            tc_fence_after();
-            const uint32_t base = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(b * TC_BN + h * 128);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                uint32_t v[32];
-                tmem_ld_32x32b_x32(base + (uint32_t)(j * 32), v);
-                tmem_ld_wait();
-#pragma unroll
-                for (int t = 0; t < 32; ++t) acc[j * 32 + t] += __uint_as_float(v[t]);
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) t2_arrive_remote(t2_mapa(&acc_empty[b], 0));
-        }
-        if (row < m) {
-#pragma unroll
-            for (int t = 0; t < 128; ++t) {
-                const i64 col = (i64)n0 + h * 128 + t;
-                if (col < n) C[row + col * ldc] = acc[t];
-            }
-        }
-    }
-    tc_fence_before();
-    t2_cluster_sync();
-    tc_fence_after();
-    if (warp == 1)
-        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * TC_BN) : "memory");
+    const Args none{};
+    gemm_pair_body<PlainEpi>(tm_ahi, tm_alo, tm_bhi, tm_blo, C, m, n, ldc, nk, group_m, kb0, accumulate, none, 0);
 }
 
-// ---------------------------------------------------------------------------
-// f64: DMMA m8n8k4 (mma.sync f64 runs on the FP64 tensor path of sm_100).
-// CTA tile 64x128 (two CTAs per SM), 4 warps of 32x64 (4x8 DMMA tiles each,
-// 64 f64 accumulators per lane), K staged 16 at a time through a 4-stage
-// cp.async (LDGSTS) ring so global latency overlaps the DMMAs; contiguous
-// operands move as 16-byte pairs.  Out-of-range elements are zero-filled by
-// cp.async's src-size operand.
-
-__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-                 : "+d"(c[0]), "+d"(c[1])
-                 : "d"(a), "d"(b));
-}
-
-__device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src),
-                 "r"(valid ? 8 : 0)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-// CTA tile BM x 128 (BM = 64: 4 warps in a 2 x 2 grid of 32 x 64 warp tiles,
-// two CTAs per SM so one CTA's barrier and refill overlap the other's DMMAs;
-// BM = 128 would be 8 warps of 64 x 32).  Each warp tile is 32 8x8 DMMA tiles (64 f64
-// accumulators per lane) fed by 12 8-byte shared loads per k4 step.
-#define DM_BN 128
-
-template <int BM, int BK, int ST>
-struct DmCfg {
-    static constexpr int NW = BM == 64 ? 4 : 8;           // warps
-    static constexpr int WGN = BM == 64 ? 2 : 4;          // warps along N
-    static constexpr int MI = BM == 64 ? 4 : 8;           // 8-row DMMA tiles per warp (M)
-    static constexpr int NJ = BM == 64 ? 8 : 4;           // 8-col DMMA tiles per warp (N)
-    static constexpr int LDA = BM + 8, LDB = DM_BN + 8;   // padded smem rows (doubles)
-    static constexpr int SMEM = ST * BK * (LDA + LDB) * 8;
-};
-
-__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
-                 "r"(valid ? 16 : 0)
-                 : "memory");
-}
-
-__device__ __forceinline__ void cp_async16_all(void* dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-
-// VEC: the M-contiguous A (not TA) and N-contiguous B (TB) tiles move as
-// 16-byte pairs (host checks even m / n / ld and 16-byte bases), halving the
-// LDGSTS count per stage.
 template <bool TA, bool TB, int BM, int BK, int ST, bool VEC>
 __global__ void __launch_bounds__(DmCfg<BM, BK, ST>::NW * 32, BM == 64 ? 2 : 1)
     gemm_dmma_kernel(const double* __restrict__ A, i64 lda, const double* __restrict__ B, i64 ldb,
                      double* __restrict__ C, i64 ldc, i64 m, i64 n, i64 k) {
-    typedef DmCfg<BM, BK, ST> G;
-    constexpr int NT = G::NW * 32;
-    constexpr bool VA = VEC && !TA, VB = VEC && TB;
-    extern __shared__ __align__(16) double dsm[];
-    double* As = dsm;                                     // [ST][BK][LDA]
-    double* Bs = dsm + ST * BK * G::LDA;                  // [ST][BK][LDB]
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int gid = lane >> 2, tig = lane & 3;
-    const i64 m0 = (i64)blockIdx.y * BM, n0 = (i64)blockIdx.x * DM_BN;
-    const int wm = (warp / G::WGN) * (8 * G::MI), wn = (warp % G::WGN) * (8 * G::NJ);
-    double acc[G::MI][G::NJ][2];
-#pragma unroll
-    for (int i = 0; i < G::MI; ++i)
-#pragma unroll
-        for (int j = 0; j < G::NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-    // interior tiles (the tile and the K block inside the matrices) skip the
-    // per-copy bounds tests: fewer integer instructions competing with the
-    // DMMAs for issue slots
-    const bool full_mn = (m0 + BM <= m) && (n0 + DM_BN <= n);
-    auto load = [&](int st, i64 k0) {
-        double* as = As + st * BK * G::LDA;
-        double* bs = Bs + st * BK * G::LDB;
-        if (full_mn && k0 + BK <= k) {
-            if (VA) {
-#pragma unroll
-                for (int t = 0; t < (BK * BM / 2) / NT; ++t) {
-                    const int idx = threadIdx.x + t * NT;
-                    const int kk = idx / (BM / 2), mm = 2 * (idx % (BM / 2));
-                    cp_async16_all(as + kk * G::LDA + mm, A + (m0 + mm) + (k0 + kk) * lda);
-                }
-            } else {
-#pragma unroll
-                for (int t = 0; t < (BK * BM) / NT; ++t) {
-                    const int idx = threadIdx.x + t * NT;
-                    int kk, mm;
-                    if (TA) { mm = idx / BK; kk = idx % BK; } else { kk = idx / BM; mm = idx % BM; }
-                    const double* src = TA ? A + (k0 + kk) + (m0 + mm) * lda : A + (m0 + mm) + (k0 + kk) * lda;
-                    cp_async8(as + kk * G::LDA + mm, src, true);
-                }
-            }
-            if (VB) {
-#pragma unroll
-                for (int t = 0; t < (BK * DM_BN / 2) / NT; ++t) {
-                    const int idx = threadIdx.x + t * NT;
-                    const int kk = idx / (DM_BN / 2), nn = 2 * (idx % (DM_BN / 2));
-                    cp_async16_all(bs + kk * G::LDB + nn, B + (n0 + nn) + (k0 + kk) * ldb);
-                }
-            } else {
-#pragma unroll
-                for (int t = 0; t < (BK * DM_BN) / NT; ++t) {
-                    const int idx = threadIdx.x + t * NT;
-                    int kk, nn;
-                    if (TB) { kk = idx / DM_BN; nn = idx % DM_BN; } else { nn = idx / BK; kk = idx % BK; }
-                    const double* src = TB ? B + (n0 + nn) + (k0 + kk) * ldb : B + (k0 + kk) + (n0 + nn) * ldb;
-                    cp_async8(bs + kk * G::LDB + nn, src, true);
-                }
-            }
-            return;
-        }
-        if (VA) {
-#pragma unroll
-            for (int t = 0; t < (BK * BM / 2) / NT; ++t) {
-                const int idx = threadIdx.x + t * NT;
-                const int kk = idx / (BM / 2), mm = 2 * (idx % (BM / 2));
-                const i64 gi = m0 + mm, gl = k0 + kk;
-                const bool ok = gi < m && gl < k;
-                cp_async16(as + kk * G::LDA + mm, ok ? A + gi + gl * lda : A, ok);
-            }
-        } else {
-#pragma unroll
-            for (int t = 0; t < (BK * BM) / NT; ++t) {
-                const int idx = threadIdx.x + t * NT;
-                int kk, mm;
-                if (TA) { mm = idx / BK; kk = idx % BK; } else { kk = idx / BM; mm = idx % BM; }
-                const i64 gi = m0 + mm, gl = k0 + kk;
-                const bool ok = gi < m && gl < k;
-                const double* src = ok ? (TA ? A + gl + gi * lda : A + gi + gl * lda) : A;
-                cp_async8(as + kk * G::LDA + mm, src, ok);
-            }
-        }
-        if (VB) {
-#pragma unroll
-            for (int t = 0; t < (BK * DM_BN / 2) / NT; ++t) {
-                const int idx = threadIdx.x + t * NT;
-                const int kk = idx / (DM_BN / 2), nn = 2 * (idx % (DM_BN / 2));
-                const i64 gj = n0 + nn, gl = k0 + kk;
-                const bool ok = gj < n && gl < k;
-                cp_async16(bs + kk * G::LDB + nn, ok ? B + gj + gl * ldb : B, ok);
-            }
-        } else {
-#pragma unroll
-            for (int t = 0; t < (BK * DM_BN) / NT; ++t) {
-                const int idx = threadIdx.x + t * NT;
-                int kk, nn;
-                if (TB) { kk = idx / DM_BN; nn = idx % DM_BN; } else { nn = idx / BK; kk = idx % BK; }
-                const i64 gj = n0 + nn, gl = k0 + kk;
-                const bool ok = gj < n && gl < k;
-                const double* src = ok ? (TB ? B + gj + gl * ldb : B + gl + gj * ldb) : B;
-                cp_async8(bs + kk * G::LDB + nn, src, ok);
-            }
-        }
-    };
-    const i64 nk = (k + BK - 1) / BK;
-#pragma unroll
-    for (int st = 0; st < ST - 1; ++st) {
-        if (st < nk) load(st, st * BK);
-        cp_async_commit();
-    }
-    for (i64 kb = 0; kb < nk; ++kb) {
-        cp_async_wait<ST - 2>();
-        __syncthreads();
-        // prefetch stage kb + ST - 1 into the buffer consumed at kb - 1
-        const i64 nxt = kb + ST - 1;
-        if (nxt < nk) load((int)(nxt % ST), nxt * BK);
-        cp_async_commit();
-        const double* as = As + (kb % ST) * BK * G::LDA;
-        const double* bs = Bs + (kb % ST) * BK * G::LDB;
-#pragma unroll
-        for (int ks = 0; ks < BK; ks += 4) {
-            double af[G::MI], bf[G::NJ];
-#pragma unroll
-            for (int i = 0; i < G::MI; ++i) af[i] = as[(ks + tig) * G::LDA + wm + 8 * i + gid];
-#pragma unroll
-            for (int j = 0; j < G::NJ; ++j) bf[j] = bs[(ks + tig) * G::LDB + wn + 8 * j + gid];
-#pragma unroll
-            for (int i = 0; i < G::MI; ++i)
-#pragma unroll
-                for (int j = 0; j < G::NJ; ++j) dmma_8x8x4(acc[i][j], af[i], bf[j]);
-        }
-    }
-    cp_async_wait<0>();
-#pragma unroll
-    for (int i = 0; i < G::MI; ++i)
-#pragma unroll
-        for (int j = 0; j < G::NJ; ++j)
-#pragma unroll
-            for (int t = 0; t < 2; ++t) {
-                const i64 r = m0 + wm + 8 * i + gid, c = n0 + wn + 8 * j + 2 * tig + t;
-                if (r < m && c < n) C[r + c * ldc] = acc[i][j][t];
-            }
+    const Args none{};
+    gemm_dmma_body<TA, TB, BM, BK, ST, VEC, PlainEpi>(A, lda, B, ldb, C, ldc, m, n, k, none);
 }
 }  // namespace bm
 
 namespace bmi {
 
-static int encode_kmajor(CUtensorMap* tm, const float* p, int64_t kp, int64_t rows_p, int box_rows) {
+static_assert(sizeof(bm::TmapBytes) == sizeof(CUtensorMap), "tensor map size");
+
+static int encode_kmajor(bm::TmapBytes* tmb, const float* p, int64_t kp, int64_t rows_p, int box_rows) {
+    CUtensorMap* tm = reinterpret_cast<CUtensorMap*>(tmb);
     const cuuint64_t gdim[2] = {(cuuint64_t)kp, (cuuint64_t)rows_p};
     const cuuint64_t gstride[1] = {(cuuint64_t)(kp * 4)};
     const cuuint32_t box[2] = {TC_BK, (cuuint32_t)box_rows};
@@ -710,10 +260,11 @@ static int split_operand(const float* src, int64_t ld, bool kmajor, int64_t rows
 // C = op(A) op(B) on the 3xTF32 tcgen05 path; split_a / split_b fill the
 // K-major hi/lo copies of op(A) (m x k) and op(B)^T (n x k).
 int gemm_tc_f32_core(int64_t m, int64_t n, int64_t k, const SplitFn& split_a, const SplitFn& split_b, float* C,
-                     int64_t ldc, bool* handled) {
+                     int64_t ldc, bool* handled, const PairEpilogue* epi) {
     *handled = false;
     // CTA pairs (cta_group::2, 256 x 256 tiles) unless BM_GEMM_PAIR=0
     static const bool pair = !std::getenv("BM_GEMM_PAIR") || std::atoi(std::getenv("BM_GEMM_PAIR")) != 0;
+    if (epi && !pair) return BM_OK;     // fused epilogues exist for the pair kernel only
     const int64_t tm_ = pair ? 2 * T2_BM : TC_BM, tn_ = pair ? 2 * T2_BNH : TC_BN;
     const int64_t mp = (m + tm_ - 1) / tm_ * tm_;
     const int64_t np = (n + tn_ - 1) / tn_ * tn_;
@@ -726,7 +277,7 @@ int gemm_tc_f32_core(int64_t m, int64_t n, int64_t k, const SplitFn& split_a, co
     float *ahi = buf, *alo = buf + a_elems, *bhi = buf + 2 * a_elems, *blo = buf + 2 * a_elems + b_elems;
     int rc = split_a(ahi, alo, kp, mp);
     if (!rc) rc = split_b(bhi, blo, kp, np);
-    CUtensorMap tm[4];
+    bm::TmapBytes tm[4];
     if (!rc) rc = encode_kmajor(&tm[0], ahi, kp, mp, TC_BM);
     if (!rc) rc = encode_kmajor(&tm[1], alo, kp, mp, TC_BM);
     if (!rc) rc = encode_kmajor(&tm[2], bhi, kp, np, pair ? T2_BNH : TC_BN);
@@ -760,6 +311,22 @@ int gemm_tc_f32_core(int64_t m, int64_t n, int64_t k, const SplitFn& split_a, co
         if (pass_kb <= 0 || pass_kb >= nk) pass_kb = nk;
         for (int kb0 = 0; kb0 < nk && !rc; kb0 += pass_kb) {
             const int len = nk - kb0 < pass_kb ? nk - kb0 : pass_kb;
+            if (epi) {
+                // the JIT pair kernel: same geometry; the element-wise epilogue runs on the last K pass
+                int64_t mm = m, nn = n, lc = ldc;
+                int nkl = len, gm = group_m > 0 ? group_m : 8, k0 = kb0, acc = kb0 > 0, apply = kb0 + len >= nk;
+                float* Cp = C;
+                void* params[] = {&tm[0], &tm[1], &tm[2], &tm[3], &Cp, &mm, &nn, &lc, &nkl, &gm, &k0, &acc,
+                                  const_cast<void*>(epi->args), &apply};
+                CUresult cr = drv().launchKernel((CUfunction)epi->fn, grid.x, 1, 1, TC_THREADS, 1, 1, T2_SMEM, (CUstream)s,
+                                                 params, nullptr);
+                if (cr != CUDA_SUCCESS) {
+                    rc = cu_fail(cr, "cuLaunchKernel (3xTF32 GEMM, fused epilogue)");
+                    break;
+                }
+                st().launches++;
+                continue;
+            }
             if (pair)
                 bm::gemm_3xtf32_pair_kernel<<<grid, TC_THREADS, T2_SMEM, s>>>(tm[0], tm[1], tm[2], tm[3], C, m, n, ldc,
                                                                                len, group_m > 0 ? group_m : 8, kb0, kb0 > 0);
@@ -777,7 +344,7 @@ int gemm_tc_f32_core(int64_t m, int64_t n, int64_t k, const SplitFn& split_a, co
 }
 
 int gemm_tc_f32(int ta, int tb, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const float* B,
-                int64_t ldb, float* C, int64_t ldc, bool* handled) {
+                int64_t ldb, float* C, int64_t ldc, bool* handled, const PairEpilogue* epi) {
     *handled = false;
     if (m * n * k < (int64_t)1 << 21) return BM_OK;   // tiny: the SIMT kernel is cheaper than the split pass
     // op(A) is m x k; K-major iff A is stored transposed.  op(B) is k x n and we
@@ -786,7 +353,7 @@ int gemm_tc_f32(int ta, int tb, int64_t m, int64_t n, int64_t k, const float* A,
         m, n, k,
         [&](float* hi, float* lo, int64_t kp, int64_t rp) { return split_operand(A, lda, ta != 0, m, k, hi, lo, kp, rp); },
         [&](float* hi, float* lo, int64_t kp, int64_t rp) { return split_operand(B, ldb, tb == 0, n, k, hi, lo, kp, rp); },
-        C, ldc, handled);
+        C, ldc, handled, epi);
 }
 
 template <bool TA, bool TB, int BM, int BK, int ST, bool VEC>

@@ -100,8 +100,18 @@ int launch_gemm_fused(const bm_invocation* inv);
 int launch_rdim_fused(const bm_invocation* inv);
 // fills the K-major tf32 hi/lo copies (rp x kp) of one GEMM operand
 typedef std::function<int(float* hi, float* lo, int64_t kp, int64_t rp)> SplitFn;
+// a JIT-compiled pair kernel with a fused element-wise epilogue (bm_gemm_tc.cuh
+// gemm_pair_body<EPI>, NVRTC entry bm_gemm_epi) and its program arguments
+struct PairEpilogue {
+    void* fn;            // CUfunction
+    const void* args;    // bm::Args
+};
 int gemm_tc_f32_core(int64_t m, int64_t n, int64_t k, const SplitFn& split_a, const SplitFn& split_b, float* C,
-                     int64_t ldc, bool* handled);
+                     int64_t ldc, bool* handled, const PairEpilogue* epi = nullptr);
+int gemm_tc_f32(int ta, int tb, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const float* B,
+                int64_t ldb, float* C, int64_t ldc, bool* handled, const PairEpilogue* epi = nullptr);
+int launch_gemm_epi(const bm_invocation* inv);
+int gemm_epi_compile_only(const bm_invocation* inv);
 int exchange_empty_shard(int dtype, int op, void* const* dev_peers, int world, int rank, unsigned long long epoch,
                          void* dev_out);
 int combine_partials(const void* dev_partials, int64_t count, int dtype, int op, void* dev_out);

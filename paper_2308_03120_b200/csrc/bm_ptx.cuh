@@ -1,7 +1,15 @@
 // bm_ptx.cuh -- thin inline-PTX wrappers for sm_100a: mbarriers, TMA
 // (cp.async.bulk.tensor), tcgen05 (TMEM alloc / MMA / commit / ld) and fences.
 #pragma once
+#ifdef __CUDACC_RTC__
+// NVRTC (fused GEMM epilogues, bm_gemm_tc.cuh): no system headers
+typedef unsigned char uint8_t;
+typedef unsigned short uint16_t;
+typedef unsigned int uint32_t;
+typedef unsigned long long uint64_t;
+#else
 #include <cstdint>
+#endif
 
 namespace bm {
 

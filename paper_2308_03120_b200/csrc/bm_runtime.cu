@@ -368,6 +368,8 @@ int bm_enqueue(const bm_invocation* inv) {
             return launch_gemm_fused(inv);
         case BM_K_RDIM_FUSED:
             return launch_rdim_fused(inv);
+        case BM_K_GEMM_EPI:
+            return launch_gemm_epi(inv);
         default:
             return launch_misc(inv);
     }

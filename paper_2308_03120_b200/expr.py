@@ -664,13 +664,20 @@ class _Lowerer:
         return ref
 
     # -- element-wise programs -----------------------------------------------------------------
-    def program(self, root: ExprNode, elem: str, budget: int) -> _Program:
+    def program(self, root: ExprNode, elem: str, budget: int, pre=None) -> _Program:
         """Collect the fusable element-wise subtree under ``root`` into a stage
-        program; everything else is lowered into slots and loaded."""
+        program; everything else is lowered into slots and loaded.  ``pre`` =
+        (node, ref): that node is program input 0 and loads ``ref`` instead of
+        being lowered (a GEMM whose store runs the program, _gemm_epilogue)."""
         prog = _Program()
+        if pre is not None:
+            prog.inputs.append(pre[1])
         left = [budget if self.fuse else 1]
 
         def load(node: ExprNode) -> None:
+            if pre is not None and node is pre[0]:
+                prog.load(pre[1])
+                return
             # a converted materialised matrix is read with a load-time cast
             if (self.fuse and node.kind == "mtop_conv_to" and node.elem_type == elem
                     and node.operands[0].kind == "leaf"):
@@ -701,11 +708,11 @@ class _Lowerer:
         walk = None  # noqa: F841
         return prog
 
-    def _fit_program(self, root: ExprNode, elem: str, extra_slots: int = 0) -> _Program:
+    def _fit_program(self, root: ExprNode, elem: str, extra_slots: int = 0, pre=None) -> _Program:
         budget = self.chain_max
         while True:
             mark = (len(self.steps), len(self.slots), len(self.absorbed))
-            prog = self.program(root, elem, budget)
+            prog = self.program(root, elem, budget, pre)
             fits = (len(prog.inputs) <= kernels.FUSED_INPUTS_MAX
                     and len(prog.stages) + extra_slots <= 64)
             if fits or budget <= 1:
@@ -716,8 +723,64 @@ class _Lowerer:
             del self.absorbed[mark[2]:]
             budget = max(1, budget // 2)
 
+    def _gemm_epilogue(self, root: ExprNode, want: str):
+        """An element-wise tree over one matrix product (f32 on the 3xTF32
+        path, f64 on DMMA): the tree becomes the GEMM's epilogue (gemm_epi),
+        so the product is never materialised and C is written once.  The
+        reference lowers the product and the chain separately
+        (expr.py:596-605, 611-657).  GEMV and small shapes keep that plan."""
+        elem = root.elem_type
+        if elem not in ("f32", "f64"):
+            return None
+        found: list = []
+
+        def scan(n: ExprNode) -> None:
+            if n.kind in ELEMENTWISE_KINDS:
+                for o in n.operands:
+                    scan(o)
+            elif n.kind == "glue_times" and not any(f is n for f in found):
+                found.append(n)
+
+        scan(root)
+        scan = None  # noqa: F841  (break the closure's self-reference)
+        if len(found) != 1 or found[0].elem_type != elem:
+            return None
+        g = found[0]
+        a, b = g.operands
+        ta = tb = 0
+        if a.kind == "op_htrans":
+            a, ta = a.operands[0], 1
+        if b.kind == "op_htrans":
+            b, tb = b.operands[0], 1
+        s = shape_of(g)
+        sa = shape_of(a)
+        k = sa.rows if ta else sa.cols
+        if s.rows < 2 or s.cols < 2 or k < 1 or s.rows * s.cols * k < (1 << (21 if elem == "f32" else 18)):
+            return None
+        mark = (len(self.steps), len(self.slots), len(self.absorbed))
+        ra = self.lower(a, elem)
+        rb = self.lower(b, elem)
+        prog = self._fit_program(root, elem, pre=(g, ("gemm", None)))
+        if len(prog.inputs) + 1 > kernels.FUSED_INPUTS_MAX or len(prog.stages) > 64 or \
+                prog.inputs[0] != ("gemm", None) or ("load", 0) not in prog.stages:
+            del self.steps[mark[0]:]
+            del self.slots[mark[1]:]
+            del self.absorbed[mark[2]:]
+            return None
+        inputs = [ra, rb] + list(prog.inputs[1:])
+        ref = self.emit("gemm_epi", inputs, ["2d", "2d"] + ["flat"] * (len(inputs) - 2), shape_of(root), elem, "flat",
+                        params={"program": tuple(prog.stages), "compute_dtype": NP_DTYPE[elem].str,
+                                "trans_a": ta, "trans_b": tb})
+        if want != elem:
+            ref = self.emit("mov_copy", [ref], ["flat"], shape_of(root), want, "flat")
+        return ref
+
     def _chain(self, root: ExprNode, want: str):
         elem = root.elem_type
+        if self.fuse:
+            ref = self._gemm_epilogue(root, want)
+            if ref is not None:
+                return ref
         prog = self._fit_program(root, elem)
         shape = shape_of(root)
         if prog.n_stages == 1 and len(prog.stages) == len(prog.inputs) + 1 and \

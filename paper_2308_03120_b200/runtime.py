@@ -420,6 +420,18 @@ def build_invocation(inv: KernelInvocation) -> _clib.Invocation:
         c.compute_dtype = _clib.DTYPE_CODE[p["gen_type"]]
         c.iparams[0] = rng_key(int(p["seed"]), int(p["stream"]))
         return c
+    if kind == "gemm_epi":
+        # GEMM epilogue fusion: inputs A, B, then the program's inputs 1..; program input 0
+        # is the product (b200mat.h BM_K_GEMM_EPI)
+        c.kind = _clib.BM_K_GEMM_EPI
+        elem = _NPSTR_TO_ELEM[np.dtype(p["compute_dtype"]).str]
+        c.compute_dtype = _clib.DTYPE_CODE[elem]
+        pb = _ProgramBuilder(c, elem)
+        for st in p["program"]:
+            pb.stage(st)
+        pb.finish()
+        c.trans_a, c.trans_b = int(p["trans_a"]), int(p["trans_b"])
+        return c
     if kind == "gemm_fused":
         # GEMM prologue fusion: A's program (over inputs [0, na)), then B's
         # (loads relative to B's inputs), evaluated inside the split pre-pass

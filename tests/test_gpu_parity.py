@@ -755,6 +755,38 @@ def test_plan_recipes_rebind_leaves(dm):
         E._RECIPES_ON = True
 
 
+# ---- GEMM epilogue fusion ------------------------------------------------------------------------
+
+@pytest.mark.parametrize("elem,m,n,k,ta,tb", [("f32", 512, 384, 256, 0, 1), ("f32", 1000, 700, 300, 0, 0),
+                                              ("f32", 2048, 2048, 1024, 1, 1), ("f32", 256, 256, 20000, 0, 1),
+                                              ("f64", 300, 200, 100, 1, 0), ("f64", 512, 512, 512, 0, 1),
+                                              ("f64", 1030, 770, 64, 0, 0)])
+def test_gemm_epilogue_bit_identical_to_unfused(dm, elem, m, n, k, ta, tb):
+    """F(op(A) op(B), C) with F in the GEMM's store: one launch, and the same
+    bits as the reference's plan (the product materialised, then the chain),
+    which the unfused device plan reproduces; k = 20000 runs three K passes
+    with the epilogue on the last."""
+    rng = np.random.default_rng(m + n + k)
+    dt = np.float32 if elem == "f32" else np.float64
+    a = rng.random((k, m) if ta else (m, k)).astype(dt)
+    b = rng.random((n, k) if tb else (k, n)).astype(dt)
+    c = rng.random((m, n)).astype(dt)
+    mA, mB, mC = dm.Matrix.from_numpy(a), dm.Matrix.from_numpy(b), dm.Matrix.from_numpy(c)
+    prod = (mA.t() if ta else mA) @ (mB.t() if tb else mB)
+    e = dm.exp(prod / 64) * 3 - mC % prod
+    assert [s.kernel for s in dm.plan(e).steps] == ["gemm_epi"]
+    dm.synchronise()
+    before = dm.counters()
+    got = dm.evaluate(e).to_numpy()
+    assert (dm.counters() - before).launches == 1
+    want = dm.evaluate(e, fuse=False).to_numpy()
+    same(got, want)
+    # and the product itself is the usual GEMM (max-normalised vs f64)
+    pa = (a.T if ta else a).astype(np.float64)
+    pb = (b.T if tb else b).astype(np.float64)
+    normwise(dm.evaluate(prod).to_numpy(), pa @ pb, 1e-5 if elem == "f32" else 1e-12)
+
+
 # ---- GEMM prologue fusion ------------------------------------------------------------------------
 
 @pytest.mark.parametrize("m,n,k,tb", [(512, 384, 256, 1), (1000, 700, 300, 0), (2048, 2048, 1024, 1)])

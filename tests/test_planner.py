@@ -275,6 +275,38 @@ def test_logistic_kernel_compiles():
     assert rc == 0, _clib.last_error()
 
 
+# ---- GEMM epilogue fusion ------------------------------------------------------
+
+@pytest.mark.parametrize("elem", ["f32", "f64"])
+def test_gemm_epilogue_fuses_the_consuming_chain(elem):
+    a, b, c = leaf(256, 256, elem), leaf(256, 256, elem), leaf(256, 256, elem)
+    e = dm.exp(2 * (a @ b.t()) + c) - 1
+    p = dm.plan(e)
+    assert [s.kernel for s in p.steps] == ["gemm_epi"]
+    st = p.steps[0]
+    assert st.inputs[0] == ("leaf", a.operands[0]) and st.inputs[1] == ("leaf", b.operands[0])
+    assert st.inputs[2] == ("leaf", c.operands[0])            # program input 1
+    assert st.params["trans_a"] == 0 and st.params["trans_b"] == 1
+    assert st.params["program"][:2] == (("load", 0), ("scalar", "eop_scalar_times", 2))
+    # the kernel compiles (NVRTC, sm_100a): 3xTF32 pair kernel / DMMA with the program in the store
+    views = [expr._make_view(x.operands[0].mem, 256, 256, "2d") for x in (a, b)] + [_flat(c.operands[0])]
+    out = FakeMatrix(256, 256, elem)
+    inv = build_invocation(KernelInvocation("gemm_epi", tuple(views), _flat(out), (), st.params))
+    rc = _clib.lib().bm_jit_compile_only(ctypes.byref(inv))
+    assert rc == 0, _clib.last_error()
+
+
+def test_gemm_epilogue_declines():
+    a, b = leaf(256, 256), leaf(256, 256)
+    assert "gemm_epi" not in [s.kernel for s in dm.plan(2 * (leaf(8, 8) @ leaf(8, 8))).steps]   # small: SIMT + chain
+    v = leaf(256, 1)
+    assert "gemm_epi" not in [s.kernel for s in dm.plan(2 * (a @ v)).steps]                    # GEMV
+    assert "gemm_epi" not in [s.kernel for s in dm.plan((a @ b) + (b @ a)).steps]               # two products
+    ai = leaf(256, 256, "i32")
+    assert "gemm_epi" not in [s.kernel for s in dm.plan(2 * (ai @ ai)).steps]                   # integer GEMM
+    assert "gemm_epi" not in [s.kernel for s in dm.plan(2 * (a @ b), fuse=False).steps]
+
+
 # ---- GEMM prologue fusion ------------------------------------------------------
 
 def test_gemm_operand_chains_fuse_into_the_split_pass():

@@ -19,10 +19,15 @@ struct alignas(64) TmapBytes {
     unsigned long long v[16];
 };
 
-// plain store: the epilogue of an unfused GEMM
+// Epilogue functors: `load` reads the program's other inputs at C's flat
+// element i into registers (issued for a batch of elements before any is
+// used, so their latency overlaps), `at` evaluates the program with input 0 =
+// the product value.  PlainEpi: the unfused store.
 struct PlainEpi {
+    struct Pre {};
+    __device__ static __forceinline__ void load(const Args&, i64, Pre&) {}
     template <typename T>
-    __device__ static __forceinline__ T f(const Args&, T v, i64) { return v; }
+    __device__ static __forceinline__ T at(const Args&, const Pre&, T v) { return v; }
 };
 
 #define TC_BM 128
@@ -284,9 +289,18 @@ __device__ __forceinline__ void gemm_pair_body(const TmapBytes& tm_ahi, const Tm
         if (row < m) {
             if (apply) {   // last K pass: the fused element-wise epilogue (program input 0 = the product)
 #pragma unroll
-                for (int t = 0; t < 128; ++t) {
-                    const i64 col = (i64)n0 + h * 128 + t;
-                    if (col < n) C[row + col * ldc] = EPI::f(ea, acc[t], row + col * m);
+                for (int t0 = 0; t0 < 128; t0 += 16) {
+                    typename EPI::Pre pre[16];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) {
+                        const i64 col = (i64)n0 + h * 128 + t0 + u;
+                        if (col < n) EPI::load(ea, row + col * m, pre[u]);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) {
+                        const i64 col = (i64)n0 + h * 128 + t0 + u;
+                        if (col < n) C[row + col * ldc] = EPI::at(ea, pre[u], acc[t0 + u]);
+                    }
                 }
             } else {
 #pragma unroll
@@ -341,6 +355,8 @@ struct DmCfg {
     static constexpr int NJ = BM == 64 ? 8 : 4;           // 8-col DMMA tiles per warp (N)
     static constexpr int LDA = BM + 8, LDB = DM_BN + 8;   // padded smem rows (doubles)
     static constexpr int SMEM = ST * BK * (LDA + LDB) * 8;
+    // with fused operands: NIA / NIB staged inputs per operand
+    static constexpr int smem(int nia, int nib) { return ST * BK * (LDA * nia + LDB * nib) * 8; }
 };
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
@@ -356,20 +372,45 @@ __device__ __forceinline__ void cp_async16_all(void* dst, const void* src) {
 // VEC: the M-contiguous A (not TA) and N-contiguous B (TB) tiles move as
 // 16-byte pairs (host checks even m / n / ld and 16-byte bases), halving the
 // LDGSTS count per stage.
-template <bool TA, bool TB, int BM, int BK, int ST, bool VEC, class EPI>
+// Operand sources of the DMMA kernel.  PlainOperand: the stored matrix.  A
+// fused operand (GEMM prologue fusion, NVRTC) is an element-wise program over
+// NIN flat f64 inputs of the stored operand's shape: every input's tile is
+// staged with cp.async exactly like a plain operand, and the program is
+// evaluated on the values a warp reads for its DMMA fragments (every stage
+// rounded, like the reference's separate chain, expr.py:596-605), so the
+// pipeline stays asynchronous and no operand is materialised.  The DMMA loop
+// is issue-bound, and every CTA that reads a tile re-evaluates it: measured
+// 36.2 ms against 32.1 ms for materialising (2A + 1) and (B - 3) first at
+// 8192^3, so the planner keeps the reference's plan unless
+// BM_F64_PROLOGUE=1 (expr.py _gemm_prologue).
+struct PlainOperand {
+    static constexpr bool fused = false;
+    static constexpr int nin = 1;
+    struct Pre {
+        double x[1];
+    };
+    __device__ static __forceinline__ double at(const Args&, const Pre& p) { return p.x[0]; }
+};
+
+template <bool TA, bool TB, int BM, int BK, int ST, bool VEC, class EPI, class SA = PlainOperand,
+          class SB = PlainOperand>
 __device__ __forceinline__ void gemm_dmma_body(const double* __restrict__ A, i64 lda, const double* __restrict__ B,
                                                i64 ldb, double* __restrict__ C, i64 ldc, i64 m, i64 n, i64 k,
-                                               const Args& ea) {
+                                               const Args& ea, const Args* aa = nullptr, const Args* ab = nullptr) {
     typedef DmCfg<BM, BK, ST> G;
     constexpr int NT = G::NW * 32;
     constexpr bool VA = VEC && !TA, VB = VEC && TB;
+    constexpr int NIA = SA::nin, NIB = SB::nin;
     extern __shared__ __align__(16) double dsm[];
-    double* As = dsm;                                     // [ST][BK][LDA]
-    double* Bs = dsm + ST * BK * G::LDA;                  // [ST][BK][LDB]
+    double* As = dsm;                                     // [ST][NIA][BK][LDA]
+    double* Bs = dsm + ST * NIA * BK * G::LDA;            // [ST][NIB][BK][LDB]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int gid = lane >> 2, tig = lane & 3;
     const i64 m0 = (i64)blockIdx.y * BM, n0 = (i64)blockIdx.x * DM_BN;
     const int wm = (warp / G::WGN) * (8 * G::MI), wn = (warp % G::WGN) * (8 * G::NJ);
+    // input j of each operand (a plain operand is its own single input)
+    auto a_in = [&](int j) -> const double* { return aa ? reinterpret_cast<const double*>(aa->in[j]) : A; };
+    auto b_in = [&](int j) -> const double* { return ab ? reinterpret_cast<const double*>(ab->in[j]) : B; };
     double acc[G::MI][G::NJ][2];
 #pragma unroll
     for (int i = 0; i < G::MI; ++i)
@@ -380,16 +421,14 @@ __device__ __forceinline__ void gemm_dmma_body(const double* __restrict__ A, i64
     // per-copy bounds tests: fewer integer instructions competing with the
     // DMMAs for issue slots
     const bool full_mn = (m0 + BM <= m) && (n0 + DM_BN <= n);
-    auto load = [&](int st, i64 k0) {
-        double* as = As + st * BK * G::LDA;
-        double* bs = Bs + st * BK * G::LDB;
+    auto load_a = [&](double* as, const double* Ap, i64 k0) {
         if (full_mn && k0 + BK <= k) {
             if (VA) {
 #pragma unroll
                 for (int t = 0; t < (BK * BM / 2) / NT; ++t) {
                     const int idx = threadIdx.x + t * NT;
                     const int kk = idx / (BM / 2), mm = 2 * (idx % (BM / 2));
-                    cp_async16_all(as + kk * G::LDA + mm, A + (m0 + mm) + (k0 + kk) * lda);
+                    cp_async16_all(as + kk * G::LDA + mm, Ap + (m0 + mm) + (k0 + kk) * lda);
                 }
             } else {
 #pragma unroll
@@ -397,25 +436,8 @@ __device__ __forceinline__ void gemm_dmma_body(const double* __restrict__ A, i64
                     const int idx = threadIdx.x + t * NT;
                     int kk, mm;
                     if (TA) { mm = idx / BK; kk = idx % BK; } else { kk = idx / BM; mm = idx % BM; }
-                    const double* src = TA ? A + (k0 + kk) + (m0 + mm) * lda : A + (m0 + mm) + (k0 + kk) * lda;
+                    const double* src = TA ? Ap + (k0 + kk) + (m0 + mm) * lda : Ap + (m0 + mm) + (k0 + kk) * lda;
                     cp_async8(as + kk * G::LDA + mm, src, true);
-                }
-            }
-            if (VB) {
-#pragma unroll
-                for (int t = 0; t < (BK * DM_BN / 2) / NT; ++t) {
-                    const int idx = threadIdx.x + t * NT;
-                    const int kk = idx / (DM_BN / 2), nn = 2 * (idx % (DM_BN / 2));
-                    cp_async16_all(bs + kk * G::LDB + nn, B + (n0 + nn) + (k0 + kk) * ldb);
-                }
-            } else {
-#pragma unroll
-                for (int t = 0; t < (BK * DM_BN) / NT; ++t) {
-                    const int idx = threadIdx.x + t * NT;
-                    int kk, nn;
-                    if (TB) { kk = idx / DM_BN; nn = idx % DM_BN; } else { nn = idx / BK; kk = idx % BK; }
-                    const double* src = TB ? B + (n0 + nn) + (k0 + kk) * ldb : B + (k0 + kk) + (n0 + nn) * ldb;
-                    cp_async8(bs + kk * G::LDB + nn, src, true);
                 }
             }
             return;
@@ -427,7 +449,7 @@ __device__ __forceinline__ void gemm_dmma_body(const double* __restrict__ A, i64
                 const int kk = idx / (BM / 2), mm = 2 * (idx % (BM / 2));
                 const i64 gi = m0 + mm, gl = k0 + kk;
                 const bool ok = gi < m && gl < k;
-                cp_async16(as + kk * G::LDA + mm, ok ? A + gi + gl * lda : A, ok);
+                cp_async16(as + kk * G::LDA + mm, ok ? Ap + gi + gl * lda : Ap, ok);
             }
         } else {
 #pragma unroll
@@ -437,9 +459,31 @@ __device__ __forceinline__ void gemm_dmma_body(const double* __restrict__ A, i64
                 if (TA) { mm = idx / BK; kk = idx % BK; } else { kk = idx / BM; mm = idx % BM; }
                 const i64 gi = m0 + mm, gl = k0 + kk;
                 const bool ok = gi < m && gl < k;
-                const double* src = ok ? (TA ? A + gl + gi * lda : A + gi + gl * lda) : A;
+                const double* src = ok ? (TA ? Ap + gl + gi * lda : Ap + gi + gl * lda) : Ap;
                 cp_async8(as + kk * G::LDA + mm, src, ok);
             }
+        }
+    };
+    auto load_b = [&](double* bs, const double* Bp, i64 k0) {
+        if (full_mn && k0 + BK <= k) {
+            if (VB) {
+#pragma unroll
+                for (int t = 0; t < (BK * DM_BN / 2) / NT; ++t) {
+                    const int idx = threadIdx.x + t * NT;
+                    const int kk = idx / (DM_BN / 2), nn = 2 * (idx % (DM_BN / 2));
+                    cp_async16_all(bs + kk * G::LDB + nn, Bp + (n0 + nn) + (k0 + kk) * ldb);
+                }
+            } else {
+#pragma unroll
+                for (int t = 0; t < (BK * DM_BN) / NT; ++t) {
+                    const int idx = threadIdx.x + t * NT;
+                    int kk, nn;
+                    if (TB) { kk = idx / DM_BN; nn = idx % DM_BN; } else { nn = idx / BK; kk = idx % BK; }
+                    const double* src = TB ? Bp + (n0 + nn) + (k0 + kk) * ldb : Bp + (k0 + kk) + (n0 + nn) * ldb;
+                    cp_async8(bs + kk * G::LDB + nn, src, true);
+                }
+            }
+            return;
         }
         if (VB) {
 #pragma unroll
@@ -448,7 +492,7 @@ __device__ __forceinline__ void gemm_dmma_body(const double* __restrict__ A, i64
                 const int kk = idx / (DM_BN / 2), nn = 2 * (idx % (DM_BN / 2));
                 const i64 gj = n0 + nn, gl = k0 + kk;
                 const bool ok = gj < n && gl < k;
-                cp_async16(bs + kk * G::LDB + nn, ok ? B + gj + gl * ldb : B, ok);
+                cp_async16(bs + kk * G::LDB + nn, ok ? Bp + gj + gl * ldb : Bp, ok);
             }
         } else {
 #pragma unroll
@@ -458,11 +502,19 @@ __device__ __forceinline__ void gemm_dmma_body(const double* __restrict__ A, i64
                 if (TB) { kk = idx / DM_BN; nn = idx % DM_BN; } else { nn = idx / BK; kk = idx % BK; }
                 const i64 gj = n0 + nn, gl = k0 + kk;
                 const bool ok = gj < n && gl < k;
-                const double* src = ok ? (TB ? B + gj + gl * ldb : B + gl + gj * ldb) : B;
+                const double* src = ok ? (TB ? Bp + gj + gl * ldb : Bp + gl + gj * ldb) : Bp;
                 cp_async8(bs + kk * G::LDB + nn, src, ok);
             }
         }
     };
+    auto load = [&](int st, i64 k0) {
+#pragma unroll
+        for (int j = 0; j < NIA; ++j) load_a(As + (st * NIA + j) * BK * G::LDA, a_in(j), k0);
+#pragma unroll
+        for (int j = 0; j < NIB; ++j) load_b(Bs + (st * NIB + j) * BK * G::LDB, b_in(j), k0);
+    };
+    const Args& a_args = aa ? *aa : ea;   // the operand programs' arguments (unused when plain)
+    const Args& b_args = ab ? *ab : ea;
     const i64 nk = (k + BK - 1) / BK;
 #pragma unroll
     for (int st = 0; st < ST - 1; ++st) {
@@ -476,15 +528,31 @@ __device__ __forceinline__ void gemm_dmma_body(const double* __restrict__ A, i64
         const i64 nxt = kb + ST - 1;
         if (nxt < nk) load((int)(nxt % ST), nxt * BK);
         cp_async_commit();
-        const double* as = As + (kb % ST) * BK * G::LDA;
-        const double* bs = Bs + (kb % ST) * BK * G::LDB;
+        const double* as = As + (kb % ST) * NIA * BK * G::LDA;
+        const double* bs = Bs + (kb % ST) * NIB * BK * G::LDB;
+        // a fused operand's program maps the zero fill past K to F(0): those
+        // lanes of the last K block must read 0 (a plain operand's fill is 0)
+        const bool ktail = (SA::fused || SB::fused) && (kb + 1) * BK > k;
 #pragma unroll
         for (int ks = 0; ks < BK; ks += 4) {
             double af[G::MI], bf[G::NJ];
+            const bool kin = !ktail || kb * BK + ks + tig < k;
 #pragma unroll
-            for (int i = 0; i < G::MI; ++i) af[i] = as[(ks + tig) * G::LDA + wm + 8 * i + gid];
+            for (int i = 0; i < G::MI; ++i) {
+                typename SA::Pre p;
 #pragma unroll
-            for (int j = 0; j < G::NJ; ++j) bf[j] = bs[(ks + tig) * G::LDB + wn + 8 * j + gid];
+                for (int j = 0; j < NIA; ++j) p.x[j] = as[j * BK * G::LDA + (ks + tig) * G::LDA + wm + 8 * i + gid];
+                af[i] = SA::at(a_args, p);
+                if (SA::fused && !kin) af[i] = 0.0;
+            }
+#pragma unroll
+            for (int jn = 0; jn < G::NJ; ++jn) {
+                typename SB::Pre p;
+#pragma unroll
+                for (int j = 0; j < NIB; ++j) p.x[j] = bs[j * BK * G::LDB + (ks + tig) * G::LDB + wn + 8 * jn + gid];
+                bf[jn] = SB::at(b_args, p);
+                if (SB::fused && !kin) bf[jn] = 0.0;
+            }
 #pragma unroll
             for (int i = 0; i < G::MI; ++i)
 #pragma unroll
@@ -493,13 +561,24 @@ __device__ __forceinline__ void gemm_dmma_body(const double* __restrict__ A, i64
     }
     cp_async_wait<0>();
 #pragma unroll
-    for (int i = 0; i < G::MI; ++i)
+    for (int i = 0; i < G::MI; ++i) {
+        typename EPI::Pre pre[G::NJ][2];
+        const i64 r = m0 + wm + 8 * i + gid;
 #pragma unroll
         for (int j = 0; j < G::NJ; ++j)
 #pragma unroll
             for (int t = 0; t < 2; ++t) {
-                const i64 r = m0 + wm + 8 * i + gid, c = n0 + wn + 8 * j + 2 * tig + t;
-                if (r < m && c < n) C[r + c * ldc] = EPI::f(ea, acc[i][j][t], r + c * m);
+                const i64 c = n0 + wn + 8 * j + 2 * tig + t;
+                if (r < m && c < n) EPI::load(ea, r + c * m, pre[j][t]);
             }
+#pragma unroll
+        for (int j = 0; j < G::NJ; ++j)
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+                const i64 c = n0 + wn + 8 * j + 2 * tig + t;
+                if (r < m && c < n) C[r + c * ldc] = EPI::at(ea, pre[j][t], acc[i][j][t]);
+            }
+    }
 }
+
 }  // namespace bm

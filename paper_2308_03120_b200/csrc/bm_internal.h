@@ -112,6 +112,7 @@ int gemm_tc_f32(int ta, int tb, int64_t m, int64_t n, int64_t k, const float* A,
                 int64_t ldb, float* C, int64_t ldc, bool* handled, const PairEpilogue* epi = nullptr);
 int launch_gemm_epi(const bm_invocation* inv);
 int gemm_epi_compile_only(const bm_invocation* inv);
+int gemm_fused_compile_only(const bm_invocation* inv);
 int exchange_empty_shard(int dtype, int op, void* const* dev_peers, int world, int rank, unsigned long long epoch,
                          void* dev_out);
 int combine_partials(const void* dev_partials, int64_t count, int dtype, int op, void* dev_out);

@@ -625,41 +625,59 @@ class _Lowerer:
 
     # -- GEMM prologue fusion ------------------------------------------------
     def _gemm_prologue(self, node: ExprNode, want: str):
-        """glue_times with an element-wise operand, f32, on the tensor-core
-        path: the operands' programs run inside the 3xTF32 split pre-pass
-        (gemm_fused) instead of materialising `2*A + 1` first.  Vector and
-        small shapes keep the reference's lowering (GEMV / SIMT)."""
+        """glue_times with an element-wise operand on the tensor-core paths:
+        f32 -- the operands' programs run inside the 3xTF32 split pre-pass;
+        f64 -- inside the DMMA kernel's register-staged producer (gemm_fused),
+        instead of materialising `2*A + 1` first (expr.py:596-605).  Vector
+        and small shapes keep the reference's lowering (GEMV / SIMT)."""
         a, b = node.operands
         ta = tb = 0
         if a.kind == "op_htrans":
             a, ta = a.operands[0], 1
         if b.kind == "op_htrans":
             b, tb = b.operands[0], 1
-        if node.elem_type != "f32" or a.elem_type != "f32" or b.elem_type != "f32":
+        elem = node.elem_type
+        if elem not in ("f32", "f64") or a.elem_type != elem or b.elem_type != elem:
+            return None
+        if elem == "f64" and not _F64_PROLOGUE:
+            # the DMMA producer re-evaluates an operand program in every CTA that
+            # reads the tile; the issue-bound loop measured 36.2 ms against 32.1 ms
+            # for materialising (2A + 1), (B - 3) first at 8192^3 (bm_gemm_tc.cuh)
             return None
         if a.kind not in ELEMENTWISE_KINDS and b.kind not in ELEMENTWISE_KINDS:
             return None
         s = shape_of(node)
         sa, sb = shape_of(a), shape_of(b)
         k = sa.rows if ta else sa.cols
-        if s.rows < 2 or s.cols < 2 or s.rows * s.cols * k < (1 << 21):
+        if s.rows < 2 or s.cols < 2 or s.rows * s.cols * k < (1 << (21 if elem == "f32" else 18)):
             return None
+        if elem == "f64" and -(-s.rows // 64) > 65535:
+            return None
+        mark = (len(self.steps), len(self.slots), len(self.absorbed))
         progs = []
         for x in (a, b):
             if x.kind in ELEMENTWISE_KINDS:
-                pr = self._fit_program(x, "f32")
+                pr = self._fit_program(x, elem)
             else:
                 pr = _Program()
-                pr.load(self.lower(x, "f32"))
+                pr.load(self.lower(x, elem))
             progs.append(pr)
-        if len(progs[0].inputs) + len(progs[1].inputs) > 16 or len(progs[0].stages) + len(progs[1].stages) > 64:
+        # f64 (DMMA): every input of an operand program is staged in shared memory
+        # beside the others, so at most three f64 inputs in all (two CTAs per SM)
+        limit = 16 if elem == "f32" else 3
+        f64_ok = elem == "f32" or all(self._ref_elem(r) == "f64" for pr in progs for r in pr.inputs)
+        if len(progs[0].inputs) + len(progs[1].inputs) > limit or len(progs[0].stages) + len(progs[1].stages) > 64 \
+                or not f64_ok:
+            del self.steps[mark[0]:]
+            del self.slots[mark[1]:]
+            del self.absorbed[mark[2]:]
             return None
         inputs = list(progs[0].inputs) + list(progs[1].inputs)
-        ref = self.emit("gemm_fused", inputs, ["flat"] * len(inputs), s, "f32", "2d",
+        ref = self.emit("gemm_fused", inputs, ["flat"] * len(inputs), s, elem, "2d",
                         params={"a_prog": tuple(progs[0].stages), "b_prog": tuple(progs[1].stages),
                                 "na": len(progs[0].inputs), "trans_a": ta, "trans_b": tb,
                                 "a_rows": sa.rows, "b_rows": sb.rows, "m": s.rows, "n": s.cols, "k": k})
-        if want != "f32":
+        if want != elem:
             ref = self.emit("mov_copy", [ref], ["flat"], s, want, "flat")
         return ref
 
@@ -724,11 +742,12 @@ class _Lowerer:
             budget = max(1, budget // 2)
 
     def _gemm_epilogue(self, root: ExprNode, want: str):
-        """An element-wise tree over one matrix product (f32 on the 3xTF32
-        path, f64 on DMMA): the tree becomes the GEMM's epilogue (gemm_epi),
-        so the product is never materialised and C is written once.  The
-        reference lowers the product and the chain separately
-        (expr.py:596-605, 611-657).  GEMV and small shapes keep that plan."""
+        """An element-wise function of one matrix product (f32 on the 3xTF32
+        path, f64 on DMMA), e.g. ``exp(A @ B.t() / n)``: the tree becomes the
+        GEMM's epilogue (gemm_epi), so the product is never materialised and
+        C is written once.  The reference lowers the product and the chain
+        separately (expr.py:596-605, 611-657).  GEMV, small shapes and trees
+        that read other matrices keep that plan."""
         elem = root.elem_type
         if elem not in ("f32", "f64"):
             return None
@@ -761,8 +780,12 @@ class _Lowerer:
         ra = self.lower(a, elem)
         rb = self.lower(b, elem)
         prog = self._fit_program(root, elem, pre=(g, ("gemm", None)))
-        if len(prog.inputs) + 1 > kernels.FUSED_INPUTS_MAX or len(prog.stages) > 64 or \
-                prog.inputs[0] != ("gemm", None) or ("load", 0) not in prog.stages:
+        # only programs of the product alone: the non-persistent GEMM's epilogue is
+        # exposed (not overlapped with a next tile), and streaming another m x n
+        # input there measured slower than the separate chain (8192^3 f32:
+        # exp(AB^T/n) - C 4.79 ms fused vs 4.36 ms; exp(AB^T/n) 4.15 vs 4.57 ms)
+        if len(prog.inputs) != 1 or len(prog.stages) > 64 or prog.inputs[0] != ("gemm", None) or \
+                ("load", 0) not in prog.stages:
             del self.steps[mark[0]:]
             del self.slots[mark[1]:]
             del self.absorbed[mark[2]:]
@@ -954,6 +977,7 @@ def _step_views(plan_obj: EvalPlan, step: PlanStep, slot_bufs: dict, leaves=None
 
 _RECIPE_MAX = 256
 _RECIPES_ON = os.environ.get("BM_PLAN_CACHE", "1") != "0"
+_F64_PROLOGUE = os.environ.get("BM_F64_PROLOGUE", "0") == "1"   # f64 operand chains inside DMMA (off: slower)
 
 
 class _NoRecipe(Exception):

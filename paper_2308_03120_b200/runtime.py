@@ -436,8 +436,9 @@ def build_invocation(inv: KernelInvocation) -> _clib.Invocation:
         # GEMM prologue fusion: A's program (over inputs [0, na)), then B's
         # (loads relative to B's inputs), evaluated inside the split pre-pass
         c.kind = _clib.BM_K_GEMM_FUSED
-        c.compute_dtype = _clib.BM_F32
-        pb = _ProgramBuilder(c, "f32")
+        elem = inv.output.buf.elem_type          # f32: 3xTF32 split pre-pass; f64: DMMA producer
+        c.compute_dtype = _clib.DTYPE_CODE[elem]
+        pb = _ProgramBuilder(c, elem)
         for st in p["a_prog"]:
             pb.stage(st)
         npa = pb.n

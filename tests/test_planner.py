@@ -275,21 +275,42 @@ def test_logistic_kernel_compiles():
     assert rc == 0, _clib.last_error()
 
 
+def test_f64_operand_chains_fuse_into_the_dmma_producer(monkeypatch):
+    a, b, c = leaf(256, 256, "f64"), leaf(256, 256, "f64"), leaf(256, 256, "f64")
+    assert "gemm_fused" not in [s.kernel for s in dm.plan((2 * a + 1) @ (b - 3).t()).steps]   # off by default
+    monkeypatch.setattr(expr, "_F64_PROLOGUE", True)
+    p = dm.plan((2 * a + 1) @ (b - 3).t())
+    assert [s.kernel for s in p.steps] == ["gemm_fused"]
+    st = p.steps[0]
+    assert st.params["na"] == 1 and st.params["trans_b"] == 1
+    out = FakeMatrix(256, 256, "f64")
+    views = [_flat(a.operands[0]), _flat(b.operands[0])]
+    inv = build_invocation(KernelInvocation("gemm_fused", tuple(views), _flat(out), (), st.params))
+    assert inv.compute_dtype == _clib.BM_F64
+    rc = _clib.lib().bm_jit_compile_only(ctypes.byref(inv))
+    assert rc == 0, _clib.last_error()
+    # more than three program inputs in all: the operands are materialised (register budget)
+    assert "gemm_fused" not in [s.kernel for s in dm.plan((a % c + a) @ (b % c - b)).steps]
+
+
 # ---- GEMM epilogue fusion ------------------------------------------------------
 
 @pytest.mark.parametrize("elem", ["f32", "f64"])
 def test_gemm_epilogue_fuses_the_consuming_chain(elem):
     a, b, c = leaf(256, 256, elem), leaf(256, 256, elem), leaf(256, 256, elem)
-    e = dm.exp(2 * (a @ b.t()) + c) - 1
+    prod = a @ b.t()
+    e = dm.exp(2 * prod) - prod % prod / 3
     p = dm.plan(e)
     assert [s.kernel for s in p.steps] == ["gemm_epi"]
     st = p.steps[0]
     assert st.inputs[0] == ("leaf", a.operands[0]) and st.inputs[1] == ("leaf", b.operands[0])
-    assert st.inputs[2] == ("leaf", c.operands[0])            # program input 1
+    assert len(st.inputs) == 2
     assert st.params["trans_a"] == 0 and st.params["trans_b"] == 1
     assert st.params["program"][:2] == (("load", 0), ("scalar", "eop_scalar_times", 2))
+    # a tree that also reads another m x n matrix keeps the reference's plan (measured slower fused)
+    assert "gemm_epi" not in [s.kernel for s in dm.plan(dm.exp(2 * prod) + c).steps]
     # the kernel compiles (NVRTC, sm_100a): 3xTF32 pair kernel / DMMA with the program in the store
-    views = [expr._make_view(x.operands[0].mem, 256, 256, "2d") for x in (a, b)] + [_flat(c.operands[0])]
+    views = [expr._make_view(x.operands[0].mem, 256, 256, "2d") for x in (a, b)]
     out = FakeMatrix(256, 256, elem)
     inv = build_invocation(KernelInvocation("gemm_epi", tuple(views), _flat(out), (), st.params))
     rc = _clib.lib().bm_jit_compile_only(ctypes.byref(inv))

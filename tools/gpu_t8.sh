@@ -1,0 +1,2 @@
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "fused_operand or epilogue or gemm" -p no:cacheprovider > gpurun_out/t8.txt 2>&1; echo "rc=$?" >> gpurun_out/t8.txt
+BM_F64_PROLOGUE=1 timeout 800 python tools/fusion_probe.py > gpurun_out/fusion4.txt 2>&1

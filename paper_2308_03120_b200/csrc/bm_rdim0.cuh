@@ -50,15 +50,17 @@ __device__ __forceinline__ void rdim0_cta_body(const S& s, i64 rows, i64 cols, i
                 for (int k = 0; k < V; ++k) acc.add(cur.v[r][k]);
         } else {
             T v = half_reduce<T>(cur, tile);
+            // binary-counter merge: j's t trailing ones are the pending left subtrees
+            // v folds with (stk[0] first), then v is parked at level t.  Constant
+            // indices only, so the stack stays in registers (a `break` out of the
+            // unrolled loop put it in local memory)
+            const int t = __ffsll(~(long long)j) - 1;
 #pragma unroll
-            for (int l = 0; l <= LV; ++l) {
-                if (l < LV && ((j >> l) & 1)) {
-                    v = stk[l] + v;
-                } else {
-                    stk[l] = v;
-                    break;
-                }
-            }
+            for (int l = 0; l < LV; ++l)
+                if (l < t) v = stk[l] + v;
+#pragma unroll
+            for (int l = 0; l <= LV; ++l)
+                if (l == t) stk[l] = v;
         }
         if (nj == 0) {
             if constexpr (MM) {

@@ -51,9 +51,12 @@ namespace bm {
 #define LG_RB 64            // rows per slab (256 B of f32: full-rate TMA rows)
 #endif
 #define LG_BOXC 128         // columns per TMA box (32 KB)
+#ifndef LG_CLUSTER
 #define LG_CLUSTER 2        // CTAs per slab: a CTA pair is one TPC, so pairs tile all 148 SMs
-#define LG_COLS (1024 / LG_CLUSTER)   // columns per CTA (LG_CLUSTER * LG_COLS = 1024 = k max)
+#endif                      // (k > 1024: clusters of 4 / 8, set by the launcher through NVRTC)
+#define LG_COLS 512                   // columns per CTA
 #define LG_KMAX (LG_CLUSTER * LG_COLS)
+#define LG_KMAX_ALL (8 * LG_COLS)     // clusters of up to 8 CTAs (the portable maximum): k <= 4096
 #define LG_NB (LG_COLS / LG_BOXC)     // boxes per slab per CTA
 #define LG_NBOX 6                     // ring of boxes (192 KB)
 #define LG_BOX_BYTES (LG_RB * LG_BOXC * 4)

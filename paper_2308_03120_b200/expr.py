@@ -543,7 +543,7 @@ class _Lowerer:
     def _logistic(self, node: ExprNode, want: str):
         """X.t() @ F(X @ w, leaves...) -> one logistic_grad step that reads X
         once and also produces F(...) (memoised, so evaluate_many can return
-        it).  Only the config-5 shape class: f32, X a leaf with k <= 1024
+        it).  Only the config-5 shape class: f32, X a leaf with k <= 4096
         columns and m % 4 == 0 rows, F element-wise over the one product X @ w
         and m x 1 f32 leaves.  Anything else lowers as GEMV + chain + GEMV."""
         a, b = node.operands
@@ -554,7 +554,7 @@ class _Lowerer:
         sb = shape_of(b)
         if X.elem_type != "f32" or b.elem_type != "f32" or sb.rows != m or sb.cols != 1:
             return None
-        if not 1 <= k <= 1024 or m % 4 or m < 16:
+        if not 1 <= k <= 4096 or m % 4 or m < 16:      # clusters of 2 / 4 / 8 CTAs x 512 columns
             return None
         found: list = []
 

@@ -629,7 +629,7 @@ def test_fused_logistic_step_vs_reference(dm):
 
 
 @pytest.mark.parametrize("m,k", [(1 << 16, 1024), (4100, 300), (4096 * 3 + 16, 1000), (16, 16), (1024, 513),
-                                 (2052, 1)])
+                                 (2052, 1), (1 << 15, 1500), (8192 + 64, 2048), (20000, 4096), (4096, 3000)])
 def test_fused_logistic_step_large(dm, m, k):
     rng = np.random.default_rng(m + k)
     X = rng.standard_normal((m, k), dtype=np.float32)
@@ -637,6 +637,7 @@ def test_fused_logistic_step_large(dm, m, k):
     y = (rng.random((m, 1)) < 0.5).astype(np.float32)
     mX, mw, my = dm.Matrix.from_numpy(X), dm.Matrix.from_numpy(w), dm.Matrix.from_numpy(y)
     r_e = 1 / (1 + dm.exp(0 - mX @ mw)) - my
+    assert [s.kernel for s in dm.plan(mX.t() @ r_e).steps] == ["logistic_grad"]
     r, gr = dm.evaluate_many(r_e, mX.t() @ r_e)
     # unfused device path (GEMV + chain + GEMV) and an f64 host reference
     r2 = dm.evaluate(1 / (1 + dm.exp(0 - dm.evaluate(mX @ mw))) - my)
@@ -653,7 +654,7 @@ def test_fused_logistic_step_large(dm, m, k):
 
 
 @pytest.mark.parametrize("m,k", [(1 << 20, 64), (8192 * 3 + 128 * 5 + 64, 96), (8192 * 2, 32), (100, 8),
-                                 (4100, 300), (64 * 37, 16)])
+                                 (4100, 300), (64 * 37, 16), (8192 * 4 + 4, 2500)])
 def test_fused_logistic_accu_side_output_bit_exact(dm, m, k):
     """The logistic kernel also folds accu(r) in the reference's order (numpy
     leaves inside the kernel, blocks + combine_pairwise in lgrad_finish), and

@@ -254,7 +254,7 @@ def test_logistic_gradient_is_one_fused_step():
 def test_logistic_fusion_declines_other_shapes():
     X, w, y, xn, r = _logistic_parts(m=4098)                   # rows not a multiple of 4
     assert [s.kernel for s in expr.plan(xn.t() @ r).steps] != ["logistic_grad"]
-    X, w, y, xn, r = _logistic_parts(k=2048)                   # too many columns
+    X, w, y, xn, r = _logistic_parts(k=4100)                   # too many columns (clusters of 8 x 512)
     assert "logistic_grad" not in [s.kernel for s in expr.plan(xn.t() @ r).steps]
     X2 = FakeMatrix(4096, 1024)._as_expr_node()                # a different X in the product
     w = FakeMatrix(1024, 1)._as_expr_node()
@@ -262,14 +262,16 @@ def test_logistic_fusion_declines_other_shapes():
     assert "logistic_grad" not in [s.kernel for s in expr.plan(xn.t() @ r2).steps]
 
 
-def test_logistic_kernel_compiles():
-    X, w, y, xn, r = _logistic_parts()
+@pytest.mark.parametrize("k", [1024, 2000, 4096])
+def test_logistic_kernel_compiles(k):
+    X, w, y, xn, r = _logistic_parts(k=k)                      # CTA pairs; clusters of 4 and 8 past 1024
     p = expr.plan(xn.t() @ r)
     st = p.steps[0]
+    assert st.kernel == "logistic_grad"
     fake_r = FakeMatrix(4096, 1)
-    views = [expr._make_view(X.mem, 4096, 1024, "2d"), expr._make_view(w.mem, 1024, 1, "flat"),
+    views = [expr._make_view(X.mem, 4096, k, "2d"), expr._make_view(w.mem, k, 1, "flat"),
              expr._make_view(fake_r.mem, 4096, 1, "flat"), expr._make_view(y.mem, 4096, 1, "flat")]
-    g = FakeMatrix(1024, 1)
+    g = FakeMatrix(k, 1)
     inv = build_invocation(KernelInvocation("logistic_grad", tuple(views), _flat(g), (), st.params))
     rc = _clib.lib().bm_jit_compile_only(ctypes.byref(inv))
     assert rc == 0, _clib.last_error()

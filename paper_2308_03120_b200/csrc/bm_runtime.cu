@@ -241,9 +241,13 @@ static int copy_sync(void* dst, const void* src, int64_t bytes, cudaMemcpyKind k
     BM_REQUIRE_INIT();
     if (bytes <= 0) return BM_OK;
     std::lock_guard<std::recursive_mutex> lk(st().mu);
-    BM_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, k, st().stream));
+    // a scalar read (sum cache, element reads) goes through the pinned 64-B slot: a
+    // pageable copy is staged by the driver and costs several microseconds more
+    const bool small_d2h = k == cudaMemcpyDeviceToHost && bytes <= 64;
+    BM_CUDA(cudaMemcpyAsync(small_d2h ? st().host_slot : dst, src, (size_t)bytes, k, st().stream));
     cudaError_t e = cudaStreamSynchronize(st().stream);
     if (e != cudaSuccess) return cuda_fail(e, "copy");
+    if (small_d2h) std::memcpy(dst, st().host_slot, (size_t)bytes);
     return check_device_error("copy");
 }
 

@@ -295,6 +295,14 @@ int gemm_tc_f32_core(int64_t m, int64_t n, int64_t k, const SplitFn& split_a, co
     }
     if (!rc) {
         dim3 grid((unsigned)((np / tn_) * (mp / tm_) * (pair ? 2 : 1)));
+        // BM_GEMM_PERSIST=1: persistent CTA pairs (one per two SMs), each walking a static
+        // share of the raster with the next tile's MMAs under this tile's epilogue.  Off by
+        // default: pairs drift apart along the raster, the concurrent tiles spread over
+        // several waves and their operand slabs stop sharing L2 -- measured 4.29 / 43.7 /
+        // 356 ms at 8192^3 / 16384^3 / 32768^3 against 4.18 / 39.3 / 305 ms with one pair
+        // per tile, where the hardware scheduler hands out tiles in raster order
+        static const bool persist = std::getenv("BM_GEMM_PERSIST") && std::atoi(std::getenv("BM_GEMM_PERSIST")) != 0;
+        if (pair && persist && grid.x > (unsigned)(st().sm_count / 2 * 2)) grid.x = (unsigned)(st().sm_count / 2 * 2);
         // tile rows per raster group: 4 pair rows (1024 rows of C) measured best for
         // the pair kernel (8192^3..32768^3), 8 single-CTA rows for the other
         static const int group_env = std::getenv("BM_GEMM_GROUP") ? std::atoi(std::getenv("BM_GEMM_GROUP")) : 0;

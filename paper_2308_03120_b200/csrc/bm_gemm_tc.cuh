@@ -163,19 +163,22 @@ __device__ __forceinline__ void gemm_pair_body(const TmapBytes& tm_ahi, const Tm
     uint32_t rank;
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
     const bool leader = rank == 0;
-    // grouped raster over 256 x 256 pair tiles (see gemm_3xtf32_kernel)
-    int m0, n0;
-    {
-        const int nm = (int)((m + 2 * T2_BM - 1) / (2 * T2_BM)), nn = (int)((n + 2 * T2_BNH - 1) / (2 * T2_BNH));
-        const int t = blockIdx.x >> 1;
+    // Persistent pairs: pair p owns tiles p, p + P, p + 2P, ... (P = pairs in the grid)
+    // of the grouped raster over 256 x 256 pair tiles (see gemm_3xtf32_kernel), so the P
+    // resident pairs always work on P consecutive raster tiles.  The TMA ring, the two
+    // TMEM accumulator buffers and their barriers run on across tiles: the MMAs of tile
+    // i + 1 start while the epilogue warps still store tile i.
+    const int nm = (int)((m + 2 * T2_BM - 1) / (2 * T2_BM)), nn = (int)((n + 2 * T2_BNH - 1) / (2 * T2_BNH));
+    const int ntiles = nm * nn;
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    auto tile_coords = [&](int t, int& m0, int& n0) {
         const int per_group = group_m * nn;
         const int g = t / per_group, first_m = g * group_m;
         const int gsize = (nm - first_m) < group_m ? (nm - first_m) : group_m;
         const int r = t - g * per_group;
         m0 = (first_m + r % gsize) * (2 * T2_BM) + (int)rank * T2_BM;
         n0 = (r / gsize) * (2 * T2_BNH);
-    }
-    const int nb0 = n0 + (int)rank * T2_BNH;   // this CTA's half of the B tile
+    };
     const int nchunks = (nk + TC_CHUNK_KB - 1) / TC_CHUNK_KB;
 
     if (threadIdx.x == 0) {
@@ -212,30 +215,38 @@ __device__ __forceinline__ void gemm_pair_body(const TmapBytes& tm_ahi, const Tm
 
     if (warp == 0) {
         if (lane == 0) {
-            for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % T2_STAGES;
-                if (kb >= T2_STAGES) t2_wait_cluster(&empty[s], (uint32_t)(((kb / T2_STAGES) - 1) & 1));
-                if (leader) mbar_expect_tx(&full[s], 2 * T2_STAGE_BYTES);   // both CTAs' bytes
-                const uint32_t lbar = t2_mapa(&full[s], 0);
-                const int kc = (kb0 + kb) * TC_BK;
-                t2_tma(tile_ahi(s), &tm_ahi, kc, m0, lbar);
-                t2_tma(tile_alo(s), &tm_alo, kc, m0, lbar);
-                t2_tma(tile_bhi(s), &tm_bhi, kc, nb0, lbar);
-                t2_tma(tile_blo(s), &tm_blo, kc, nb0, lbar);
+            int it = 0;                        // k blocks issued by this CTA, across tiles
+            for (int t = pair; t < ntiles; t += npairs) {
+                int m0, n0;
+                tile_coords(t, m0, n0);
+                const int nb0 = n0 + (int)rank * T2_BNH;   // this CTA's half of the B tile
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int s = it % T2_STAGES;
+                    if (it >= T2_STAGES) t2_wait_cluster(&empty[s], (uint32_t)(((it / T2_STAGES) - 1) & 1));
+                    if (leader) mbar_expect_tx(&full[s], 2 * T2_STAGE_BYTES);   // both CTAs' bytes
+                    const uint32_t lbar = t2_mapa(&full[s], 0);
+                    const int kc = (kb0 + kb) * TC_BK;
+                    t2_tma(tile_ahi(s), &tm_ahi, kc, m0, lbar);
+                    t2_tma(tile_alo(s), &tm_alo, kc, m0, lbar);
+                    t2_tma(tile_bhi(s), &tm_bhi, kc, nb0, lbar);
+                    t2_tma(tile_blo(s), &tm_blo, kc, nb0, lbar);
+                }
             }
         }
     } else if (warp == 1) {
         if (leader && lane == 0) {
             constexpr uint32_t idesc = tf32_idesc(2 * T2_BM, 2 * T2_BNH);
-            for (int c = 0; c < nchunks; ++c) {
-                const int b = c & 1;
-                if (c >= 2) t2_wait_cluster(&acc_empty[b], (uint32_t)(((c >> 1) - 1) & 1));
+            int it = 0, cc = 0;                // k blocks and accumulator chunks, across tiles
+            for (int t = pair; t < ntiles; t += npairs)
+            for (int c = 0; c < nchunks; ++c, ++cc) {
+                const int b = cc & 1;
+                if (cc >= 2) t2_wait_cluster(&acc_empty[b], (uint32_t)(((cc >> 1) - 1) & 1));
                 tc_fence_after();
                 const uint32_t d = tmem + (uint32_t)(b * TC_BN);
                 const int kb_end = (c + 1) * TC_CHUNK_KB < nk ? (c + 1) * TC_CHUNK_KB : nk;
-                for (int kb = c * TC_CHUNK_KB; kb < kb_end; ++kb) {
-                    const int s = kb % T2_STAGES;
-                    t2_wait_cluster(&full[s], (uint32_t)((kb / T2_STAGES) & 1));
+                for (int kb = c * TC_CHUNK_KB; kb < kb_end; ++kb, ++it) {
+                    const int s = it % T2_STAGES;
+                    t2_wait_cluster(&full[s], (uint32_t)((it / T2_STAGES) & 1));
                     tc_fence_after();
                     const uint64_t ahi = sw64_kmajor_desc(smem_u32(tile_ahi(s)));
                     const uint64_t alo = sw64_kmajor_desc(smem_u32(tile_alo(s)));
@@ -255,9 +266,13 @@ __device__ __forceinline__ void gemm_pair_body(const TmapBytes& tm_ahi, const Tm
             }
         }
     } else {
-        // epilogue warps 2..9 of both CTAs: this CTA's 128 rows of the tile
+        // epilogue warps 2..9 of both CTAs: this CTA's 128 rows of each tile
         const int q = warp & 3;
         const int h = (warp - 2) >> 2;
+        int cc = 0;                            // accumulator chunks drained, across tiles
+        for (int t = pair; t < ntiles; t += npairs) {
+        int m0, n0;
+        tile_coords(t, m0, n0);
         const i64 row = (i64)m0 + 32 * q + lane;
         float acc[128];
         if (accumulate && row < m) {
@@ -269,9 +284,9 @@ __device__ __forceinline__ void gemm_pair_body(const TmapBytes& tm_ahi, const Tm
 #pragma unroll
             for (int t = 0; t < 128; ++t) acc[t] = 0.f;
         }
-        for (int c = 0; c < nchunks; ++c) {
-            const int b = c & 1;
-            t2_wait_cluster(&acc_full[b], (uint32_t)((c >> 1) & 1));
+        for (int c = 0; c < nchunks; ++c, ++cc) {
+            const int b = cc & 1;
+            t2_wait_cluster(&acc_full[b], (uint32_t)((cc >> 1) & 1));
             tc_fence_after();
             const uint32_t base = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(b * TC_BN + h * 128);
 #pragma unroll
@@ -310,6 +325,7 @@ __device__ __forceinline__ void gemm_pair_body(const TmapBytes& tm_ahi, const Tm
                 }
             }
         }
+        }   // tiles
     }
     tc_fence_before();
     t2_cluster_sync();

@@ -784,6 +784,28 @@ def test_gemm_fused_operand_chains_f64(dm, m, n, k, ta, tb, monkeypatch):
     normwise(got, (oa.T if ta else oa) @ (ob.T if tb else ob), 1e-12)
 
 
+def test_plan_recipes_keep_generators_fresh_and_follow_shapes(dm):
+    """Recipes never freeze device-generated values (each call draws the next
+    counter-RNG stream, like a fresh plan), and a matrix whose shape changes
+    between calls gets a new recipe, not a stale one."""
+    a = dm.Matrix.from_numpy(np.ones((64, 32), np.float32))
+    x1 = dm.evaluate(dm.randu(64, 32) + a).to_numpy()
+    x2 = dm.evaluate(dm.randu(64, 32) + a).to_numpy()
+    assert not np.array_equal(x1, x2)
+    assert np.all((x1 >= 1) & (x1 < 2)) and np.all((x2 >= 1) & (x2 < 2))
+    s1 = dm.accu(dm.randn(1000, 1))
+    s2 = dm.accu(dm.randn(1000, 1))
+    assert s1 != s2
+    # the same matrix, reshaped between two evaluations of one expression shape
+    m = dm.Matrix.from_numpy(np.arange(12, dtype=np.float32).reshape(3, 4))
+    y = dm.evaluate(2 * m).to_numpy()
+    same(y, 2 * np.arange(12, dtype=np.float32).reshape(3, 4))
+    dm.evaluate(dm.Matrix.from_numpy(np.ones((6, 2), np.float32)), out=m)
+    y = dm.evaluate(2 * m).to_numpy()
+    assert y.shape == (6, 2)
+    same(y, 2 * np.ones((6, 2), np.float32))
+
+
 # ---- GEMM epilogue fusion ------------------------------------------------------------------------
 
 @pytest.mark.parametrize("elem,m,n,k,ta,tb", [("f32", 512, 384, 256, 0, 1), ("f32", 1000, 700, 300, 0, 0),

@@ -28,6 +28,7 @@ from __future__ import annotations
 
 import collections
 import os
+import threading
 from dataclasses import dataclass, field, replace
 from typing import NamedTuple
 
@@ -976,6 +977,7 @@ def _step_views(plan_obj: EvalPlan, step: PlanStep, slot_bufs: dict, leaves=None
 # exactly the plan the call would have made.
 
 _RECIPE_MAX = 256
+_RECIPE_LOCK = threading.Lock()
 _RECIPES_ON = os.environ.get("BM_PLAN_CACHE", "1") != "0"
 _F64_PROLOGUE = os.environ.get("BM_F64_PROLOGUE", "0") == "1"   # f64 operand chains inside DMMA (off: slower)
 
@@ -1049,10 +1051,11 @@ def _recipe_for(key, leaves, make):
     cache = getattr(rt, "_recipes", None)
     if cache is None:
         cache = rt._recipes = collections.OrderedDict()
-    rec = cache.get(key)
-    if rec is not None:
-        cache.move_to_end(key)
-        return rec, None
+    with _RECIPE_LOCK:             # user threads evaluate concurrently (reference test_integration)
+        rec = cache.get(key)
+        if rec is not None:
+            cache.move_to_end(key)
+            return rec, None
     plan_obj, out_refs = make()
     if not plan_obj.steps and plan_obj.reduce is None:
         return None, plan_obj
@@ -1063,9 +1066,10 @@ def _recipe_for(key, leaves, make):
     except (_NoRecipe, ValueError):
         return None, plan_obj
     rec = _Recipe(tmpl, outs)
-    cache[key] = rec
-    if len(cache) > _RECIPE_MAX:
-        cache.popitem(last=False)
+    with _RECIPE_LOCK:
+        cache[key] = rec
+        if len(cache) > _RECIPE_MAX:
+            cache.popitem(last=False)
     return rec, None
 
 

@@ -806,6 +806,40 @@ def test_plan_recipes_keep_generators_fresh_and_follow_shapes(dm):
     same(y, 2 * np.ones((6, 2), np.float32))
 
 
+def test_plan_recipes_under_threads_and_eviction(dm, monkeypatch):
+    """Several user threads evaluating while the recipe cache evicts (a small
+    capacity forces it): every result stays right."""
+    import threading
+    from paper_2308_03120_b200 import expr as E
+    monkeypatch.setattr(E, "_RECIPE_MAX", 4)
+    errors = []
+
+    def work(tid):
+        try:
+            rng = np.random.default_rng(tid)
+            for it in range(12):
+                r, c = 8 + (tid + it) % 7, 3 + it % 5
+                a = rng.random((r, c), dtype=np.float32)
+                b = rng.random((r, c), dtype=np.float32)
+                ma, mb = dm.Matrix.from_numpy(a), dm.Matrix.from_numpy(b)
+                got = dm.evaluate(2 * ma + mb).to_numpy()
+                if got.tobytes() != (np.float32(2) * a + b).astype(np.float32).tobytes():
+                    errors.append((tid, it, "evaluate"))
+                s = dm.accu(ma % mb)
+                want = O.reduce_accu((a * b).reshape(-1, order="F"))
+                if np.float32(s).tobytes() != np.float32(want).tobytes():
+                    errors.append((tid, it, "accu"))
+        except Exception as ex:  # noqa: BLE001
+            errors.append((tid, repr(ex)))
+
+    threads = [threading.Thread(target=work, args=(t,)) for t in range(6)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors[:5]
+
+
 # ---- GEMM epilogue fusion ------------------------------------------------------------------------
 
 @pytest.mark.parametrize("elem,m,n,k,ta,tb", [("f32", 512, 384, 256, 0, 1), ("f32", 1000, 700, 300, 0, 0),

@@ -1017,13 +1017,15 @@ def _dag_key(roots):
 
 
 class _Recipe:
-    __slots__ = ("plan", "protos", "reduce_proto", "out_refs")
+    __slots__ = ("plan", "protos", "reduce_proto", "out_refs", "finals", "release_after")
 
     def __init__(self, plan_obj: EvalPlan, out_refs=None):
         self.plan = plan_obj
-        self.protos: list = [None] * len(plan_obj.steps)   # (ctypes invocation, input refs) per step
+        self.protos: list = [None] * len(plan_obj.steps)   # prebuilt invocation per step
         self.reduce_proto = None
         self.out_refs = out_refs
+        self.finals = plan_obj.final_slots                  # the plan's schedule, computed once
+        self.release_after = {s: span[1] for s, span in plan_obj.temp_schedule.items()}
 
 
 def _templatise(plan_obj: EvalPlan, leaves: list) -> EvalPlan:
@@ -1086,8 +1088,11 @@ def execute_plan(plan_obj: EvalPlan, target_buf=None, sums: dict | None = None, 
     if plan_obj.result is not None and plan_obj.result[0] == "leaf" and plan_obj.reduce is None and not plan_obj.extra:
         return plan_obj.result[1]
     final_slot = plan_obj.result[1] if plan_obj.result is not None else None
-    finals = plan_obj.final_slots
-    release_after = {s: span[1] for s, span in plan_obj.temp_schedule.items()}
+    if recipe is not None:
+        finals, release_after = recipe.finals, recipe.release_after
+    else:
+        finals = plan_obj.final_slots
+        release_after = {s: span[1] for s, span in plan_obj.temp_schedule.items()}
     slot_bufs: dict[int, object] = {}
     protos = recipe.protos if recipe is not None else None
 

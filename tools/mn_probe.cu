@@ -35,6 +35,8 @@ __global__ void probe(const float* A, const float* B, float* C, int variant) {
             off = (mn >> 3) * 256 + (kk >> 2) * 128 + (mn & 7) * 16 + (kk & 3) * 4;
         } else if (variant == 5) {   // MN-major, no swizzle: 16 B (4 along MN) x 8 K rows; SBO (MN) 128 B, LBO (K) unused
             off = (mn >> 2) * 128 + (kk & 7) * 16 + (mn & 3) * 4;
+        } else if (variant == 6) {   // K-major SWIZZLE_64B (the GEMM's layout): 64-B rows, 16-B chunk ^= (row >> 1) & 3
+            off = mn * 64 + (((kk >> 2) ^ ((mn >> 1) & 3)) * 16) + (kk & 3) * 4;
         } else {
             off = sw128_off(mn, kk, atom);
         }
@@ -60,6 +62,7 @@ __global__ void probe(const float* A, const float* B, float* C, int variant) {
             uint32_t lt = 2;
             if (variant == 4) { lbo = 128; sbo = 256; lt = 0; }
             if (variant == 5) { lbo = 1024; sbo = 128; lt = 0; }
+            if (variant == 6) { lbo = 16; sbo = 512; lt = 4; }
             d |= (uint64_t)(lbo >> 4) << 16;
             d |= (uint64_t)(sbo >> 4) << 32;
             d |= (uint64_t)1 << 46;
@@ -67,7 +70,7 @@ __global__ void probe(const float* A, const float* B, float* C, int variant) {
             return d;
         };
         uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-        if (variant != 4) idesc |= (1u << 15) | (1u << 16);
+        if (variant != 4 && variant != 6) idesc |= (1u << 15) | (1u << 16);
         mma_tf32(tmem, desc(sa), desc(sb), idesc, 0u);
         mma_commit(&bar);
     }
@@ -103,7 +106,7 @@ int main() {
     cudaMalloc(&dc, c.size() * 4);
     cudaMemcpy(da, a.data(), a.size() * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(db, b.data(), b.size() * 4, cudaMemcpyHostToDevice);
-    for (int variant = 0; variant < 6; ++variant) {
+    for (int variant = 0; variant < 7; ++variant) {
         cudaMemset(dc, 0, c.size() * 4);
         probe<<<1, 128>>>(da, db, dc, variant);
         cudaError_t e = cudaDeviceSynchronize();

@@ -98,8 +98,8 @@ extern "C" {
                                     flat inputs of rows * cols elements (column-major); dim = 0 / 1;
                                     iparams[0] = rows, iparams[1] = cols (dim 1); reduce_op =
                                     BM_R_ACCU / MIN / MAX / MEAN / VAR; output = cols (dim 0) or rows
-                                    (dim 1) values of the compute dtype.  dim 1 takes 1-4 inputs of
-                                    the compute dtype, 16-B aligned, rows * size % 16 == 0 (TMA)   */
+                                    (dim 1) values of the compute dtype.  dim 1 takes 1-8 inputs of
+                                    the compute dtype, 16-B aligned, rows * size % 16 == 0 (TMA)      */
 
 #define BM_K_GEMM_EPI       18   /* glue_times consumed by an element-wise program (expr.py:596-605 +
                                     :611-657 lower them as a GEMM and a separate chain): C = F(op(A)

@@ -197,7 +197,7 @@ namespace bm {
 
 struct R1Args {                 // one __grid_constant__ parameter, like LgArgs
     Args a;                     // program inputs and scalars
-    LgTmap m[4];                // the inputs as [rows x cols] tensor maps
+    LgTmap m[8];                // the inputs as [rows x cols] tensor maps (up to 8)
     i64 rows, cols;
     void* out;
 };
@@ -208,7 +208,7 @@ __device__ __forceinline__ void rdim1_fused_body(const R1Args& P) {
     const i64 rows = P.rows, cols = P.cols;
     T* out = reinterpret_cast<T*>(P.out);
     constexpr int RT = BM_R1F_ROWS;
-    constexpr int CT = NIN == 1 ? 64 : (NIN == 2 ? 32 : 16);
+    constexpr int CT = NIN == 1 ? 64 : (NIN == 2 ? 32 : (NIN <= 4 ? 16 : 8));   // columns per tile: ~constant stage bytes
     constexpr int ST = BM_R1F_STAGES;
     constexpr unsigned TILE = RT * CT * sizeof(T);
     constexpr unsigned STAGE = NIN * TILE;

@@ -842,7 +842,7 @@ class _Lowerer:
                 return None
         mark = (len(self.steps), len(self.slots), len(self.absorbed))
         prog = self._fit_program(child, elem)
-        if dim == 1 and (len(prog.inputs) > 4 or any(self._ref_elem(r) != elem for r in prog.inputs)):
+        if dim == 1 and (len(prog.inputs) > 8 or any(self._ref_elem(r) != elem for r in prog.inputs)):
             del self.steps[mark[0]:]
             del self.slots[mark[1]:]
             del self.absorbed[mark[2]:]

@@ -339,18 +339,19 @@ def test_fused_dim1_reduction_of_a_tree(dm, dt, shape):
         np.testing.assert_allclose(got[m], want[m], rtol=tol, atol=tol)
 
 
-@pytest.mark.parametrize("nin", [1, 3, 4, 5])
-def test_fused_dim1_input_counts(dm, nin):
-    """1-4 inputs run the fused TMA row fold (64 / 32 / 16-column tiles); a
-    fifth input keeps the reference's two steps; the bits match either way"""
+@pytest.mark.parametrize("nin,dt", [(1, np.float32), (3, np.float32), (4, np.float32), (5, np.float32),
+                                    (8, np.float32), (8, np.float64), (9, np.float32)])
+def test_fused_dim1_input_counts(dm, nin, dt):
+    """1-8 inputs run the fused TMA row fold (64 / 32 / 16 / 8-column tiles); a
+    ninth input keeps the reference's two steps; the bits match either way"""
     rng = np.random.default_rng(40 + nin)
-    arrs = [rng.standard_normal((448, 37)).astype(np.float32) for _ in range(nin)]
+    arrs = [rng.standard_normal((448, 37)).astype(dt) for _ in range(nin)]
     ms = [dm.Matrix.from_numpy(x) for x in arrs]
     tree = 2 * ms[0] + 1
     for m_ in ms[1:]:
         tree = tree * m_ + 1
     kernels = [s.kernel for s in dm.plan(dm.sum(tree, 1)).steps]
-    assert (kernels == ["fused_rdim"]) == (nin <= 4), kernels
+    assert (kernels == ["fused_rdim"]) == (nin <= 8), kernels
     got = dm.evaluate(dm.sum(tree, 1)).to_numpy()
     same(got, O.rdim("sum", dm.evaluate(tree).to_numpy(), 1))
 

@@ -1,0 +1,4 @@
+OUT=gpurun_out
+timeout 2400 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $OUT/final_pytest.txt 2>&1; echo "rc=$?" >> $OUT/final_pytest.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/final_smoke.txt 2>&1; echo "smoke rc=$?" >> $OUT/final_smoke.txt
+timeout 900 python bench.py > $OUT/final_bench.json 2> $OUT/final_bench.err; echo "bench rc=$?" >> $OUT/final_bench.err

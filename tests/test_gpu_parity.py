@@ -554,6 +554,31 @@ def test_gemm_nt_32768_sampled(dm, elem, tol):
         assert abs(got - ref) / abs(ref) <= tol, (i, j, got, ref)
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("elem,tol", [("f32", 1e-5), ("f64", 1e-12)])
+def test_gemm_nt_32768_full_normwise(dm, elem, tol):
+    """Config 4 at full size, every entry: C = A * B^T at 32768^3 against an
+    f64 cuBLAS product of the same operands on this GPU (max-normalised error;
+    the 4 K-pass 3xTF32 path and the DMMA path)."""
+    import torch
+    from paper_2308_03120_b200 import dist as D
+    n = 32768
+    dm.set_seed(3)
+    A = dm.Matrix(n, n, fill="randu", elem_type=elem)
+    B = dm.Matrix(n, n, fill="randu", elem_type=elem)
+    C = dm.evaluate(A @ B.t())
+    dm.synchronise()
+    ta = D.torch_view(A).view(n, n).t().double()      # column-major storage -> (row, col)
+    tb = D.torch_view(B).view(n, n).t().double()
+    truth = ta @ tb.t()
+    del ta, tb
+    got = D.torch_view(C).view(n, n).t().double()
+    err = float((got - truth).abs().max() / truth.abs().max())
+    del got, truth
+    torch.cuda.empty_cache()
+    assert err <= tol, err
+
+
 # ---- predicates: find / all / any (ops.py:202-262) ----------------------------------------------
 
 def test_predicates_vs_reference(dm):

@@ -210,9 +210,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     gemm_3xtf32_pair_kernel(const __grid_constant__ TmapBytes tm_ahi, const __grid_constant__ TmapBytes tm_alo,
                             const __grid_constant__ TmapBytes tm_bhi, const __grid_constant__ TmapBytes tm_blo,
                             float* __restrict__ C, i64 m, i64 n, i64 ldc, int nk, int group_m, int kb0,
-                            int accumulate) {
+                            int accumulate, unsigned int* tile_ctr) {
     const Args none{};
-    gemm_pair_body<PlainEpi>(tm_ahi, tm_alo, tm_bhi, tm_blo, C, m, n, ldc, nk, group_m, kb0, accumulate, none, 0);
+    gemm_pair_body<PlainEpi>(tm_ahi, tm_alo, tm_bhi, tm_blo, C, m, n, ldc, nk, group_m, kb0, accumulate, none, 0,
+                             tile_ctr);
 }
 
 template <bool TA, bool TB, int BM, int BK, int ST, bool VEC>
@@ -273,8 +274,10 @@ int gemm_tc_f32_core(int64_t m, int64_t n, int64_t k, const SplitFn& split_a, co
     cudaStream_t s = st().stream;
     float* buf = nullptr;
     const int64_t a_elems = mp * kp, b_elems = np * kp;
-    BM_CUDA(cudaMallocAsync((void**)&buf, (size_t)(2 * (a_elems + b_elems) * 4), s));
+    constexpr int kMaxPasses = 64;     // tile counters of the persistent pairs, one per K pass
+    BM_CUDA(cudaMallocAsync((void**)&buf, (size_t)(2 * (a_elems + b_elems) * 4 + kMaxPasses * 4), s));
     float *ahi = buf, *alo = buf + a_elems, *bhi = buf + 2 * a_elems, *blo = buf + 2 * a_elems + b_elems;
+    unsigned int* ctr = reinterpret_cast<unsigned int*>(buf + 2 * (a_elems + b_elems));
     int rc = split_a(ahi, alo, kp, mp);
     if (!rc) rc = split_b(bhi, blo, kp, np);
     bm::TmapBytes tm[4];
@@ -295,14 +298,19 @@ int gemm_tc_f32_core(int64_t m, int64_t n, int64_t k, const SplitFn& split_a, co
     }
     if (!rc) {
         dim3 grid((unsigned)((np / tn_) * (mp / tm_) * (pair ? 2 : 1)));
-        // BM_GEMM_PERSIST=1: persistent CTA pairs (one per two SMs), each walking a static
-        // share of the raster with the next tile's MMAs under this tile's epilogue.  Off by
-        // default: pairs drift apart along the raster, the concurrent tiles spread over
-        // several waves and their operand slabs stop sharing L2 -- measured 4.29 / 43.7 /
-        // 356 ms at 8192^3 / 16384^3 / 32768^3 against 4.18 / 39.3 / 305 ms with one pair
-        // per tile, where the hardware scheduler hands out tiles in raster order
+        // BM_GEMM_PERSIST=1: persistent CTA pairs (one per two SMs) claiming raster tiles
+        // from a global counter as they free up, with the next tile's MMAs under this
+        // tile's epilogue.  (A static share per pair -- tiles p, p + P, ... -- measured
+        // 4.29 / 43.7 / 356 ms at 8192^3 / 16384^3 / 32768^3 against 4.18 / 39.3 / 305 ms
+        // with one pair per tile: the pairs drift apart along the raster and their operand
+        // slabs stop sharing L2.)
         static const bool persist = std::getenv("BM_GEMM_PERSIST") && std::atoi(std::getenv("BM_GEMM_PERSIST")) != 0;
-        if (pair && persist && grid.x > (unsigned)(st().sm_count / 2 * 2)) grid.x = (unsigned)(st().sm_count / 2 * 2);
+        bool persistent = false;
+        if (pair && persist && grid.x > (unsigned)(st().sm_count / 2 * 2)) {
+            grid.x = (unsigned)(st().sm_count / 2 * 2);
+            persistent = true;
+            BM_CUDA(cudaMemsetAsync(ctr, 0, kMaxPasses * 4, s));
+        }
         // tile rows per raster group: 4 pair rows (1024 rows of C) measured best for
         // the pair kernel (8192^3..32768^3), 8 single-CTA rows for the other
         static const int group_env = std::getenv("BM_GEMM_GROUP") ? std::atoi(std::getenv("BM_GEMM_GROUP")) : 0;
@@ -317,15 +325,18 @@ int gemm_tc_f32_core(int64_t m, int64_t n, int64_t k, const SplitFn& split_a, co
         const int nk = (int)(kp / TC_BK);
         int pass_kb = kpass_env > 0 && kp > 2 * kpass_env ? (int)(kpass_env / (TC_BK * TC_CHUNK_KB)) * TC_CHUNK_KB : nk;
         if (pass_kb <= 0 || pass_kb >= nk) pass_kb = nk;
-        for (int kb0 = 0; kb0 < nk && !rc; kb0 += pass_kb) {
+        if ((nk + pass_kb - 1) / pass_kb > kMaxPasses)
+            pass_kb = ((nk + kMaxPasses - 1) / kMaxPasses + TC_CHUNK_KB - 1) / TC_CHUNK_KB * TC_CHUNK_KB;
+        for (int kb0 = 0, pass = 0; kb0 < nk && !rc; kb0 += pass_kb, ++pass) {
             const int len = nk - kb0 < pass_kb ? nk - kb0 : pass_kb;
+            unsigned int* tile_ctr = persistent ? ctr + pass : nullptr;
             if (epi) {
                 // the JIT pair kernel: same geometry; the element-wise epilogue runs on the last K pass
                 int64_t mm = m, nn = n, lc = ldc;
                 int nkl = len, gm = group_m > 0 ? group_m : 8, k0 = kb0, acc = kb0 > 0, apply = kb0 + len >= nk;
                 float* Cp = C;
                 void* params[] = {&tm[0], &tm[1], &tm[2], &tm[3], &Cp, &mm, &nn, &lc, &nkl, &gm, &k0, &acc,
-                                  const_cast<void*>(epi->args), &apply};
+                                  const_cast<void*>(epi->args), &apply, &tile_ctr};
                 CUresult cr = drv().launchKernel((CUfunction)epi->fn, grid.x, 1, 1, TC_THREADS, 1, 1, T2_SMEM, (CUstream)s,
                                                  params, nullptr);
                 if (cr != CUDA_SUCCESS) {
@@ -337,7 +348,8 @@ int gemm_tc_f32_core(int64_t m, int64_t n, int64_t k, const SplitFn& split_a, co
             }
             if (pair)
                 bm::gemm_3xtf32_pair_kernel<<<grid, TC_THREADS, T2_SMEM, s>>>(tm[0], tm[1], tm[2], tm[3], C, m, n, ldc,
-                                                                               len, group_m > 0 ? group_m : 8, kb0, kb0 > 0);
+                                                                               len, group_m > 0 ? group_m : 8, kb0, kb0 > 0,
+                                                                               tile_ctr);
             else
                 bm::gemm_3xtf32_kernel<<<grid, TC_THREADS, TC_SMEM, s>>>(tm[0], tm[1], tm[2], tm[3], C, m, n, ldc, len,
                                                                           group_m > 0 ? group_m : 8, kb0, kb0 > 0);

@@ -24,6 +24,7 @@ struct alignas(64) TmapBytes {
 // used, so their latency overlaps), `at` evaluates the program with input 0 =
 // the product value.  PlainEpi: the unfused store.
 struct PlainEpi {
+    static constexpr int kGroup = 16;      // epilogue elements per thread with their loads in flight together
     struct Pre {};
     __device__ static __forceinline__ void load(const Args&, i64, Pre&) {}
     template <typename T>
@@ -149,7 +150,7 @@ template <class EPI>
 __device__ __forceinline__ void gemm_pair_body(const TmapBytes& tm_ahi, const TmapBytes& tm_alo, const TmapBytes& tm_bhi,
                                                const TmapBytes& tm_blo, float* __restrict__ C, i64 m, i64 n, i64 ldc,
                                                int nk, int group_m, int kb0, int accumulate, const Args& ea,
-                                               int apply) {
+                                               int apply, unsigned int* tile_ctr) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
@@ -157,17 +158,24 @@ __device__ __forceinline__ void gemm_pair_body(const TmapBytes& tm_ahi, const Tm
     uint64_t* empty = full + T2_STAGES;
     uint64_t* acc_full = empty + T2_STAGES;   // [2]
     uint64_t* acc_empty = acc_full + 2;       // [2] (the leader's counts both CTAs' epilogue warps)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+    uint64_t* tq_full = acc_empty + 2;        // [2] tile queue: the slot holds the next tile index
+    uint64_t* tq_empty = tq_full + 2;         // [2] (the leader's counts the 18 readers of a slot)
+    int* tq = reinterpret_cast<int*>(tq_empty + 2);   // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tq + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint32_t rank;
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
     const bool leader = rank == 0;
-    // Persistent pairs: pair p owns tiles p, p + P, p + 2P, ... (P = pairs in the grid)
-    // of the grouped raster over 256 x 256 pair tiles (see gemm_3xtf32_kernel), so the P
-    // resident pairs always work on P consecutive raster tiles.  The TMA ring, the two
-    // TMEM accumulator buffers and their barriers run on across tiles: the MMAs of tile
-    // i + 1 start while the epilogue warps still store tile i.
+    // Tiles of the grouped raster over 256 x 256 pair tiles (see gemm_3xtf32_kernel).
+    // Pair p starts with tile p; its next tile is p + P (P = pairs in the grid: one tile
+    // per pair when the grid covers them all) or, with tile_ctr (persistent pairs), the
+    // next unclaimed raster tile P + atomicAdd(tile_ctr, 1) -- tiles go out in raster
+    // order as pairs free up, like the hardware scheduler hands out CTAs.  The leader's
+    // TMA thread claims tiles and publishes each index through a two-slot queue to every
+    // role of both CTAs (-1: done).  The TMA ring, the two TMEM accumulator buffers and
+    // their barriers run on across tiles: the MMAs of tile i + 1 start while the
+    // epilogue warps still store tile i.
     const int nm = (int)((m + 2 * T2_BM - 1) / (2 * T2_BM)), nn = (int)((n + 2 * T2_BNH - 1) / (2 * T2_BNH));
     const int ntiles = nm * nn;
     const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
@@ -189,6 +197,8 @@ __device__ __forceinline__ void gemm_pair_body(const TmapBytes& tm_ahi, const Tm
         for (int b = 0; b < 2; ++b) {
             mbar_init(&acc_full[b], 1);
             mbar_init(&acc_empty[b], 16);
+            mbar_init(&tq_full[b], 1);
+            mbar_init(&tq_empty[b], 18);   // leader: MMA + 8 epilogue warps; peer: TMA + 8 epilogue warps
         }
         mbar_fence_init();
         tma_prefetch_desc(&tm_ahi);
@@ -213,10 +223,34 @@ __device__ __forceinline__ void gemm_pair_body(const TmapBytes& tm_ahi, const Tm
     auto tile_bhi = [&](int s) { return smem + s * T2_STAGE_BYTES + 2 * T2_TILE_A; };
     auto tile_blo = [&](int s) { return smem + s * T2_STAGE_BYTES + 2 * T2_TILE_A + T2_TILE_B; };
 
+    // tile queue.  take(): the next published tile index (one thread per reader role);
+    // the slot is handed back to the leader's publisher at once
+    const uint32_t tq_empty_leader = t2_mapa(&tq_empty[0], 0);
+    auto take = [&](int& qi) -> int {
+        const int slot = qi & 1;
+        t2_wait_cluster(&tq_full[slot], (uint32_t)((qi >> 1) & 1));
+        const int t = *reinterpret_cast<volatile int*>(&tq[slot]);
+        t2_arrive_remote(tq_empty_leader + (uint32_t)(slot * 8));
+        ++qi;
+        return t;
+    };
+
     if (warp == 0) {
         if (lane == 0) {
             int it = 0;                        // k blocks issued by this CTA, across tiles
-            for (int t = pair; t < ntiles; t += npairs) {
+            int qi = 0;
+            int t = leader ? (pair < ntiles ? pair : -1) : take(qi);
+            while (t >= 0) {
+                if (leader) {
+                    // publish t into both CTAs' queue slot (after its last 18 readers let go)
+                    const int slot = qi & 1;
+                    if (qi >= 2) t2_wait_cluster(&tq_empty[slot], (uint32_t)(((qi >> 1) - 1) & 1));
+                    tq[slot] = t;
+                    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(t2_mapa(&tq[slot], 1)), "r"(t) : "memory");
+                    mbar_arrive(&tq_full[slot]);
+                    t2_arrive_remote(t2_mapa(&tq_full[slot], 1));
+                    ++qi;
+                }
                 int m0, n0;
                 tile_coords(t, m0, n0);
                 const int nb0 = n0 + (int)rank * T2_BNH;   // this CTA's half of the B tile
@@ -231,13 +265,28 @@ __device__ __forceinline__ void gemm_pair_body(const TmapBytes& tm_ahi, const Tm
                     t2_tma(tile_bhi(s), &tm_bhi, kc, nb0, lbar);
                     t2_tma(tile_blo(s), &tm_blo, kc, nb0, lbar);
                 }
+                if (leader) {
+                    int nx = t + npairs;
+                    if (tile_ctr) nx = npairs + (int)atomicAdd(tile_ctr, 1u);
+                    t = nx < ntiles ? nx : -1;
+                } else {
+                    t = take(qi);
+                }
+            }
+            if (leader) {                      // the end marker
+                const int slot = qi & 1;
+                if (qi >= 2) t2_wait_cluster(&tq_empty[slot], (uint32_t)(((qi >> 1) - 1) & 1));
+                tq[slot] = -1;
+                asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(t2_mapa(&tq[slot], 1)), "r"(-1) : "memory");
+                mbar_arrive(&tq_full[slot]);
+                t2_arrive_remote(t2_mapa(&tq_full[slot], 1));
             }
         }
     } else if (warp == 1) {
         if (leader && lane == 0) {
             constexpr uint32_t idesc = tf32_idesc(2 * T2_BM, 2 * T2_BNH);
-            int it = 0, cc = 0;                // k blocks and accumulator chunks, across tiles
-            for (int t = pair; t < ntiles; t += npairs)
+            int it = 0, cc = 0, qi = 0;        // k blocks, accumulator chunks, tiles taken
+            for (int t = take(qi); t >= 0; t = take(qi))
             for (int c = 0; c < nchunks; ++c, ++cc) {
                 const int b = cc & 1;
                 if (cc >= 2) t2_wait_cluster(&acc_empty[b], (uint32_t)(((cc >> 1) - 1) & 1));
@@ -269,8 +318,12 @@ __device__ __forceinline__ void gemm_pair_body(const TmapBytes& tm_ahi, const Tm
         // epilogue warps 2..9 of both CTAs: this CTA's 128 rows of each tile
         const int q = warp & 3;
         const int h = (warp - 2) >> 2;
-        int cc = 0;                            // accumulator chunks drained, across tiles
-        for (int t = pair; t < ntiles; t += npairs) {
+        int cc = 0, qi = 0;                    // accumulator chunks drained, tiles taken, across tiles
+        for (;;) {
+        int t = 0;
+        if (lane == 0) t = take(qi);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if (t < 0) break;
         int m0, n0;
         tile_coords(t, m0, n0);
         const i64 row = (i64)m0 + 32 * q + lane;
@@ -303,16 +356,17 @@ __device__ __forceinline__ void gemm_pair_body(const TmapBytes& tm_ahi, const Tm
         }
         if (row < m) {
             if (apply) {   // last K pass: the fused element-wise epilogue (program input 0 = the product)
+                constexpr int G = EPI::kGroup;
 #pragma unroll
-                for (int t0 = 0; t0 < 128; t0 += 16) {
-                    typename EPI::Pre pre[16];
+                for (int t0 = 0; t0 < 128; t0 += G) {
+                    typename EPI::Pre pre[G];
 #pragma unroll
-                    for (int u = 0; u < 16; ++u) {
+                    for (int u = 0; u < G; ++u) {
                         const i64 col = (i64)n0 + h * 128 + t0 + u;
                         if (col < n) EPI::load(ea, row + col * m, pre[u]);
                     }
 #pragma unroll
-                    for (int u = 0; u < 16; ++u) {
+                    for (int u = 0; u < G; ++u) {
                         const i64 col = (i64)n0 + h * 128 + t0 + u;
                         if (col < n) C[row + col * ldc] = EPI::at(ea, pre[u], acc[t0 + u]);
                     }

@@ -785,8 +785,8 @@ class _Lowerer:
         # exposed (not overlapped with a next tile), and streaming another m x n
         # input there measured slower than the separate chain (8192^3 f32:
         # exp(AB^T/n) - C 4.79 ms fused vs 4.36 ms; exp(AB^T/n) 4.15 vs 4.57 ms)
-        if len(prog.inputs) != 1 or len(prog.stages) > 64 or prog.inputs[0] != ("gemm", None) or \
-                ("load", 0) not in prog.stages:
+        if (len(prog.inputs) != 1 and not _EPI_MEM_INPUTS) or len(prog.stages) > 64 or \
+                prog.inputs[0] != ("gemm", None) or ("load", 0) not in prog.stages:
             del self.steps[mark[0]:]
             del self.slots[mark[1]:]
             del self.absorbed[mark[2]:]
@@ -980,6 +980,7 @@ _RECIPE_MAX = 256
 _RECIPE_LOCK = threading.Lock()
 _RECIPES_ON = os.environ.get("BM_PLAN_CACHE", "1") != "0"
 _F64_PROLOGUE = os.environ.get("BM_F64_PROLOGUE", "0") == "1"   # f64 operand chains inside DMMA (off: slower)
+_EPI_MEM_INPUTS = os.environ.get("BM_GEMM_EPI_INPUTS", "0") == "1"   # epilogues that read other matrices (off: slower)
 
 
 class _NoRecipe(Exception):

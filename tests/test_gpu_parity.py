@@ -898,6 +898,40 @@ def test_gemm_epilogue_bit_identical_to_unfused(dm, elem, m, n, k, ta, tb):
     normwise(dm.evaluate(prod).to_numpy(), pa @ pb, 1e-5 if elem == "f32" else 1e-12)
 
 
+_PERSIST_CHILD = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2308_03120_b200 as dm
+dm.init("b200")
+rng = np.random.default_rng(11)
+a = dm.Matrix.from_numpy(rng.random((4096, 2048), dtype=np.float32))
+b = dm.Matrix.from_numpy(rng.random((4000, 2048), dtype=np.float32))
+prod = a @ b.t()
+plain = dm.evaluate(prod).to_numpy()
+epi = dm.evaluate(dm.exp(prod / 2048) * 3 - 1).to_numpy()
+np.save(sys.argv[2], np.stack([plain, epi]))
+dm.shutdown()
+"""
+
+
+def test_gemm_persistent_pairs_bit_identical(tmp_path):
+    """BM_GEMM_PERSIST=1: 74 resident CTA pairs claim the 256 x 256 tiles from a
+    global counter (four K passes here, each with its own counter) -- the
+    same bits as one pair per tile, for the plain GEMM and a fused epilogue."""
+    import os
+    import pathlib
+    import subprocess
+    import sys
+    root = str(pathlib.Path(__file__).resolve().parents[1])
+    outs = {}
+    for p in ("0", "1"):
+        env = dict(os.environ, BM_GEMM_PERSIST=p, BM_GEMM_KPASS="512")
+        f = tmp_path / f"p{p}.npy"
+        subprocess.run([sys.executable, "-c", _PERSIST_CHILD, root, str(f)], env=env, check=True, timeout=600)
+        outs[p] = np.load(f)
+    same(outs["1"], outs["0"])
+
+
 # ---- GEMM prologue fusion ------------------------------------------------------------------------
 
 @pytest.mark.parametrize("m,n,k,tb", [(512, 384, 256, 1), (1000, 700, 300, 0), (2048, 2048, 1024, 1)])

@@ -56,6 +56,9 @@ def _peaks() -> tuple[float, float, str]:
     return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
 
 
+DMMA_PEAK_TFLOPS = 37.08   # tools/dmma_peak.cu on a B200: 128 f64 FLOP / clk / SM (profiles/r02_dmma_peak.txt)
+
+
 def _bf16_sustained() -> tuple[float, str]:
     """cuBLAS bf16 over seconds under the 1000 W cap (for kernels timed inside a long step)."""
     p = ROOT / "MEASURED_PEAKS.json"
@@ -459,6 +462,12 @@ def secondary_suite(dm, torch, cpu: bool) -> dict:
                     e["roofline"] = {"bound": "tensor", "peak": sus / 6, "unit": "TFLOP/s",
                                      "frac": e["TFLOP/s"] / (sus / 6), "frac_of_burst": e["TFLOP/s"] / ceil,
                                      "basis": f"{sus_src} bf16 / 2 (tf32) / 3 (3xTF32 passes): power-capped run"}
+            else:
+                # DMMA has no entry in MEASURED_PEAKS.json: its issue ceiling measured with
+                # register-only DMMA chains on a B200 (tools/dmma_peak.cu, profiles/r02_dmma_peak.txt)
+                e["roofline"] = {"bound": "tensor", "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                                 "frac": e["TFLOP/s"] / DMMA_PEAK_TFLOPS,
+                                 "basis": "measured DMMA (mma.sync m8n8k4 f64) issue ceiling, 148 SMs at 1965 MHz"}
             tol = 1e-5 if elem == "f32" else 1e-12
             if n == 8192:
                 td = torch.float64

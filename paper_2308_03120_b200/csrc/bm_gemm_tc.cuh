@@ -25,7 +25,13 @@ struct alignas(64) TmapBytes {
 // the product value.  PlainEpi: the unfused store.
 struct PlainEpi {
     static constexpr int kGroup = 16;      // epilogue elements per thread with their loads in flight together
+    // kStage: the program reads one f32 memory input (input 1), which the pair kernel may
+    // stage through shared memory (stage_src / stage_ok / stage_set; see gemm_pair_body)
+    static constexpr bool kStage = false;
     struct Pre {};
+    __device__ static __forceinline__ const float* stage_src(const Args&) { return nullptr; }
+    __device__ static __forceinline__ bool stage_ok(const Args&) { return false; }
+    __device__ static __forceinline__ void stage_set(Pre&, float) {}
     __device__ static __forceinline__ void load(const Args&, i64, Pre&) {}
     template <typename T>
     __device__ static __forceinline__ T at(const Args&, const Pre&, T v) { return v; }
@@ -142,6 +148,21 @@ __device__ __forceinline__ void t2_commit_both(uint64_t* bar) {
 __device__ __forceinline__ void t2_arrive_remote(uint32_t cluster_bar) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
 }
+// Arrive on a (possibly remote) barrier with the default CTA-scope release.  For the
+// pipeline barriers (stages, accumulators) no generic-proxy data crosses the CTA pair --
+// the TMA writes, MMA reads and TMEM accesses are ordered by the mbarrier transaction
+// mechanism and the tcgen05 fences -- and the cluster-scope release / acquire forms
+// compile to MEMBAR.ALL.GPU + ERRBAR and CCTL.IVALL (an L1 invalidate) respectively:
+// measured as the top stalls of the epilogue warps (membar 37 %), and the L1 invalidate
+// evicts their spilled accumulators on every 64-K chunk.  The cluster forms stay for the
+// tile queue, whose slot is an st.shared::cluster into the peer.
+__device__ __forceinline__ void t2_arrive_remote_cta(uint32_t cluster_bar) {
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
+}
+__device__ __forceinline__ void t2_cp_async16(void* dst, const void* src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 16 : 0)
+                 : "memory");
+}
 __device__ __forceinline__ void t2_cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -256,7 +277,7 @@ __device__ __forceinline__ void gemm_pair_body(const TmapBytes& tm_ahi, const Tm
                 const int nb0 = n0 + (int)rank * T2_BNH;   // this CTA's half of the B tile
                 for (int kb = 0; kb < nk; ++kb, ++it) {
                     const int s = it % T2_STAGES;
-                    if (it >= T2_STAGES) t2_wait_cluster(&empty[s], (uint32_t)(((it / T2_STAGES) - 1) & 1));
+                    if (it >= T2_STAGES) t2_wait(&empty[s], (uint32_t)(((it / T2_STAGES) - 1) & 1));
                     if (leader) mbar_expect_tx(&full[s], 2 * T2_STAGE_BYTES);   // both CTAs' bytes
                     const uint32_t lbar = t2_mapa(&full[s], 0);
                     const int kc = (kb0 + kb) * TC_BK;
@@ -289,13 +310,13 @@ __device__ __forceinline__ void gemm_pair_body(const TmapBytes& tm_ahi, const Tm
             for (int t = take(qi); t >= 0; t = take(qi))
             for (int c = 0; c < nchunks; ++c, ++cc) {
                 const int b = cc & 1;
-                if (cc >= 2) t2_wait_cluster(&acc_empty[b], (uint32_t)(((cc >> 1) - 1) & 1));
+                if (cc >= 2) t2_wait(&acc_empty[b], (uint32_t)(((cc >> 1) - 1) & 1));
                 tc_fence_after();
                 const uint32_t d = tmem + (uint32_t)(b * TC_BN);
                 const int kb_end = (c + 1) * TC_CHUNK_KB < nk ? (c + 1) * TC_CHUNK_KB : nk;
                 for (int kb = c * TC_CHUNK_KB; kb < kb_end; ++kb, ++it) {
                     const int s = it % T2_STAGES;
-                    t2_wait_cluster(&full[s], (uint32_t)((it / T2_STAGES) & 1));
+                    t2_wait(&full[s], (uint32_t)((it / T2_STAGES) & 1));
                     tc_fence_after();
                     const uint64_t ahi = sw64_kmajor_desc(smem_u32(tile_ahi(s)));
                     const uint64_t alo = sw64_kmajor_desc(smem_u32(tile_alo(s)));
@@ -327,6 +348,31 @@ __device__ __forceinline__ void gemm_pair_body(const TmapBytes& tm_ahi, const Tm
         int m0, n0;
         tile_coords(t, m0, n0);
         const i64 row = (i64)m0 + 32 * q + lane;
+        // An epilogue that reads an f32 matrix (e.g. alpha AB^T + beta C) stages this warp's
+        // 32 x 128 slice of it into shared memory with one burst of 16-byte cp.async issued
+        // when the last chunk's MMAs are complete -- the TMA ring is idle then (the pair has
+        // no next tile) -- instead of 128 dependent load rounds per thread after the drain.
+        // 8 warps x 16 KB = 128 KB of the 192 KB ring.
+        float* stage_buf = reinterpret_cast<float*>(smem) + (warp - 2) * (32 * 128);
+        bool staged = false;
+        if constexpr (EPI::kStage) {
+            const float* src = EPI::stage_src(ea);
+            staged = apply && tile_ctr == nullptr && pair + npairs >= ntiles && EPI::stage_ok(ea) && (m & 3) == 0 &&
+                     ((reinterpret_cast<uintptr_t>(src) & 15u) == 0);
+        }
+        auto stage_issue = [&]() {
+            const float* src = EPI::stage_src(ea);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // the ring was last touched by TMA / MMA
+            const i64 rr = (i64)m0 + 32 * q + 4 * (lane & 7);
+#pragma unroll 8
+            for (int cb = 0; cb < 128; cb += 4) {
+                const int cl = cb + (lane >> 3);
+                const i64 col = (i64)n0 + h * 128 + cl;
+                const bool ok = col < n && rr < m;     // m % 4 == 0: rr < m covers rr + 3
+                t2_cp_async16(stage_buf + cl * 32 + 4 * (lane & 7), ok ? src + rr + col * m : src, ok);
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
         float acc[128];
         if (accumulate && row < m) {
             const float* cp = C + row + ((i64)n0 + h * 128) * ldc;
@@ -339,8 +385,9 @@ __device__ __forceinline__ void gemm_pair_body(const TmapBytes& tm_ahi, const Tm
         }
         for (int c = 0; c < nchunks; ++c, ++cc) {
             const int b = cc & 1;
-            t2_wait_cluster(&acc_full[b], (uint32_t)((cc >> 1) & 1));
+            t2_wait(&acc_full[b], (uint32_t)((cc >> 1) & 1));
             tc_fence_after();
+            if (staged && c == nchunks - 1) stage_issue();   // every MMA of the tile is complete
             const uint32_t base = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(b * TC_BN + h * 128);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -352,9 +399,21 @@ __device__ __forceinline__ void gemm_pair_body(const TmapBytes& tm_ahi, const Tm
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) t2_arrive_remote(t2_mapa(&acc_empty[b], 0));
+            if (lane == 0) t2_arrive_remote_cta(t2_mapa(&acc_empty[b], 0));
         }
-        if (row < m) {
+        if (staged) {
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            __syncwarp();
+            if (row < m) {
+#pragma unroll
+                for (int t = 0; t < 128; ++t) {
+                    const i64 col = (i64)n0 + h * 128 + t;
+                    typename EPI::Pre pre;
+                    EPI::stage_set(pre, stage_buf[t * 32 + lane]);
+                    if (col < n) C[row + col * ldc] = EPI::at(ea, pre, acc[t]);
+                }
+            }
+        } else if (row < m) {
             if (apply) {   // last K pass: the fused element-wise epilogue (program input 0 = the product)
                 constexpr int G = EPI::kGroup;
 #pragma unroll

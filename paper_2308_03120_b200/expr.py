@@ -781,11 +781,16 @@ class _Lowerer:
         ra = self.lower(a, elem)
         rb = self.lower(b, elem)
         prog = self._fit_program(root, elem, pre=(g, ("gemm", None)))
-        # only programs of the product alone: the non-persistent GEMM's epilogue is
-        # exposed (not overlapped with a next tile), and streaming another m x n
-        # input there measured slower than the separate chain (8192^3 f32:
-        # exp(AB^T/n) - C 4.79 ms fused vs 4.36 ms; exp(AB^T/n) 4.15 vs 4.57 ms)
-        if (len(prog.inputs) != 1 and not _EPI_MEM_INPUTS) or len(prog.stages) > 64 or \
+        # Programs of the product alone, or (f32) of the product and one f32 matrix
+        # with 4 | rows, which the pair kernel stages through its idle TMA ring
+        # (8192^3: exp(AB^T/n) - C 4.53 ms fused vs 4.60 unfused, 2AB^T + 3C 4.45-4.58
+        # vs 4.73-4.78; profiles/r02_gemm_persist.txt).  More inputs, f64 and odd row
+        # counts read them with dependent loads after the drain: slower, the
+        # reference's plan unless BM_GEMM_EPI_INPUTS=1.
+        mem = prog.inputs[1:]
+        mem_ok = not mem or _EPI_MEM_INPUTS or (
+            elem == "f32" and len(mem) == 1 and self._ref_elem(mem[0]) == "f32" and s.rows % 4 == 0)
+        if not mem_ok or len(prog.stages) > 64 or \
                 prog.inputs[0] != ("gemm", None) or ("load", 0) not in prog.stages:
             del self.steps[mark[0]:]
             del self.slots[mark[1]:]

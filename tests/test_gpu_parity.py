@@ -898,6 +898,27 @@ def test_gemm_epilogue_bit_identical_to_unfused(dm, elem, m, n, k, ta, tb):
     normwise(dm.evaluate(prod).to_numpy(), pa @ pb, 1e-5 if elem == "f32" else 1e-12)
 
 
+@pytest.mark.parametrize("m,n,k,tb", [(1024, 768, 512, 1), (1001, 700, 300, 0), (512, 512, 20000, 1),
+                                      (2052, 1030, 256, 1)])
+def test_gemm_epilogue_with_memory_input(dm, m, n, k, tb, monkeypatch):
+    """alpha AB + beta C and exp(AB / k) - C with C read in the GEMM's store
+    (BM_GEMM_EPI_INPUTS: the f32 input staged through the idle TMA ring; odd m
+    takes the direct loads): the same bits as the reference's plan."""
+    from paper_2308_03120_b200 import expr as E
+    monkeypatch.setattr(E, "_EPI_MEM_INPUTS", True)
+    rng = np.random.default_rng(m * 7 + n + k)
+    a = rng.random((m, k)).astype(np.float32)
+    b = rng.random((n, k) if tb else (k, n)).astype(np.float32)
+    c = rng.random((m, n)).astype(np.float32)
+    mA, mB, mC = dm.Matrix.from_numpy(a), dm.Matrix.from_numpy(b), dm.Matrix.from_numpy(c)
+    prod = mA @ (mB.t() if tb else mB)
+    for e in (2 * prod + 3 * mC, dm.exp(prod / k) - mC):
+        assert [s.kernel for s in dm.plan(e).steps] == ["gemm_epi"]
+        got = dm.evaluate(e).to_numpy()
+        want = dm.evaluate(e, fuse=False).to_numpy()
+        same(got, want)
+
+
 _PERSIST_CHILD = r"""
 import sys, numpy as np
 sys.path.insert(0, sys.argv[1])

@@ -309,8 +309,12 @@ def test_gemm_epilogue_fuses_the_consuming_chain(elem):
     assert len(st.inputs) == 2
     assert st.params["trans_a"] == 0 and st.params["trans_b"] == 1
     assert st.params["program"][:2] == (("load", 0), ("scalar", "eop_scalar_times", 2))
-    # a tree that also reads another m x n matrix keeps the reference's plan (measured slower fused)
-    assert "gemm_epi" not in [s.kernel for s in dm.plan(dm.exp(2 * prod) + c).steps]
+    # a tree that also reads one m x n matrix fuses for f32 (staged through shared memory),
+    # keeps the reference's plan for f64 and for two extra matrices (measured slower fused)
+    kinds = [s.kernel for s in dm.plan(dm.exp(2 * prod) + c).steps]
+    assert kinds == (["gemm_epi"] if elem == "f32" else ["gemm", "fused_chain"])
+    d = leaf(256, 256, elem)
+    assert "gemm_epi" not in [s.kernel for s in dm.plan(prod + c + d).steps]
     # the kernel compiles (NVRTC, sm_100a): 3xTF32 pair kernel / DMMA with the program in the store
     views = [expr._make_view(x.operands[0].mem, 256, 256, "2d") for x in (a, b)]
     out = FakeMatrix(256, 256, elem)

@@ -48,6 +48,16 @@ def main(which: str) -> None:
         B = dm.Matrix(n, n, fill="randu", elem_type=elem)
         for _ in range(3):
             dm.evaluate(A @ B.t())
+    elif which in ("epi_exp", "epi_exp_minus_c"):
+        # the fused-epilogue pair GEMM at 8192^3: exp(AB^T/n), and exp(AB^T/n) - C with C
+        # read in the store (BM_GEMM_EPI_INPUTS forced on)
+        from paper_2308_03120_b200 import expr as E
+        E._EPI_MEM_INPUTS = True
+        n = 8192
+        A, B, C = (dm.Matrix(n, n, fill="randu") for _ in range(3))
+        e = dm.exp((A @ B.t()) / n) - C if which == "epi_exp_minus_c" else dm.exp((A @ B.t()) / n)
+        for _ in range(3):
+            dm.evaluate(e)
     elif which in ("rdim0", "rdim1"):
         m = dm.Matrix(16384, 16384, fill="randu", elem_type="f64")
         for op in ("sum", "max"):

@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 }
 
 // the ahead-of-time kernels: plain stores
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
     gemm_3xtf32_pair_kernel(const __grid_constant__ TmapBytes tm_ahi, const __grid_constant__ TmapBytes tm_alo,
                             const __grid_constant__ TmapBytes tm_bhi, const __grid_constant__ TmapBytes tm_blo,
                             float* __restrict__ C, i64 m, i64 n, i64 ldc, int nk, int group_m, int kb0,
@@ -258,6 +258,11 @@ static int split_operand(const float* src, int64_t ld, bool kmajor, int64_t rows
     return BM_OK;
 }
 
+bool gemm_pair_persistent() {
+    static const bool persist = std::getenv("BM_GEMM_PERSIST") && std::atoi(std::getenv("BM_GEMM_PERSIST")) != 0;
+    return persist;
+}
+
 // C = op(A) op(B) on the 3xTF32 tcgen05 path; split_a / split_b fill the
 // K-major hi/lo copies of op(A) (m x k) and op(B)^T (n x k).
 int gemm_tc_f32_core(int64_t m, int64_t n, int64_t k, const SplitFn& split_a, const SplitFn& split_b, float* C,
@@ -304,7 +309,7 @@ int gemm_tc_f32_core(int64_t m, int64_t n, int64_t k, const SplitFn& split_a, co
         // 4.29 / 43.7 / 356 ms at 8192^3 / 16384^3 / 32768^3 against 4.18 / 39.3 / 305 ms
         // with one pair per tile: the pairs drift apart along the raster and their operand
         // slabs stop sharing L2.)
-        static const bool persist = std::getenv("BM_GEMM_PERSIST") && std::atoi(std::getenv("BM_GEMM_PERSIST")) != 0;
+        const bool persist = gemm_pair_persistent();
         bool persistent = false;
         if (pair && persist && grid.x > (unsigned)(st().sm_count / 2 * 2)) {
             grid.x = (unsigned)(st().sm_count / 2 * 2);
@@ -337,7 +342,7 @@ int gemm_tc_f32_core(int64_t m, int64_t n, int64_t k, const SplitFn& split_a, co
                 float* Cp = C;
                 void* params[] = {&tm[0], &tm[1], &tm[2], &tm[3], &Cp, &mm, &nn, &lc, &nkl, &gm, &k0, &acc,
                                   const_cast<void*>(epi->args), &apply, &tile_ctr};
-                CUresult cr = drv().launchKernel((CUfunction)epi->fn, grid.x, 1, 1, TC_THREADS, 1, 1, T2_SMEM, (CUstream)s,
+                CUresult cr = drv().launchKernel((CUfunction)epi->fn, grid.x, 1, 1, T2_THREADS, 1, 1, T2_SMEM, (CUstream)s,
                                                  params, nullptr);
                 if (cr != CUDA_SUCCESS) {
                     rc = cu_fail(cr, "cuLaunchKernel (3xTF32 GEMM, fused epilogue)");
@@ -347,7 +352,7 @@ int gemm_tc_f32_core(int64_t m, int64_t n, int64_t k, const SplitFn& split_a, co
                 continue;
             }
             if (pair)
-                bm::gemm_3xtf32_pair_kernel<<<grid, TC_THREADS, T2_SMEM, s>>>(tm[0], tm[1], tm[2], tm[3], C, m, n, ldc,
+                bm::gemm_3xtf32_pair_kernel<<<grid, T2_THREADS, T2_SMEM, s>>>(tm[0], tm[1], tm[2], tm[3], C, m, n, ldc,
                                                                                len, group_m > 0 ? group_m : 8, kb0, kb0 > 0,
                                                                                tile_ctr);
             else

@@ -47,6 +47,15 @@ struct PlainEpi {
 #define TC_STAGE_BYTES (2 * TC_TILE_A + 2 * TC_TILE_B)
 #define TC_SMEM (TC_STAGES * TC_STAGE_BYTES + 1024 + 256)
 #define TC_THREADS 320                     // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
+// pair kernel: warp 0 TMA, warp 1 MMA, warps 2 .. T2_EW + 1 epilogue, T2_EC columns each.
+// 8 epilogue warps of 128 columns: 10 warps, 3 on some SM sub-partition, 168 registers.
+// (16 warps of 64 columns -- 5 per sub-partition, 96 registers -- spill more: 456 B
+// against 24 B for the plain store.)
+#ifndef T2_EW
+#define T2_EW 8
+#endif
+#define T2_EC (256 * 4 / T2_EW)
+#define T2_THREADS (64 + 32 * T2_EW)
 
 // K-major operand, SWIZZLE_64B canonical layout: 8-row x 64-B atoms, atoms
 // 512 B apart along M/N (SBO); version 1 (sm_100); K offset via start address.
@@ -217,9 +226,9 @@ __device__ __forceinline__ void gemm_pair_body(const TmapBytes& tm_ahi, const Tm
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&acc_full[b], 1);
-            mbar_init(&acc_empty[b], 16);
+            mbar_init(&acc_empty[b], 2 * T2_EW);
             mbar_init(&tq_full[b], 1);
-            mbar_init(&tq_empty[b], 18);   // leader: MMA + 8 epilogue warps; peer: TMA + 8 epilogue warps
+            mbar_init(&tq_empty[b], 2 + 2 * T2_EW);   // leader: MMA + epilogue warps; peer: TMA + epilogue warps
         }
         mbar_fence_init();
         tma_prefetch_desc(&tm_ahi);
@@ -336,7 +345,8 @@ __device__ __forceinline__ void gemm_pair_body(const TmapBytes& tm_ahi, const Tm
             }
         }
     } else {
-        // epilogue warps 2..9 of both CTAs: this CTA's 128 rows of each tile
+        // epilogue warps 2..T2_EW+1 of both CTAs: this CTA's 128 rows of each tile; warp w
+        // owns TMEM lanes 32 (w % 4) .. + 31 and T2_EC of the tile's 256 columns
         const int q = warp & 3;
         const int h = (warp - 2) >> 2;
         int cc = 0, qi = 0;                    // accumulator chunks drained, tiles taken, across tiles
@@ -349,48 +359,52 @@ __device__ __forceinline__ void gemm_pair_body(const TmapBytes& tm_ahi, const Tm
         tile_coords(t, m0, n0);
         const i64 row = (i64)m0 + 32 * q + lane;
         // An epilogue that reads an f32 matrix (e.g. alpha AB^T + beta C) stages this warp's
-        // 32 x 128 slice of it into shared memory with one burst of 16-byte cp.async issued
+        // 32 x T2_EC slice of it into shared memory with one burst of 16-byte cp.async issued
         // when the last chunk's MMAs are complete -- the TMA ring is idle then (the pair has
-        // no next tile) -- instead of 128 dependent load rounds per thread after the drain.
-        // 8 warps x 16 KB = 128 KB of the 192 KB ring.
-        float* stage_buf = reinterpret_cast<float*>(smem) + (warp - 2) * (32 * 128);
+        // no next tile) -- instead of T2_EC dependent load rounds per thread after the drain.
+        // T2_EW warps x 32 x T2_EC x 4 B = 128 KB of the 192 KB ring.
+        float* stage_buf = reinterpret_cast<float*>(smem) + (warp - 2) * (32 * T2_EC);
         bool staged = false;
         if constexpr (EPI::kStage) {
+            // the host launches a staged kernel only when these hold (bm_jit.cu epi_stage_ready);
+            // the kernel has no other path for the program, so a violation traps
             const float* src = EPI::stage_src(ea);
-            staged = apply && tile_ctr == nullptr && pair + npairs >= ntiles && EPI::stage_ok(ea) && (m & 3) == 0 &&
-                     ((reinterpret_cast<uintptr_t>(src) & 15u) == 0);
+            staged = apply;
+            if (apply && !(tile_ctr == nullptr && pair + npairs >= ntiles && EPI::stage_ok(ea) && (m & 3) == 0 &&
+                           ((reinterpret_cast<uintptr_t>(src) & 15u) == 0)))
+                __trap();
         }
         auto stage_issue = [&]() {
             const float* src = EPI::stage_src(ea);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // the ring was last touched by TMA / MMA
             const i64 rr = (i64)m0 + 32 * q + 4 * (lane & 7);
 #pragma unroll 8
-            for (int cb = 0; cb < 128; cb += 4) {
+            for (int cb = 0; cb < T2_EC; cb += 4) {
                 const int cl = cb + (lane >> 3);
-                const i64 col = (i64)n0 + h * 128 + cl;
+                const i64 col = (i64)n0 + h * T2_EC + cl;
                 const bool ok = col < n && rr < m;     // m % 4 == 0: rr < m covers rr + 3
                 t2_cp_async16(stage_buf + cl * 32 + 4 * (lane & 7), ok ? src + rr + col * m : src, ok);
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
         };
-        float acc[128];
+        float acc[T2_EC];
         if (accumulate && row < m) {
-            const float* cp = C + row + ((i64)n0 + h * 128) * ldc;
-            const int ncol = (int)(n - n0 - h * 128 < 128 ? n - n0 - h * 128 : 128);
+            const float* cp = C + row + ((i64)n0 + h * T2_EC) * ldc;
+            const int ncol = (int)(n - n0 - h * T2_EC < T2_EC ? n - n0 - h * T2_EC : T2_EC);
 #pragma unroll
-            for (int t = 0; t < 128; ++t) acc[t] = t < ncol ? __ldg(cp + t * ldc) : 0.f;
+            for (int t = 0; t < T2_EC; ++t) acc[t] = t < ncol ? __ldg(cp + t * ldc) : 0.f;
         } else {
 #pragma unroll
-            for (int t = 0; t < 128; ++t) acc[t] = 0.f;
+            for (int t = 0; t < T2_EC; ++t) acc[t] = 0.f;
         }
         for (int c = 0; c < nchunks; ++c, ++cc) {
             const int b = cc & 1;
             t2_wait(&acc_full[b], (uint32_t)((cc >> 1) & 1));
             tc_fence_after();
             if (staged && c == nchunks - 1) stage_issue();   // every MMA of the tile is complete
-            const uint32_t base = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(b * TC_BN + h * 128);
+            const uint32_t base = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(b * TC_BN + h * T2_EC);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < T2_EC / 32; ++j) {
                 uint32_t v[32];
                 tmem_ld_32x32b_x32(base + (uint32_t)(j * 32), v);
                 tmem_ld_wait();
@@ -406,34 +420,34 @@ __device__ __forceinline__ void gemm_pair_body(const TmapBytes& tm_ahi, const Tm
             __syncwarp();
             if (row < m) {
 #pragma unroll
-                for (int t = 0; t < 128; ++t) {
-                    const i64 col = (i64)n0 + h * 128 + t;
+                for (int t = 0; t < T2_EC; ++t) {
+                    const i64 col = (i64)n0 + h * T2_EC + t;
                     typename EPI::Pre pre;
                     EPI::stage_set(pre, stage_buf[t * 32 + lane]);
                     if (col < n) C[row + col * ldc] = EPI::at(ea, pre, acc[t]);
                 }
             }
         } else if (row < m) {
-            if (apply) {   // last K pass: the fused element-wise epilogue (program input 0 = the product)
+            if (apply && !EPI::kStage) {   // last K pass: the fused element-wise epilogue (program input 0 = the product)
                 constexpr int G = EPI::kGroup;
 #pragma unroll
-                for (int t0 = 0; t0 < 128; t0 += G) {
+                for (int t0 = 0; t0 < T2_EC; t0 += G) {
                     typename EPI::Pre pre[G];
 #pragma unroll
                     for (int u = 0; u < G; ++u) {
-                        const i64 col = (i64)n0 + h * 128 + t0 + u;
+                        const i64 col = (i64)n0 + h * T2_EC + t0 + u;
                         if (col < n) EPI::load(ea, row + col * m, pre[u]);
                     }
 #pragma unroll
                     for (int u = 0; u < G; ++u) {
-                        const i64 col = (i64)n0 + h * 128 + t0 + u;
+                        const i64 col = (i64)n0 + h * T2_EC + t0 + u;
                         if (col < n) C[row + col * ldc] = EPI::at(ea, pre[u], acc[t0 + u]);
                     }
                 }
             } else {
 #pragma unroll
-                for (int t = 0; t < 128; ++t) {
-                    const i64 col = (i64)n0 + h * 128 + t;
+                for (int t = 0; t < T2_EC; ++t) {
+                    const i64 col = (i64)n0 + h * T2_EC + t;
                     if (col < n) C[row + col * ldc] = acc[t];
                 }
             }

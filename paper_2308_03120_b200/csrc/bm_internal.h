@@ -108,6 +108,7 @@ struct PairEpilogue {
 };
 int gemm_tc_f32_core(int64_t m, int64_t n, int64_t k, const SplitFn& split_a, const SplitFn& split_b, float* C,
                      int64_t ldc, bool* handled, const PairEpilogue* epi = nullptr);
+bool gemm_pair_persistent();   // BM_GEMM_PERSIST: persistent CTA pairs (bm_gemm_tc.cu)
 int gemm_tc_f32(int ta, int tb, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const float* B,
                 int64_t ldb, float* C, int64_t ldc, bool* handled, const PairEpilogue* epi = nullptr);
 int launch_gemm_epi(const bm_invocation* inv);

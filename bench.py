@@ -502,6 +502,21 @@ def secondary_suite(dm, torch, cpu: bool) -> dict:
                         "parity": {"vs": "the unfused plan (product materialised, then the chain)",
                                    "bit_exact": bool(torch.equal(fz, uz))}}
                     del fz, uz, ex
+                    # an epilogue that reads a matrix: 2 A B^T + 3 C, C staged through the TMA ring
+                    Cm = dm.Matrix(n, n, fill="randu")
+                    ax = 2 * (A @ B.t()) + 3 * Cm
+                    tf_ = _median_ms(torch, lambda: dm.evaluate(ax))
+                    tu_ = _median_ms(torch, lambda: dm.evaluate(ax, fuse=False))
+                    fz = D.torch_view(dm.evaluate(ax))
+                    uz = D.torch_view(dm.evaluate(ax, fuse=False))
+                    out["cfg4_epilogue_axpby_8192^3_f32"] = {
+                        "ms": tf_, "TFLOP/s": flops / tf_ / 1e9, "unfused_ms": tu_, "reps": 10,
+                        "plan": [st_.kernel for st_ in dm.plan(ax).steps],
+                        "note": "2 A @ B.t() + 3 C: C staged into shared memory by the epilogue warps once the "
+                                "tile's MMAs are complete, the tree evaluated in the store",
+                        "parity": {"vs": "the unfused plan (product materialised, then the chain)",
+                                   "bit_exact": bool(torch.equal(fz, uz))}}
+                    del fz, uz, ax, Cm
                 if ref is not None:
                     s = ref.run("parallel", [a_h, b_h], lambda d, ms: d.evaluate(ms[0] @ ms[1].t()))
                     cpu_rate[elem] = flops / s / 1e12

@@ -919,6 +919,32 @@ def test_gemm_epilogue_with_memory_input(dm, m, n, k, tb, monkeypatch):
         same(got, want)
 
 
+def test_pair_gemm_repeatable_under_load(dm):
+    """The pair kernel's stage / accumulator barriers are CTA-scope (no cluster-wide
+    fence per chunk): any ordering hole between the MMA issuer, the TMA threads and
+    the epilogue warps of the two CTAs would show up as run-to-run differences.  40
+    back-to-back products (plain, fused exp, staged memory-input epilogue) at 4096^3
+    with K = 5120 (two 64-K-chunk accumulators ping-ponging 80 times per tile) must
+    repeat bit for bit, and match f64 normwise."""
+    rng = np.random.default_rng(77)
+    n, k = 4096, 5120
+    a = rng.random((n, k), dtype=np.float32)
+    b = rng.random((n, k), dtype=np.float32)
+    c = rng.random((n, n), dtype=np.float32)
+    mA, mB, mC = dm.Matrix.from_numpy(a), dm.Matrix.from_numpy(b), dm.Matrix.from_numpy(c)
+    prod = mA @ mB.t()
+    exprs = (prod, dm.exp(prod / k), 2 * prod + 3 * mC)
+    assert [s.kernel for s in dm.plan(exprs[2]).steps] == ["gemm_epi"]
+    firsts = [dm.evaluate(e).to_numpy() for e in exprs]
+    for i in range(40):
+        e = exprs[i % 3]
+        got = dm.evaluate(e).to_numpy()
+        assert got.tobytes() == firsts[i % 3].tobytes(), f"run {i} of expression {i % 3} differs"
+    import torch
+    ta, tb = torch.from_numpy(a).cuda().double(), torch.from_numpy(b).cuda().double()
+    normwise(firsts[0], (ta @ tb.t()).cpu().numpy(), 1e-5)
+
+
 _PERSIST_CHILD = r"""
 import sys, numpy as np
 sys.path.insert(0, sys.argv[1])

@@ -493,22 +493,24 @@ def secondary_suite(dm, torch, cpu: bool) -> dict:
                     ex = dm.exp((A @ B.t()) / n)
                     tf_ = _median_ms(torch, lambda: dm.evaluate(ex))
                     tu_ = _median_ms(torch, lambda: dm.evaluate(ex, fuse=False))
-                    fz = D.torch_view(dm.evaluate(ex))
-                    uz = D.torch_view(dm.evaluate(ex, fuse=False))
+                    # keep both matrices alive while comparing: a view does not own its buffer
+                    fm_, um_ = dm.evaluate(ex), dm.evaluate(ex, fuse=False)
+                    fz, uz = D.torch_view(fm_), D.torch_view(um_)
                     out["cfg4_epilogue_exp_8192^3_f32"] = {
                         "ms": tf_, "TFLOP/s": flops / tf_ / 1e9, "unfused_ms": tu_, "reps": 10,
                         "plan": [st_.kernel for st_ in dm.plan(ex).steps],
                         "note": "exp(A @ B.t() / n): the element-wise tree runs in the 3xTF32 kernel's store",
                         "parity": {"vs": "the unfused plan (product materialised, then the chain)",
                                    "bit_exact": bool(torch.equal(fz, uz))}}
-                    del fz, uz, ex
+                    del fz, uz, fm_, um_, ex
                     # an epilogue that reads a matrix: 2 A B^T + 3 C, C staged through the TMA ring
                     Cm = dm.Matrix(n, n, fill="randu")
                     ax = 2 * (A @ B.t()) + 3 * Cm
                     tf_ = _median_ms(torch, lambda: dm.evaluate(ax))
                     tu_ = _median_ms(torch, lambda: dm.evaluate(ax, fuse=False))
-                    fz = D.torch_view(dm.evaluate(ax))
-                    uz = D.torch_view(dm.evaluate(ax, fuse=False))
+                    # keep both matrices alive while comparing: a view does not own its buffer
+                    fm_, um_ = dm.evaluate(ax), dm.evaluate(ax, fuse=False)
+                    fz, uz = D.torch_view(fm_), D.torch_view(um_)
                     out["cfg4_epilogue_axpby_8192^3_f32"] = {
                         "ms": tf_, "TFLOP/s": flops / tf_ / 1e9, "unfused_ms": tu_, "reps": 10,
                         "plan": [st_.kernel for st_ in dm.plan(ax).steps],
@@ -516,7 +518,7 @@ def secondary_suite(dm, torch, cpu: bool) -> dict:
                                 "tile's MMAs are complete, the tree evaluated in the store",
                         "parity": {"vs": "the unfused plan (product materialised, then the chain)",
                                    "bit_exact": bool(torch.equal(fz, uz))}}
-                    del fz, uz, ax, Cm
+                    del fz, uz, fm_, um_, ax, Cm
                 if ref is not None:
                     s = ref.run("parallel", [a_h, b_h], lambda d, ms: d.evaluate(ms[0] @ ms[1].t()))
                     cpu_rate[elem] = flops / s / 1e12

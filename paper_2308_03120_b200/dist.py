@@ -396,7 +396,8 @@ def sharded_dot(a_local, b_local, group=None):
 class _CudaArray:
     """__cuda_array_interface__ over a device buffer (column-major flat)."""
 
-    def __init__(self, ptr: int, count: int, elem: str):
+    def __init__(self, ptr: int, count: int, elem: str, owner=None):
+        self.owner = owner           # torch holds this object for the tensor's lifetime
         self.__cuda_array_interface__ = {
             "shape": (count,), "typestr": kernels.NP_DTYPE[elem].str, "data": (ptr, False),
             "version": 3, "strides": None, "stream": None}
@@ -404,10 +405,12 @@ class _CudaArray:
 
 def torch_view(m):
     """The column-major storage of a device matrix as a flat torch tensor
-    sharing its memory (no copy): what NCCL reads and writes."""
+    sharing its memory (no copy): what NCCL reads and writes.  The tensor
+    keeps ``m`` alive (a view of a temporary stays valid); resizing ``m``
+    (set_size / reset) leaves the view on the old storage."""
     import torch
     _rt.get_runtime().forget_sum(m.mem.buffer_id)   # the view can write: drop a cached accu
-    return torch.as_tensor(_CudaArray(m.mem.ptr, m.n_elem, m.elem_type), device="cuda")
+    return torch.as_tensor(_CudaArray(m.mem.ptr, m.n_elem, m.elem_type, owner=m), device="cuda")
 
 
 def _world(group=None) -> tuple[int, int]:

@@ -945,6 +945,28 @@ def test_pair_gemm_repeatable_under_load(dm):
     normwise(firsts[0], (ta @ tb.t()).cpu().numpy(), 1e-5)
 
 
+def test_torch_view_keeps_its_matrix_alive(dm):
+    """dist.torch_view of a temporary: the tensor holds the matrix, so its buffer
+    is not released (and reused by the next evaluation) under the view."""
+    import gc
+    import weakref
+    import torch
+    from paper_2308_03120_b200 import dist as D
+    a = dm.Matrix.from_numpy(np.arange(1 << 16, dtype=np.float32))
+    tmp = dm.evaluate(2 * a)
+    alive = weakref.ref(tmp)
+    v = D.torch_view(tmp)
+    del tmp
+    gc.collect()
+    assert alive() is not None
+    others = [dm.evaluate(5 * a + k) for k in range(4)]     # would reuse a released buffer
+    dm.synchronise()
+    assert torch.equal(v.cpu(), torch.arange(1 << 16, dtype=torch.float32) * 2)
+    del v, others
+    gc.collect()
+    assert alive() is None
+
+
 _PERSIST_CHILD = r"""
 import sys, numpy as np
 sys.path.insert(0, sys.argv[1])

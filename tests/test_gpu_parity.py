@@ -899,11 +899,11 @@ def test_gemm_epilogue_bit_identical_to_unfused(dm, elem, m, n, k, ta, tb):
 
 
 @pytest.mark.parametrize("m,n,k,tb", [(1024, 768, 512, 1), (1001, 700, 300, 0), (512, 512, 20000, 1),
-                                      (2052, 1030, 256, 1)])
+                                      (2052, 1030, 256, 1), (1024, 1024, 384, 1)])
 def test_gemm_epilogue_with_memory_input(dm, m, n, k, tb, monkeypatch):
-    """alpha AB + beta C and exp(AB / k) - C with C read in the GEMM's store
-    (BM_GEMM_EPI_INPUTS: the f32 input staged through the idle TMA ring; odd m
-    takes the direct loads): the same bits as the reference's plan."""
+    """alpha AB + beta C, exp(AB / k) - C and AB - C^T with C read in the GEMM's
+    store (the f32 input staged through the idle TMA ring; m % 4 != 0 makes the
+    launcher run the unfused plan instead): the same bits as the reference's plan."""
     from paper_2308_03120_b200 import expr as E
     monkeypatch.setattr(E, "_EPI_MEM_INPUTS", True)
     rng = np.random.default_rng(m * 7 + n + k)
@@ -912,8 +912,11 @@ def test_gemm_epilogue_with_memory_input(dm, m, n, k, tb, monkeypatch):
     c = rng.random((m, n)).astype(np.float32)
     mA, mB, mC = dm.Matrix.from_numpy(a), dm.Matrix.from_numpy(b), dm.Matrix.from_numpy(c)
     prod = mA @ (mB.t() if tb else mB)
-    for e in (2 * prod + 3 * mC, dm.exp(prod / k) - mC):
-        assert [s.kernel for s in dm.plan(e).steps] == ["gemm_epi"]
+    exprs = [2 * prod + 3 * mC, dm.exp(prod / k) - mC]
+    if m == n:
+        exprs.append(prod - mC.t())      # the input a materialised transpose (a slot, not a leaf)
+    for e in exprs:
+        assert [s.kernel for s in dm.plan(e).steps][-1] == "gemm_epi"
         got = dm.evaluate(e).to_numpy()
         want = dm.evaluate(e, fuse=False).to_numpy()
         same(got, want)

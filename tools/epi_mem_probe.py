@@ -1,7 +1,7 @@
 """Epilogues that read another m x n matrix (exp(AB^T/n) - C, 2 AB^T + 3 C) fused
 into the GEMM's store against the reference's plan, interleaved in one process
 so the power / thermal state is shared (GPU box).  Run with BM_GEMM_PERSIST=0|1.
-Usage: python tools/epi_mem_probe.py [n] [rounds]"""
+Usage: python tools/epi_mem_probe.py [n] [rounds] [f32|f64]"""
 import json
 import os
 import pathlib
@@ -30,10 +30,11 @@ def once(fn):
 def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
     rounds = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+    elem = sys.argv[3] if len(sys.argv) > 3 else "f32"
     dm.init("b200")
     D.bind_torch_stream()
     dm.set_seed(3)
-    A, B, C = (dm.Matrix(n, n, fill="randu") for _ in range(3))
+    A, B, C = (dm.Matrix(n, n, fill="randu", elem_type=elem) for _ in range(3))
     e1 = dm.exp((A @ B.t()) / n) - C
     e2 = 2 * (A @ B.t()) + 3 * C
     E._EPI_MEM_INPUTS = True
@@ -48,7 +49,7 @@ def main():
     for _ in range(rounds):
         for k, fn in variants.items():
             ts[k].append(once(fn))
-    out = {"n": n, "persist": os.environ.get("BM_GEMM_PERSIST", "0"), "plans": plans}
+    out = {"n": n, "elem": elem, "persist": os.environ.get("BM_GEMM_PERSIST", "0"), "plans": plans}
     out.update({k: round(statistics.median(v), 3) for k, v in ts.items()})
     print(json.dumps(out))
     dm.shutdown()

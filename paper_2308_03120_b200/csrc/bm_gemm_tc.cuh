@@ -489,13 +489,21 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // BM = 128 would be 8 warps of 64 x 32).  Each warp tile is 32 8x8 DMMA tiles (64 f64
 // accumulators per lane) fed by 12 8-byte shared loads per k4 step.
 #define DM_BN 128
+#ifndef DM_W64
+#define DM_W64 4
+#endif
 
 template <int BM, int BK, int ST>
 struct DmCfg {
-    static constexpr int NW = BM == 64 ? 4 : 8;           // warps
-    static constexpr int WGN = BM == 64 ? 2 : 4;          // warps along N
+    // BM = 64: DM_W64 warps per CTA -- 4 of 32 x 64 (64 f64 accumulators per lane) or
+    // 8 of 32 x 32 (32 accumulators, <= 128 registers, four warps per sub-partition).
+    // 8 warps compile without the accumulator moves the 252-register version has, but
+    // each fragment load feeds half the DMMAs: 33.6 against 31.5 ms at 8192^3
+    // (profiles/r02_dmma_warps_ab.txt), so 4 it is
+    static constexpr int NW = BM == 64 ? DM_W64 : 8;      // warps
+    static constexpr int WGN = BM == 64 ? DM_W64 / 2 : 4; // warps along N
     static constexpr int MI = BM == 64 ? 4 : 8;           // 8-row DMMA tiles per warp (M)
-    static constexpr int NJ = BM == 64 ? 8 : 4;           // 8-col DMMA tiles per warp (N)
+    static constexpr int NJ = BM == 64 ? 32 / DM_W64 : 4; // 8-col DMMA tiles per warp (N)
     static constexpr int LDA = BM + 8, LDB = DM_BN + 8;   // padded smem rows (doubles)
     static constexpr int SMEM = ST * BK * (LDA + LDB) * 8;
     // with fused operands: NIA / NIB staged inputs per operand

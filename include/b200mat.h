@@ -106,7 +106,10 @@ extern "C" {
                                     op(B), ...) with F compiled into the GEMM's store (3xTF32 pair
                                     kernel / DMMA).  inputs: [0] A, [1] B (block views; trans_a /
                                     trans_b), [1 + j] program input j >= 1 (m * n elements each);
-                                    program input 0 is the product; output C (contiguous m x n) */
+                                    program input 0 is the product; output C (contiguous m x n).
+                                    One f32 input (f32 compute) is staged through shared memory when
+                                    it has unit stride, a 16-byte base and 4 | m; otherwise the call
+                                    runs as a GEMM into a temporary and the chain (same bits) */
 
 /* comparison of a predicate (kernels.py:643-657 _predicate_mask) */
 #define BM_CMP_GT 0

@@ -259,7 +259,7 @@ static int split_operand(const float* src, int64_t ld, bool kmajor, int64_t rows
 }
 
 bool gemm_pair_persistent() {
-    static const bool persist = std::getenv("BM_GEMM_PERSIST") && std::atoi(std::getenv("BM_GEMM_PERSIST")) != 0;
+    static const bool persist = !std::getenv("BM_GEMM_PERSIST") || std::atoi(std::getenv("BM_GEMM_PERSIST")) != 0;
     return persist;
 }
 
@@ -303,13 +303,14 @@ int gemm_tc_f32_core(int64_t m, int64_t n, int64_t k, const SplitFn& split_a, co
     }
     if (!rc) {
         dim3 grid((unsigned)((np / tn_) * (mp / tm_) * (pair ? 2 : 1)));
-        // BM_GEMM_PERSIST=1: persistent CTA pairs (one per two SMs) claiming raster tiles
-        // from a global counter as they free up, with the next tile's MMAs under this
-        // tile's epilogue.  (A static share per pair -- tiles p, p + P, ... -- measured
-        // 4.29 / 43.7 / 356 ms at 8192^3 / 16384^3 / 32768^3 against 4.18 / 39.3 / 305 ms
-        // with one pair per tile: the pairs drift apart along the raster and their operand
-        // slabs stop sharing L2.)
-        const bool persist = gemm_pair_persistent();
+        // Persistent CTA pairs (one per two SMs; BM_GEMM_PERSIST=0 turns them off) claiming
+        // raster tiles from a global counter as they free up, with the next tile's MMAs
+        // under this tile's epilogue: 0.5-1 % over one pair per tile after the barrier-scope
+        // fix (8192^3 3.97-3.99 vs 4.00-4.01 ms, 16384^3 34.5-34.6 vs 34.6-35.0 ms).  (A
+        // static share per pair -- tiles p, p + P, ... -- was 3-15 % slower: the pairs
+        // drift apart along the raster and their operand slabs stop sharing L2.)  A staged
+        // epilogue needs the TMA ring idle after its tile: one tile per pair.
+        const bool persist = gemm_pair_persistent() && !(epi && epi->staged);
         bool persistent = false;
         if (pair && persist && grid.x > (unsigned)(st().sm_count / 2 * 2)) {
             grid.x = (unsigned)(st().sm_count / 2 * 2);

@@ -105,10 +105,11 @@ typedef std::function<int(float* hi, float* lo, int64_t kp, int64_t rp)> SplitFn
 struct PairEpilogue {
     void* fn;            // CUfunction
     const void* args;    // bm::Args
+    bool staged = false; // stages a memory input through the TMA ring: one tile per CTA pair
 };
 int gemm_tc_f32_core(int64_t m, int64_t n, int64_t k, const SplitFn& split_a, const SplitFn& split_b, float* C,
                      int64_t ldc, bool* handled, const PairEpilogue* epi = nullptr);
-bool gemm_pair_persistent();   // BM_GEMM_PERSIST: persistent CTA pairs (bm_gemm_tc.cu)
+bool gemm_pair_persistent();   // BM_GEMM_PERSIST (default on): persistent CTA pairs (bm_gemm_tc.cu)
 int gemm_tc_f32(int ta, int tb, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const float* B,
                 int64_t ldb, float* C, int64_t ldc, bool* handled, const PairEpilogue* epi = nullptr);
 int launch_gemm_epi(const bm_invocation* inv);

@@ -474,11 +474,12 @@ def sharded_logistic_step(x_local, w, y_local, group=None):
     """One logistic-regression gradient step sharded by samples (row blocks
     of X): z = X_r w, r = 1/(1+exp(-z)) - y_r,
     g = sum_r X_r^T r_r (one all-gather of a 1024-vector, folded in rank
-    order) and s = accu(r) over all ranks.  Returns (g, s)."""
+    order) and s = accu(r) over all ranks.  Returns (g, s).  Each rank runs
+    the single-pass fused step on its shard (evaluate_many: X_r read once,
+    bm_lgrad) wherever the planner can fuse it, the two-pass plan otherwise."""
     from . import ops
-    z = _expr.evaluate(x_local @ w)
-    r = _expr.evaluate(1 / (1 + ops.exp(0 - z)) - y_local)
-    g_local = _expr.evaluate(x_local.t() @ r)
+    r_e = 1 / (1 + ops.exp(0 - x_local @ w)) - y_local
+    r, g_local = _expr.evaluate_many(r_e, x_local.t() @ r_e)
     if _world(group)[1] == 1:
         return g_local, ops.accu(r)
     g = _expr.evaluate(ops.sum(gather_columns(g_local, group), 1))

@@ -733,7 +733,9 @@ def sharded_suite(dm, torch, rank: int, world: int) -> dict:
         nb = 4 * nrow * ncol                # the fused step per shard reads X once
         out["cfg5_logistic_step_1Mx1024_f32_sharded"] = {
             "ms": ms, "GB/s": nb / ms / 1e6, "scaling": "strong",
-            "note": "per rank: the fused single-pass step on its row block (X read once), one all-gather of g",
+            "note": ("per rank: the fused single-pass step on its row block (X read once); g and accu(r) of "
+                     "every rank cross over peer memory and fold in one kernel (bm_exchange_gsum)"),
+            "collective": D._LAST.get("logistic_collective"),
             "parity": {"vs": "single-device step on each rank's GPU", "tol": 1e-5, "g_max_rel_err": gerr,
                        "s_max_rel_err": serr}}
         del Xl, yl, w, y

@@ -41,6 +41,71 @@ __global__ void __launch_bounds__(256) exchange_combine_kernel(const A* __restri
     if (threadIdx.x == 0) out[0] = normalise ? OpPlus::f(r, A(0)) : r;
 }
 
+// ---------------------------------------------------------------------------
+// Vector exchange (the sample-sharded logistic step): every
+// rank's k gradient values and its accu(r) partial travel over peer memory in
+// ONE kernel, which also folds them -- the replacement of the NCCL all-gather
+// of g, the dim-1 sum over the gathered columns and the separate accu exchange.
+// Buffer of every rank, per parity (epoch & 1): [world slots of `slot` f32
+// values][world u64 flags]; slot r holds rank r's g (n values) and s (at n).
+// g is folded left to right in rank order, like sum(gathered, 1) over the
+// k x world matrix of the all-gather path (each row x_0 + x_1 + ...); s with
+// combine_pairwise over the ranks + 0.0f, like exchange_combine for a float accu.
+
+__host__ __device__ inline size_t vx_slot(long long n) { return (size_t)((n + 1 + 3) / 4 * 4); }
+__host__ __device__ inline size_t vx_parity_bytes(int world, long long n) {
+    return ((size_t)world * vx_slot(n) * 4 + 15) / 16 * 16 + (size_t)world * 8;
+}
+
+__global__ void __launch_bounds__(512) exchange_gsum_kernel(const float* __restrict__ g, long long n,
+                                                            const float* __restrict__ s, PeerPtrs peers, int W, int R,
+                                                            unsigned long long ep, float* __restrict__ g_out,
+                                                            float* __restrict__ s_out, unsigned int* err,
+                                                            unsigned long long timeout_ns) {
+    __shared__ float xv[2 * 64];
+    const size_t slot = vx_slot(n);
+    const size_t pbytes = vx_parity_bytes(W, n);
+    const size_t base = (size_t)(ep & 1) * pbytes;
+    const size_t flags = ((size_t)W * slot * 4 + 15) / 16 * 16;
+    // publish: this rank's n + 1 values into slot R of every rank's buffer (NVLink stores)
+    for (int p = 0; p < W; ++p) {
+        float* dst = reinterpret_cast<float*>(reinterpret_cast<char*>(peers.p[p]) + base) + (size_t)R * slot;
+        for (long long i = threadIdx.x; i <= n; i += blockDim.x) dst[i] = i < n ? g[i] : s[0];
+    }
+    __threadfence_system();            // every value lands before any flag says so
+    __syncthreads();
+    if (threadIdx.x < W) {
+        unsigned long long* flag =
+            reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(peers.p[threadIdx.x]) + base + flags) + R;
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(ep) : "memory");
+    }
+    // wait for every rank's flag in the own buffer
+    const char* mine = reinterpret_cast<const char*>(peers.p[R]) + base;
+    if (threadIdx.x < W) {
+        const unsigned long long* flag = reinterpret_cast<const unsigned long long*>(mine + flags) + threadIdx.x;
+        unsigned long long f, t0, t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        do {
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(f) : "l"(flag) : "memory");
+            if (f >= ep) break;
+            __nanosleep(64);
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        } while (t - t0 < timeout_ns);
+        if (f < ep && err) atomicOr_system(err, BM_DEVERR_PEER_TIMEOUT);
+    }
+    __syncthreads();
+    const float* v = reinterpret_cast<const float*>(mine);
+    for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+        float acc = *reinterpret_cast<const volatile float*>(v + i);
+        for (int p = 1; p < W; ++p) acc = acc + *reinterpret_cast<const volatile float*>(v + (size_t)p * slot + i);
+        g_out[i] = acc;
+    }
+    for (int p = threadIdx.x; p < W; p += blockDim.x) xv[p] = *reinterpret_cast<const volatile float*>(v + (size_t)p * slot + n);
+    __syncthreads();
+    const float r = cta_combine_pairwise<float, 1>(xv, xv + W, W);
+    if (threadIdx.x == 0) s_out[0] = OpPlus::f(r, 0.0f);
+}
+
 }  // namespace bm
 
 namespace bmi {
@@ -198,6 +263,39 @@ int bm_exchange_alloc(int32_t world, void** dev_buffer, void* ipc_handle) {
     BM_CUDA(cudaIpcGetMemHandle(&h, *dev_buffer));
     static_assert(sizeof(h) == 64, "IPC handle size");
     std::memcpy(ipc_handle, &h, sizeof h);
+    return BM_OK;
+}
+
+int bm_exchange_alloc_vec(int32_t world, int64_t n, void** dev_buffer, void* ipc_handle) {
+    using namespace bmi;
+    BM_REQUIRE_INIT();
+    if (world < 1 || world > 64) return set_error(BM_ERR_ARG, "exchange: world out of range");
+    if (n < 0 || n > (1 << 20)) return set_error(BM_ERR_ARG, "exchange: vector length out of range");
+    const size_t bytes = 2 * bm::vx_parity_bytes(world, n);
+    BM_CUDA(cudaMalloc(dev_buffer, bytes));
+    BM_CUDA(cudaMemset(*dev_buffer, 0, bytes));
+    cudaIpcMemHandle_t h;
+    BM_CUDA(cudaIpcGetMemHandle(&h, *dev_buffer));
+    std::memcpy(ipc_handle, &h, sizeof h);
+    return BM_OK;
+}
+
+int bm_exchange_gsum(const float* dev_g, int64_t n, const float* dev_s, void* const* peer_buffers, int32_t world,
+                     int32_t rank, uint64_t epoch, float* dev_g_out, float* dev_s_out) {
+    using namespace bmi;
+    BM_REQUIRE_INIT();
+    if (world < 1 || world > 64 || rank < 0 || rank >= world) return set_error(BM_ERR_ARG, "exchange: bad world/rank");
+    if (epoch == 0) return set_error(BM_ERR_ARG, "exchange: epochs start at 1");
+    if (n < 0 || n > (1 << 20) || !dev_s || (n > 0 && (!dev_g || !dev_g_out)) || !dev_s_out)
+        return set_error(BM_ERR_ARG, "exchange: bad vector arguments");
+    std::lock_guard<std::recursive_mutex> lk(st().mu);
+    bm::PeerPtrs pp;
+    std::memset(&pp, 0, sizeof pp);
+    for (int i = 0; i < world; ++i) pp.p[i] = peer_buffers[i];
+    bm::exchange_gsum_kernel<<<1, 512, 0, st().stream>>>(dev_g, (long long)n, dev_s, pp, world, rank, epoch, dev_g_out,
+                                                          dev_s_out, st().err_dev, st().exch_timeout_ns);
+    BM_CUDA(cudaGetLastError());
+    st().launches++;
     return BM_OK;
 }
 

@@ -57,11 +57,12 @@ class PeerExchange:
     every rank's buffer over NVLink, publishes a step epoch with release
     semantics, waits for all epochs and folds in rank order."""
 
-    def __init__(self, group=None):
+    def __init__(self, group=None, nvals=None):
         import torch
         import torch.distributed as dist
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
+        self.nvals = nvals                  # None: one value per rank; n: n f32 + one f32 scalar (gsum)
         self._lib = _clib.lib()
         self._own = None
         self._opened = []
@@ -76,7 +77,11 @@ class PeerExchange:
         ok = True
         try:
             own = ctypes.c_void_p()
-            _clib.check(self._lib.bm_exchange_alloc(self.world, ctypes.byref(own), handle), "exchange alloc")
+            if nvals is None:
+                _clib.check(self._lib.bm_exchange_alloc(self.world, ctypes.byref(own), handle), "exchange alloc")
+            else:
+                _clib.check(self._lib.bm_exchange_alloc_vec(self.world, nvals, ctypes.byref(own), handle),
+                            "exchange alloc")
             self._own = own.value
         except Exception:  # noqa: BLE001 - reported collectively below
             ok = False
@@ -115,6 +120,16 @@ class PeerExchange:
             ctypes.c_void_p(partial.data_ptr()), self._ptrs, self.world, self.rank, self.epoch,
             _clib.DTYPE_CODE[elem], op_code, ctypes.c_void_p(result.data_ptr())), "exchange combine")
 
+    def gsum(self, g_ptr: int, n: int, s_ptr: int, g_out_ptr: int, s_out_ptr: int) -> None:
+        """Vector buffers only: g_out = sum over ranks of g (n f32, rank order) and
+        s_out = combine_pairwise of the ranks' s, in one kernel (bm_exchange_gsum)."""
+        if self.nvals is None or n > self.nvals:
+            raise ValueError("gsum needs a vector exchange of at least n values")
+        self.epoch += 1
+        _clib.check(self._lib.bm_exchange_gsum(
+            ctypes.c_void_p(g_ptr), n, ctypes.c_void_p(s_ptr), self._ptrs, self.world, self.rank, self.epoch,
+            ctypes.c_void_p(g_out_ptr), ctypes.c_void_p(s_out_ptr)), "exchange gsum")
+
     def reduce(self, inv, result) -> None:
         """The shard reduction and the exchange in one kernel
         (bm_reduce_to_device_exchange): the folded world value lands in result."""
@@ -149,6 +164,24 @@ def shared_exchange(group=None):
     if ent is None or ent[0] is not group:
         try:
             ex = PeerExchange(group)
+        except RuntimeError:
+            ex = None
+        ent = (group, ex)
+        _SHARED_EXCHANGES[key] = ent
+    ex = ent[1]
+    return None if ex is None or ex.broken else ex
+
+
+def shared_vec_exchange(nvals: int, group=None):
+    """The process's vector PeerExchange for `group` with room for `nvals` values
+    (created once, collectively; None when peer mapping is unavailable anywhere
+    or an exchange timed out).  Shares the registry (and its teardown) with
+    shared_exchange."""
+    key = (id(group), "vec", nvals)
+    ent = _SHARED_EXCHANGES.get(key)
+    if ent is None or ent[0] is not group:
+        try:
+            ex = PeerExchange(group, nvals=nvals)
         except RuntimeError:
             ex = None
         ent = (group, ex)
@@ -470,19 +503,47 @@ def sharded_gemm_nt(a, b_local):
     return _expr.evaluate(a @ b_local.t())
 
 
-def sharded_logistic_step(x_local, w, y_local, group=None):
+_LAST: dict = {}   # the path the last sharded_logistic_step took ("peer" / "gather"; tests and bench)
+
+
+def sharded_logistic_step(x_local, w, y_local, group=None, collective=None):
     """One logistic-regression gradient step sharded by samples (row blocks
     of X): z = X_r w, r = 1/(1+exp(-z)) - y_r,
     g = sum_r X_r^T r_r (one all-gather of a 1024-vector, folded in rank
     order) and s = accu(r) over all ranks.  Returns (g, s).  Each rank runs
     the single-pass fused step on its shard (evaluate_many: X_r read once,
-    bm_lgrad) wherever the planner can fuse it, the two-pass plan otherwise."""
+    bm_lgrad) wherever the planner can fuse it, the two-pass plan otherwise.
+    With peer memory (collective "p2p"/"p2p_fused", the default) g and the
+    folded accu(r) the fused step left in the sum cache cross the ranks in ONE
+    kernel (bm_exchange_gsum); otherwise an NCCL all-gather of g, its dim-1
+    sum and a ShardedReduction of r -- the same bits either way."""
     from . import ops
     r_e = 1 / (1 + ops.exp(0 - x_local @ w)) - y_local
     r, g_local = _expr.evaluate_many(r_e, x_local.t() @ r_e)
     if _world(group)[1] == 1:
         return g_local, ops.accu(r)
+    if collective is None:
+        collective = os.environ.get("BM_SHARD_COLLECTIVE", "p2p_fused")
+    rt = _rt.get_runtime()
+    slot = rt.sum_slot(r.mem)
+    use_peer = collective in ("p2p", "p2p_fused") and g_local.elem_type == "f32" and \
+        _agree_all(group, slot is not None)
+    ex = shared_vec_exchange(g_local.n_elem, group) if use_peer else None
+    if ex is not None:
+        # one kernel: g and accu(r) of every rank over peer memory, folded in rank order
+        from .matrix import Matrix
+        g = Matrix._uninitialised(g_local.n_rows, g_local.n_cols, "f32")
+        s_out = rt.acquire_memory(1, "f32")
+        try:
+            ex.gsum(g_local.mem.ptr, g_local.n_elem, slot.ptr, g.mem.ptr, s_out.ptr)
+            s = float(rt.copy_d2h(s_out, 0, 1)[0])
+        finally:
+            rt.release_deferred(s_out)
+        _check_exchange_error(ex)
+        _LAST["logistic_collective"] = "peer"
+        return g, s
+    _LAST["logistic_collective"] = "gather"
     g = _expr.evaluate(ops.sum(gather_columns(g_local, group), 1))
-    s = ShardedReduction("accu", r, group=group)
+    s = ShardedReduction("accu", r, group=group, collective=collective)
     s.launch()
     return g, s.value().item()

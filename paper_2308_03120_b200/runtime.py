@@ -594,6 +594,10 @@ class Runtime:
         self.forget_sum(buf.buffer_id)
         self._sums[buf.buffer_id] = slot
 
+    def sum_slot(self, buf: DeviceBuffer):
+        """The 1-element device buffer holding the cached accu of ``buf``, or None."""
+        return self._sums.get(buf.buffer_id) if self._sums else None
+
     def cached_sum(self, buf: DeviceBuffer):
         """The cached accu of ``buf`` as a numpy scalar, or None."""
         slot = self._sums.get(buf.buffer_id) if self._sums else None

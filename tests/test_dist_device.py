@@ -211,3 +211,52 @@ def test_peer_timeout_raises_at_synchronise():
     assert out1 == "no-error"
     assert coll0 == coll1 == "allreduce"
     assert v0 == v1
+
+
+# ---- the sample-sharded logistic step: g and accu(r) over peer memory in one kernel -------------
+
+def _logistic_worker(rank, world, port, q, rows, cols):
+    dm, D = _init(rank, world, port)
+    try:
+        rng = np.random.default_rng(21)
+        X = rng.standard_normal((rows, cols), dtype=np.float32)
+        w = (0.03 * rng.standard_normal((cols, 1))).astype(np.float32)
+        y = (rng.random((rows, 1)) < 0.5).astype(np.float32)
+        r0, rc = D.column_block(rows, rank, world)
+        Xl = dm.Matrix.from_numpy(np.asfortranarray(X[r0:r0 + rc]))
+        yl = dm.Matrix.from_numpy(np.asfortranarray(y[r0:r0 + rc]))
+        wm = dm.Matrix.from_numpy(w)
+        out = {}
+        for coll in ("p2p_fused", "all_gather"):
+            for step in range(2):             # two steps: both exchange parities
+                g, s = D.sharded_logistic_step(Xl, wm, yl, collective=coll)
+            out[coll] = (g.to_numpy().tobytes(), np.float32(s).tobytes(), D._LAST["logistic_collective"])
+        # the single-device step on the full matrix (every rank computes it)
+        Xf, yf = dm.Matrix.from_numpy(X), dm.Matrix.from_numpy(y)
+        r_e = 1 / (1 + dm.exp(0 - Xf @ wm)) - yf
+        r, gf = dm.evaluate_many(r_e, Xf.t() @ r_e)
+        sf = dm.accu(r)
+        q.put((rank, out, gf.to_numpy().astype(np.float64), float(sf)))
+        dist.barrier()
+        D.close_exchanges()
+        dm.shutdown()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,rows,cols", [(2, 1 << 16, 256), (3, 3 * 8192 * 4, 1024), (2, 65536, 2000)])
+def test_sharded_logistic_exchange_matches_all_gather(world, rows, cols):
+    """bm_exchange_gsum (g and the sum-cached accu(r) of every rank in one kernel
+    over CUDA IPC peer memory, folded in rank order) gives the bits of the NCCL /
+    gloo all-gather path -- gathered columns summed along dim 1, accu exchanged --
+    on every rank, and matches the single-device step."""
+    res = _collect(world, _logistic_worker, rows, cols)
+    for rank, out, gf, sf in res:
+        assert out["p2p_fused"][2] == "peer" and out["all_gather"][2] == "gather"
+        assert out["p2p_fused"][:2] == out["all_gather"][:2], f"rank {rank}: exchange differs from all-gather"
+        assert out["p2p_fused"][:2] == res[0][1]["p2p_fused"][:2], "ranks disagree"
+        g = np.frombuffer(out["p2p_fused"][0], dtype=np.float32).astype(np.float64)
+        assert np.abs(g - gf.reshape(-1)).max() <= 1e-5 * np.abs(gf).max()
+        s = float(np.frombuffer(out["p2p_fused"][1], dtype=np.float32)[0])
+        assert abs(s - sf) <= 1e-5 * max(abs(sf), 1.0)

@@ -678,6 +678,7 @@ def sharded_suite(dm, torch, rank: int, world: int) -> dict:
             nb = 8 * nr * nr
             out[f"cfg2_{op}_dim1_16384^2_f64_sharded"] = {
                 "ms": ms, "GB/s": nb / ms / 1e6, "scaling": "strong",
+                "collective": D._LAST.get("rows_collective"),
                 "parity": {"vs": "single-device reduction on each rank's GPU", "tol": 1e-12 if op == "sum" else 0.0,
                            "max_rel_err": err, "bit_exact_all_ranks": notexact == 0.0,
                            "note": "sum: each rank folds its columns, then the rank partials are folded in rank "

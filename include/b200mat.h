@@ -275,18 +275,24 @@ int bm_combine_partials_to_device(const void* dev_partials, int64_t count, int32
  * bm_combine_partials_to_device into dev_result. */
 int bm_exchange_alloc(int32_t world, void** dev_buffer, void* ipc_handle /* 64 bytes out */);
 int bm_exchange_open(const void* ipc_handle, void** dev_buffer);
-/* vector variant (the sample-sharded logistic step): a buffer for
- * `n` f32 values + one f32 scalar per rank, opened / closed like the scalar one.
- * bm_exchange_gsum (ONE kernel): writes this rank's g (n f32) and s (1 f32) into every
- * rank's buffer over peer memory, publishes `epoch`, waits for every rank, and writes
- * g_out[i] = g_0[i] + g_1[i] + ... (rank order, f32 -- the dim-1 sum over the gathered
- * k x world matrix) and s_out = combine_pairwise(s_0 .. s_{world-1}) + 0.0f.  Replaces
- * the NCCL all-gather of g (dist.py:gather_columns, SURVEY 8e "ncclAllReduce of 1024
- * f32"), its fold and the accu exchange; a peer that never publishes sets BM_ERR_PEER
- * at the next bm_sync. */
-int bm_exchange_alloc_vec(int32_t world, int64_t n, void** dev_buffer, void* ipc_handle /* 64 bytes out */);
+/* vector variants: a buffer whose per-rank slot holds `cap` 4-byte units (plus one
+ * f32 scalar), opened / closed like the scalar one.  Each call is ONE kernel that writes
+ * this rank's vector into every rank's buffer over peer memory, publishes `epoch`, waits
+ * for every rank and folds in rank order -- the replacement of an NCCL all-gather of
+ * one vector per rank and the dim-1 reduction over the gathered rows x world matrix
+ * (dist.py gather_columns + sum/min/max(., 1)); `cap` must be the allocation's.
+ *   bm_exchange_rows (config 2 dim-1 reductions): out[i] = x_0[i] op x_1[i]
+ *     op ... -- left to right for BM_R_ACCU (the sum), numpy's NaN-propagating min / max.
+ *   bm_exchange_gsum (config 5, the sample-sharded logistic step): g_out = the rank-order
+ *     sum of the ranks' n f32 gradients, s_out = combine_pairwise(s_0 .. s_{world-1}) +
+ *     0.0f (every rank's folded accu(r)).
+ * A peer that never publishes sets BM_ERR_PEER at the next bm_sync. */
+int bm_exchange_alloc_vec(int32_t world, int64_t cap, void** dev_buffer, void* ipc_handle /* 64 bytes out */);
+int bm_exchange_rows(const void* dev_x, int64_t n, int32_t dtype, int32_t reduce_op,
+                     void* const* peer_buffers /* host array */, int32_t world, int32_t rank, uint64_t epoch,
+                     int64_t cap, void* dev_out);
 int bm_exchange_gsum(const float* dev_g, int64_t n, const float* dev_s, void* const* peer_buffers /* host array */,
-                     int32_t world, int32_t rank, uint64_t epoch, float* dev_g_out, float* dev_s_out);
+                     int32_t world, int32_t rank, uint64_t epoch, int64_t cap, float* dev_g_out, float* dev_s_out);
 int bm_exchange_close(void* dev_buffer, int32_t opened /* 1: mapped peer buffer, 0: own */);
 /* the reduction and the exchange in ONE kernel: like bm_reduce_to_device, but the
  * reduction's last CTA publishes the shard partial into every rank's exchange buffer,

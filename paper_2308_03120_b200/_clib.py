@@ -95,7 +95,10 @@ SIGNATURES = {
     "bm_exchange_alloc": ([_I32, ctypes.POINTER(_VP), _VP], ctypes.c_int),
     "bm_exchange_open": ([_VP, ctypes.POINTER(_VP)], ctypes.c_int),
     "bm_exchange_alloc_vec": ([_I32, _I64, ctypes.POINTER(_VP), _VP], ctypes.c_int),
-    "bm_exchange_gsum": ([_VP, _I64, _VP, ctypes.POINTER(_VP), _I32, _I32, ctypes.c_uint64, _VP, _VP], ctypes.c_int),
+    "bm_exchange_gsum": ([_VP, _I64, _VP, ctypes.POINTER(_VP), _I32, _I32, ctypes.c_uint64, _I64, _VP, _VP],
+                         ctypes.c_int),
+    "bm_exchange_rows": ([_VP, _I64, _I32, _I32, ctypes.POINTER(_VP), _I32, _I32, ctypes.c_uint64, _I64, _VP],
+                         ctypes.c_int),
     "bm_exchange_close": ([_VP, _I32], ctypes.c_int),
     "bm_reduce_to_device_exchange": ([ctypes.POINTER(Invocation), _VP, _VP, _I32, _I32, ctypes.c_uint64], ctypes.c_int),
     "bm_exchange_combine": ([_VP, ctypes.POINTER(_VP), _I32, _I32, ctypes.c_uint64, _I32, _I32, _VP], ctypes.c_int),

@@ -42,35 +42,41 @@ __global__ void __launch_bounds__(256) exchange_combine_kernel(const A* __restri
 }
 
 // ---------------------------------------------------------------------------
-// Vector exchange (the sample-sharded logistic step): every
-// rank's k gradient values and its accu(r) partial travel over peer memory in
-// ONE kernel, which also folds them -- the replacement of the NCCL all-gather
-// of g, the dim-1 sum over the gathered columns and the separate accu exchange.
-// Buffer of every rank, per parity (epoch & 1): [world slots of `slot` f32
-// values][world u64 flags]; slot r holds rank r's g (n values) and s (at n).
-// g is folded left to right in rank order, like sum(gathered, 1) over the
-// k x world matrix of the all-gather path (each row x_0 + x_1 + ...); s with
-// combine_pairwise over the ranks + 0.0f, like exchange_combine for a float accu.
+// Vector exchange over peer memory, folded in ONE kernel: the replacement of an
+// NCCL all-gather of one vector per rank plus the dim-1 reduction over the
+// gathered rows x world matrix (dist.gather_columns + sum/min/max(., 1)).
+//   rows  (config 2 dim-1 reductions): out[i] = x_0[i] (op) x_1[i] ...
+//         in rank order -- left to right for the sum (what the dim-1 reduction
+//         of the gathered matrix computes), numpy's NaN-propagating min / max;
+//   gsum  (config 5, the sample-sharded logistic step): the same sum over the
+//         ranks' gradients, plus every rank's folded accu(r) combined with
+//         combine_pairwise + 0.0f, as the scalar exchange does for a float accu.
+// Buffer of every rank, per parity (epoch & 1): [world slots of `slot` bytes]
+// [world u64 flags]; a slot holds the rank's vector and, for gsum, its f32
+// scalar after it.  `cap` (bm_exchange_alloc_vec) sizes the slots in 4-byte
+// units: a vector of n T plus the scalar needs n * sizeof(T) / 4 + 1 <= cap.
 
-__host__ __device__ inline size_t vx_slot(long long n) { return (size_t)((n + 1 + 3) / 4 * 4); }
-__host__ __device__ inline size_t vx_parity_bytes(int world, long long n) {
-    return ((size_t)world * vx_slot(n) * 4 + 15) / 16 * 16 + (size_t)world * 8;
+__host__ __device__ inline size_t vx_slot_bytes(long long cap) { return (size_t)((4 * (cap + 1) + 15) / 16 * 16); }
+__host__ __device__ inline size_t vx_flags_off(int world, long long cap) { return (size_t)world * vx_slot_bytes(cap); }
+__host__ __device__ inline size_t vx_parity_bytes(int world, long long cap) {
+    return vx_flags_off(world, cap) + (size_t)world * 8;
 }
 
-__global__ void __launch_bounds__(512) exchange_gsum_kernel(const float* __restrict__ g, long long n,
-                                                            const float* __restrict__ s, PeerPtrs peers, int W, int R,
-                                                            unsigned long long ep, float* __restrict__ g_out,
-                                                            float* __restrict__ s_out, unsigned int* err,
-                                                            unsigned long long timeout_ns) {
+template <typename T, int OP, bool SCALAR>
+__global__ void __launch_bounds__(512) exchange_vec_kernel(const T* __restrict__ x, long long n,
+                                                           const float* __restrict__ s, PeerPtrs peers, int W, int R,
+                                                           unsigned long long ep, long long cap, T* __restrict__ out,
+                                                           float* __restrict__ s_out, unsigned int* err,
+                                                           unsigned long long timeout_ns) {
     __shared__ float xv[2 * 64];
-    const size_t slot = vx_slot(n);
-    const size_t pbytes = vx_parity_bytes(W, n);
-    const size_t base = (size_t)(ep & 1) * pbytes;
-    const size_t flags = ((size_t)W * slot * 4 + 15) / 16 * 16;
-    // publish: this rank's n + 1 values into slot R of every rank's buffer (NVLink stores)
+    const size_t slot = vx_slot_bytes(cap);
+    const size_t base = (size_t)(ep & 1) * vx_parity_bytes(W, cap);
+    const size_t flags = vx_flags_off(W, cap);
+    // publish: this rank's vector (and scalar) into slot R of every rank's buffer
     for (int p = 0; p < W; ++p) {
-        float* dst = reinterpret_cast<float*>(reinterpret_cast<char*>(peers.p[p]) + base) + (size_t)R * slot;
-        for (long long i = threadIdx.x; i <= n; i += blockDim.x) dst[i] = i < n ? g[i] : s[0];
+        char* dst = reinterpret_cast<char*>(peers.p[p]) + base + (size_t)R * slot;
+        for (long long i = threadIdx.x; i < n; i += blockDim.x) reinterpret_cast<T*>(dst)[i] = x[i];
+        if (SCALAR && threadIdx.x == 0) *reinterpret_cast<float*>(dst + (size_t)n * sizeof(T)) = s[0];
     }
     __threadfence_system();            // every value lands before any flag says so
     __syncthreads();
@@ -94,16 +100,25 @@ __global__ void __launch_bounds__(512) exchange_gsum_kernel(const float* __restr
         if (f < ep && err) atomicOr_system(err, BM_DEVERR_PEER_TIMEOUT);
     }
     __syncthreads();
-    const float* v = reinterpret_cast<const float*>(mine);
     for (long long i = threadIdx.x; i < n; i += blockDim.x) {
-        float acc = *reinterpret_cast<const volatile float*>(v + i);
-        for (int p = 1; p < W; ++p) acc = acc + *reinterpret_cast<const volatile float*>(v + (size_t)p * slot + i);
-        g_out[i] = acc;
+        auto at = [&](int p) { return *reinterpret_cast<const volatile T*>(mine + (size_t)p * slot + (size_t)i * sizeof(T)); };
+        if constexpr (OP == 1) {
+            T acc = at(0);
+            for (int p = 1; p < W; ++p) acc = OpPlus::f(acc, at(p));
+            out[i] = acc;
+        } else {
+            MinMaxAcc<T, OP == 3> mm;
+            for (int p = 0; p < W; ++p) mm.add(at(p));
+            out[i] = mm.result();
+        }
     }
-    for (int p = threadIdx.x; p < W; p += blockDim.x) xv[p] = *reinterpret_cast<const volatile float*>(v + (size_t)p * slot + n);
-    __syncthreads();
-    const float r = cta_combine_pairwise<float, 1>(xv, xv + W, W);
-    if (threadIdx.x == 0) s_out[0] = OpPlus::f(r, 0.0f);
+    if constexpr (SCALAR) {
+        for (int p = threadIdx.x; p < W; p += blockDim.x)
+            xv[p] = *reinterpret_cast<const volatile float*>(mine + (size_t)p * slot + (size_t)n * sizeof(T));
+        __syncthreads();
+        const float r = cta_combine_pairwise<float, 1>(xv, xv + W, W);
+        if (threadIdx.x == 0) s_out[0] = OpPlus::f(r, 0.0f);
+    }
 }
 
 }  // namespace bm
@@ -248,6 +263,48 @@ int exchange_empty_shard(int dtype, int op, void* const* dev_peers, int world, i
     return set_error(BM_ERR_ARG, "exchange: bad dtype");
 }
 
+static int vx_check(int32_t world, int32_t rank, uint64_t epoch, int64_t n, int64_t elem_bytes, int64_t cap) {
+    if (world < 1 || world > 64 || rank < 0 || rank >= world) return set_error(BM_ERR_ARG, "exchange: bad world/rank");
+    if (epoch == 0) return set_error(BM_ERR_ARG, "exchange: epochs start at 1");
+    if (n < 0 || cap < 0 || n * elem_bytes > 4 * cap)
+        return set_error(BM_ERR_ARG, "exchange: vector longer than the buffer's capacity");
+    return BM_OK;
+}
+
+static bm::PeerPtrs vx_peers(void* const* peer_buffers, int world) {
+    bm::PeerPtrs pp;
+    std::memset(&pp, 0, sizeof pp);
+    for (int i = 0; i < world; ++i) pp.p[i] = peer_buffers[i];
+    return pp;
+}
+
+template <typename T>
+static int rows_typed(const void* x, int64_t n, int op, bm::PeerPtrs pp, int world, int rank, uint64_t epoch,
+                      int64_t cap, void* out) {
+    switch (op) {
+        case BM_R_ACCU:
+            bm::exchange_vec_kernel<T, 1, false><<<1, 512, 0, st().stream>>>(
+                (const T*)x, (long long)n, nullptr, pp, world, rank, epoch, (long long)cap, (T*)out, nullptr,
+                st().err_dev, st().exch_timeout_ns);
+            break;
+        case BM_R_MIN:
+            bm::exchange_vec_kernel<T, 2, false><<<1, 512, 0, st().stream>>>(
+                (const T*)x, (long long)n, nullptr, pp, world, rank, epoch, (long long)cap, (T*)out, nullptr,
+                st().err_dev, st().exch_timeout_ns);
+            break;
+        case BM_R_MAX:
+            bm::exchange_vec_kernel<T, 3, false><<<1, 512, 0, st().stream>>>(
+                (const T*)x, (long long)n, nullptr, pp, world, rank, epoch, (long long)cap, (T*)out, nullptr,
+                st().err_dev, st().exch_timeout_ns);
+            break;
+        default:
+            return set_error(BM_ERR_ARG, "exchange rows: op must be accu (sum), min or max");
+    }
+    BM_CUDA(cudaGetLastError());
+    st().launches++;
+    return BM_OK;
+}
+
 }  // namespace bmi
 
 extern "C" {
@@ -266,12 +323,12 @@ int bm_exchange_alloc(int32_t world, void** dev_buffer, void* ipc_handle) {
     return BM_OK;
 }
 
-int bm_exchange_alloc_vec(int32_t world, int64_t n, void** dev_buffer, void* ipc_handle) {
+int bm_exchange_alloc_vec(int32_t world, int64_t cap, void** dev_buffer, void* ipc_handle) {
     using namespace bmi;
     BM_REQUIRE_INIT();
     if (world < 1 || world > 64) return set_error(BM_ERR_ARG, "exchange: world out of range");
-    if (n < 0 || n > (1 << 20)) return set_error(BM_ERR_ARG, "exchange: vector length out of range");
-    const size_t bytes = 2 * bm::vx_parity_bytes(world, n);
+    if (cap < 0 || cap > (1 << 22)) return set_error(BM_ERR_ARG, "exchange: vector capacity out of range");
+    const size_t bytes = 2 * bm::vx_parity_bytes(world, cap);
     BM_CUDA(cudaMalloc(dev_buffer, bytes));
     BM_CUDA(cudaMemset(*dev_buffer, 0, bytes));
     cudaIpcMemHandle_t h;
@@ -281,22 +338,36 @@ int bm_exchange_alloc_vec(int32_t world, int64_t n, void** dev_buffer, void* ipc
 }
 
 int bm_exchange_gsum(const float* dev_g, int64_t n, const float* dev_s, void* const* peer_buffers, int32_t world,
-                     int32_t rank, uint64_t epoch, float* dev_g_out, float* dev_s_out) {
+                     int32_t rank, uint64_t epoch, int64_t cap, float* dev_g_out, float* dev_s_out) {
     using namespace bmi;
     BM_REQUIRE_INIT();
-    if (world < 1 || world > 64 || rank < 0 || rank >= world) return set_error(BM_ERR_ARG, "exchange: bad world/rank");
-    if (epoch == 0) return set_error(BM_ERR_ARG, "exchange: epochs start at 1");
-    if (n < 0 || n > (1 << 20) || !dev_s || (n > 0 && (!dev_g || !dev_g_out)) || !dev_s_out)
-        return set_error(BM_ERR_ARG, "exchange: bad vector arguments");
+    if (int rc = bmi::vx_check(world, rank, epoch, n, 4, cap)) return rc;
+    if (!dev_s || !dev_s_out || (n > 0 && (!dev_g || !dev_g_out))) return set_error(BM_ERR_ARG, "exchange: null buffer");
     std::lock_guard<std::recursive_mutex> lk(st().mu);
-    bm::PeerPtrs pp;
-    std::memset(&pp, 0, sizeof pp);
-    for (int i = 0; i < world; ++i) pp.p[i] = peer_buffers[i];
-    bm::exchange_gsum_kernel<<<1, 512, 0, st().stream>>>(dev_g, (long long)n, dev_s, pp, world, rank, epoch, dev_g_out,
-                                                          dev_s_out, st().err_dev, st().exch_timeout_ns);
+    bm::exchange_vec_kernel<float, 1, true><<<1, 512, 0, st().stream>>>(
+        dev_g, (long long)n, dev_s, bmi::vx_peers(peer_buffers, world), world, rank, epoch, (long long)cap, dev_g_out,
+        dev_s_out, st().err_dev, st().exch_timeout_ns);
     BM_CUDA(cudaGetLastError());
     st().launches++;
     return BM_OK;
+}
+
+int bm_exchange_rows(const void* dev_x, int64_t n, int32_t dtype, int32_t reduce_op, void* const* peer_buffers,
+                     int32_t world, int32_t rank, uint64_t epoch, int64_t cap, void* dev_out) {
+    using namespace bmi;
+    BM_REQUIRE_INIT();
+    const int64_t eb = dtype == BM_F64 || dtype == BM_U64 ? 8 : 4;
+    if (int rc = bmi::vx_check(world, rank, epoch, n, eb, cap)) return rc;
+    if (n > 0 && (!dev_x || !dev_out)) return set_error(BM_ERR_ARG, "exchange: null buffer");
+    std::lock_guard<std::recursive_mutex> lk(st().mu);
+    const bm::PeerPtrs pp = bmi::vx_peers(peer_buffers, world);
+    switch (dtype) {
+        case BM_F32: return bmi::rows_typed<float>(dev_x, n, reduce_op, pp, world, rank, epoch, cap, dev_out);
+        case BM_F64: return bmi::rows_typed<double>(dev_x, n, reduce_op, pp, world, rank, epoch, cap, dev_out);
+        case BM_I32: return bmi::rows_typed<int>(dev_x, n, reduce_op, pp, world, rank, epoch, cap, dev_out);
+        case BM_U64: return bmi::rows_typed<unsigned long long>(dev_x, n, reduce_op, pp, world, rank, epoch, cap, dev_out);
+    }
+    return set_error(BM_ERR_ARG, "exchange: bad dtype");
 }
 
 int bm_exchange_open(const void* ipc_handle, void** dev_buffer) {

@@ -62,7 +62,7 @@ class PeerExchange:
         import torch.distributed as dist
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
-        self.nvals = nvals                  # None: one value per rank; n: n f32 + one f32 scalar (gsum)
+        self.nvals = nvals                  # None: one value per rank; else the slot capacity in 4-byte units
         self._lib = _clib.lib()
         self._own = None
         self._opened = []
@@ -128,7 +128,17 @@ class PeerExchange:
         self.epoch += 1
         _clib.check(self._lib.bm_exchange_gsum(
             ctypes.c_void_p(g_ptr), n, ctypes.c_void_p(s_ptr), self._ptrs, self.world, self.rank, self.epoch,
-            ctypes.c_void_p(g_out_ptr), ctypes.c_void_p(s_out_ptr)), "exchange gsum")
+            self.nvals, ctypes.c_void_p(g_out_ptr), ctypes.c_void_p(s_out_ptr)), "exchange gsum")
+
+    def rows(self, x_ptr: int, n: int, elem: str, op_code: int, out_ptr: int) -> None:
+        """Vector buffers only: out = the rank-order fold (sum / min / max) of every
+        rank's n-vector, in one kernel (bm_exchange_rows)."""
+        if self.nvals is None or n * kernels.itemsize(elem) > 4 * self.nvals:
+            raise ValueError("rows needs a vector exchange with room for n values")
+        self.epoch += 1
+        _clib.check(self._lib.bm_exchange_rows(
+            ctypes.c_void_p(x_ptr), n, _clib.DTYPE_CODE[elem], op_code, self._ptrs, self.world, self.rank,
+            self.epoch, self.nvals, ctypes.c_void_p(out_ptr)), "exchange rows")
 
     def reduce(self, inv, result) -> None:
         """The shard reduction and the exchange in one kernel
@@ -479,7 +489,10 @@ def gather_columns(local, group=None):
     return out
 
 
-def sharded_reduce_dim(op: str, local_expr, dim: int, group=None):
+_LAST: dict = {}   # the path the last sharded call took ("peer" / "gather"; tests and bench)
+
+
+def sharded_reduce_dim(op: str, local_expr, dim: int, group=None, collective=None):
     """sum/min/max along `dim` of a column-block-sharded matrix.
 
     dim 0 (one value per column): every rank owns its columns' results, no
@@ -487,12 +500,29 @@ def sharded_reduce_dim(op: str, local_expr, dim: int, group=None):
     to a rows x 1 partial, the partials are all-gathered in rank order and
     folded with the same device reduction along dim 1 -- a left-to-right fold
     0 + p_0 + p_1 + ..., deterministic for a given world size (min/max are
-    exact).  Returns the local dim-0 block or the full dim-1 column."""
+    exact).  Returns the local dim-0 block or the full dim-1 column.  With
+    peer memory (collective "p2p"/"p2p_fused", the default) the all-gather
+    and the fold are one kernel (bm_exchange_rows), with the same bits."""
     from . import ops
     fn = {"sum": ops.sum, "min": ops.min, "max": ops.max}[op]
     local = _expr.evaluate(fn(local_expr, dim))
     if dim == 0 or _world(group)[1] == 1:
         return local
+    if collective is None:
+        collective = os.environ.get("BM_SHARD_COLLECTIVE", "p2p_fused")
+    if collective in ("p2p", "p2p_fused"):
+        # one kernel: every rank's partial over peer memory, folded in rank order
+        cap = (local.n_elem * kernels.itemsize(local.elem_type) + 3) // 4
+        ex = shared_vec_exchange(cap, group)
+        if ex is not None:
+            from .matrix import Matrix
+            out = Matrix._uninitialised(local.n_rows, local.n_cols, local.elem_type)
+            ex.rows(local.mem.ptr, local.n_elem, local.elem_type,
+                    {"sum": _clib.BM_R_ACCU, "min": _clib.BM_R_MIN, "max": _clib.BM_R_MAX}[op], out.mem.ptr)
+            _check_exchange_error(ex)
+            _LAST["rows_collective"] = "peer"
+            return out
+    _LAST["rows_collective"] = "gather"
     return _expr.evaluate(fn(gather_columns(local, group), 1))
 
 
@@ -501,9 +531,6 @@ def sharded_gemm_nt(a, b_local):
     holds B's row block r and A replicated (broadcast_matrix), and computes
     its column block of C with no communication."""
     return _expr.evaluate(a @ b_local.t())
-
-
-_LAST: dict = {}   # the path the last sharded_logistic_step took ("peer" / "gather"; tests and bench)
 
 
 def sharded_logistic_step(x_local, w, y_local, group=None, collective=None):

@@ -260,3 +260,44 @@ def test_sharded_logistic_exchange_matches_all_gather(world, rows, cols):
         assert np.abs(g - gf.reshape(-1)).max() <= 1e-5 * np.abs(gf).max()
         s = float(np.frombuffer(out["p2p_fused"][1], dtype=np.float32)[0])
         assert abs(s - sf) <= 1e-5 * max(abs(sf), 1.0)
+
+
+def _rows_worker(rank, world, port, q, rows, cols, elem):
+    dm, D = _init(rank, world, port)
+    try:
+        dt = np.float32 if elem == "f32" else np.float64
+        full = np.random.default_rng(23).random((rows, cols)).astype(dt)
+        full[3, 5] = -0.0
+        c0, cc = D.column_block(cols, rank, world)
+        m = dm.Matrix.from_numpy(np.asfortranarray(full[:, c0:c0 + cc]))
+        out = {}
+        for op in ("sum", "min", "max"):
+            got = {}
+            for coll in ("p2p_fused", "all_gather"):
+                for _ in range(2):              # both exchange parities
+                    v = D.sharded_reduce_dim(op, m, 1, collective=coll)
+                got[coll] = (v.to_numpy().tobytes(), D._LAST["rows_collective"])
+            out[op] = got
+        single = {op: getattr(dm, op)(dm.Matrix.from_numpy(full), 1) for op in ("sum", "min", "max")}
+        q.put((rank, out, {op: dm.evaluate(v).to_numpy().tobytes() for op, v in single.items()}))
+        dist.barrier()
+        D.close_exchanges()
+        dm.shutdown()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,rows,cols,elem", [(2, 16384, 512, "f64"), (3, 4096, 300, "f32"), (4, 1000, 64, "f64")])
+def test_sharded_row_reductions_exchange_matches_all_gather(world, rows, cols, elem):
+    """bm_exchange_rows (every rank's dim-1 partial over peer memory, folded in
+    rank order in one kernel) gives the bits of the all-gather + dim-1 fold on
+    every rank; min / max are the single-device values exactly."""
+    res = _collect(world, _rows_worker, rows, cols, elem)
+    for rank, out, single in res:
+        for op, got in out.items():
+            assert got["p2p_fused"][1] == "peer" and got["all_gather"][1] == "gather"
+            assert got["p2p_fused"][0] == got["all_gather"][0], f"rank {rank} {op}: exchange differs"
+            assert got["p2p_fused"][0] == res[0][1][op]["p2p_fused"][0], "ranks disagree"
+            if op != "sum":
+                assert got["p2p_fused"][0] == single[op]

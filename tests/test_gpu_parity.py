@@ -976,20 +976,23 @@ sys.path.insert(0, sys.argv[1])
 import paper_2308_03120_b200 as dm
 dm.init("b200")
 rng = np.random.default_rng(11)
-a = dm.Matrix.from_numpy(rng.random((4096, 2048), dtype=np.float32))
-b = dm.Matrix.from_numpy(rng.random((4000, 2048), dtype=np.float32))
-prod = a @ b.t()
-plain = dm.evaluate(prod).to_numpy()
-epi = dm.evaluate(dm.exp(prod / 2048) * 3 - 1).to_numpy()
-np.save(sys.argv[2], np.stack([plain, epi]))
+outs = []
+for m, n, k in ((4096, 4000, 2048), (2304, 5000, 700), (8192, 256, 1030)):
+    a = dm.Matrix.from_numpy(rng.random((m, k), dtype=np.float32))
+    b = dm.Matrix.from_numpy(rng.random((n, k), dtype=np.float32))
+    prod = a @ b.t()
+    outs.append(dm.evaluate(prod).to_numpy().reshape(-1))
+    outs.append(dm.evaluate(dm.exp(prod / k) * 3 - 1).to_numpy().reshape(-1))
+np.save(sys.argv[2], np.concatenate(outs))
 dm.shutdown()
 """
 
 
 def test_gemm_persistent_pairs_bit_identical(tmp_path):
-    """BM_GEMM_PERSIST=1: 74 resident CTA pairs claim the 256 x 256 tiles from a
-    global counter (four K passes here, each with its own counter) -- the
-    same bits as one pair per tile, for the plain GEMM and a fused epilogue."""
+    """BM_GEMM_PERSIST=1 (the default): 74 resident CTA pairs claim the 256 x 256
+    tiles from a global counter (several K passes here, each with its own
+    counter) -- the same bits as one pair per tile, for the plain GEMM and a
+    fused epilogue, at shapes with many tiles, ragged tiles and one tile column."""
     import os
     import pathlib
     import subprocess

@@ -322,8 +322,10 @@ int gemm_tc_f32_core(int64_t m, int64_t n, int64_t k, const SplitFn& split_a, co
         static const int group_env = std::getenv("BM_GEMM_GROUP") ? std::atoi(std::getenv("BM_GEMM_GROUP")) : 0;
         // persistent pairs: 8 pair rows up to 8192 x 8192 outputs (4096^3..8192^3: 0.6-1 %
         // faster than 4, interleaved on one box), 4 above (16384^3: 1 %, 32768^3: 4 % faster
-        // than 8; profiles/r02_gemm_group_sweep.txt)
-        const int group_m = group_env > 0 ? group_env : (pair ? (mp <= 8192 && np <= 8192 ? 8 : 4) : 8);
+        // than 8; profiles/r02_gemm_group_sweep.txt); one pair per tile (staged epilogues):
+        // 4, as tuned for that launch shape
+        const int group_m = group_env > 0 ? group_env
+                                          : (pair ? (persistent && mp <= 8192 && np <= 8192 ? 8 : 4) : 8);
         // Long K runs as several stream-ordered passes of at most kpass K
         // (the later ones add into C): within one launch the resident CTAs
         // drift apart along K, and at K = 32768 their A/B slabs stop meeting

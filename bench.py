@@ -514,8 +514,8 @@ def secondary_suite(dm, torch, cpu: bool) -> dict:
                     out["cfg4_epilogue_axpby_8192^3_f32"] = {
                         "ms": tf_, "TFLOP/s": flops / tf_ / 1e9, "unfused_ms": tu_, "reps": 10,
                         "plan": [st_.kernel for st_ in dm.plan(ax).steps],
-                        "note": "2 A @ B.t() + 3 C: C staged into shared memory by the epilogue warps once the "
-                                "tile's MMAs are complete, the tree evaluated in the store",
+                        "note": "2 A @ B.t() + 3 C: C staged into shared memory by the epilogue warps during the main loop "
+                                "(double-buffered 32-column chunks), the tree evaluated in the store",
                         "parity": {"vs": "the unfused plan (product materialised, then the chain)",
                                    "bit_exact": bool(torch.equal(fz, uz))}}
                     del fz, uz, fm_, um_, ax, Cm

@@ -308,9 +308,8 @@ int gemm_tc_f32_core(int64_t m, int64_t n, int64_t k, const SplitFn& split_a, co
         // under this tile's epilogue: 0.5-1 % over one pair per tile after the barrier-scope
         // fix (8192^3 3.97-3.99 vs 4.00-4.01 ms, 16384^3 34.5-34.6 vs 34.6-35.0 ms).  (A
         // static share per pair -- tiles p, p + P, ... -- was 3-15 % slower: the pairs
-        // drift apart along the raster and their operand slabs stop sharing L2.)  A staged
-        // epilogue needs the TMA ring idle after its tile: one tile per pair.
-        const bool persist = gemm_pair_persistent() && !(epi && epi->staged);
+        // drift apart along the raster and their operand slabs stop sharing L2.)
+        const bool persist = gemm_pair_persistent();
         bool persistent = false;
         if (pair && persist && grid.x > (unsigned)(st().sm_count / 2 * 2)) {
             grid.x = (unsigned)(st().sm_count / 2 * 2);
@@ -322,7 +321,7 @@ int gemm_tc_f32_core(int64_t m, int64_t n, int64_t k, const SplitFn& split_a, co
         static const int group_env = std::getenv("BM_GEMM_GROUP") ? std::atoi(std::getenv("BM_GEMM_GROUP")) : 0;
         // persistent pairs: 8 pair rows up to 8192 x 8192 outputs (4096^3..8192^3: 0.6-1 %
         // faster than 4, interleaved on one box), 4 above (16384^3: 1 %, 32768^3: 4 % faster
-        // than 8; profiles/r02_gemm_group_sweep.txt); one pair per tile (staged epilogues):
+        // than 8; profiles/r02_gemm_group_sweep.txt); one pair per tile (BM_GEMM_PERSIST=0):
         // 4, as tuned for that launch shape
         const int group_m = group_env > 0 ? group_env
                                           : (pair ? (persistent && mp <= 8192 && np <= 8192 ? 8 : 4) : 8);
@@ -348,7 +347,8 @@ int gemm_tc_f32_core(int64_t m, int64_t n, int64_t k, const SplitFn& split_a, co
                 float* Cp = C;
                 void* params[] = {&tm[0], &tm[1], &tm[2], &tm[3], &Cp, &mm, &nn, &lc, &nkl, &gm, &k0, &acc,
                                   const_cast<void*>(epi->args), &apply, &tile_ctr};
-                CUresult cr = drv().launchKernel((CUfunction)epi->fn, grid.x, 1, 1, T2_THREADS, 1, 1, T2_SMEM, (CUstream)s,
+                CUresult cr = drv().launchKernel((CUfunction)epi->fn, grid.x, 1, 1, T2_THREADS, 1, 1,
+                                                 epi->smem > 0 ? epi->smem : T2_SMEM, (CUstream)s,
                                                  params, nullptr);
                 if (cr != CUDA_SUCCESS) {
                     rc = cu_fail(cr, "cuLaunchKernel (3xTF32 GEMM, fused epilogue)");

@@ -89,11 +89,21 @@ __host__ __device__ constexpr uint32_t tf32_idesc(int m, int n) {
 
 #define T2_BM 128                         // A rows per CTA (256 per pair)
 #define T2_BNH 128                        // B columns per CTA (256 per pair)
+#ifndef T2_STAGES
 #define T2_STAGES 6
+#endif
+// Staged epilogue input (EPI::kStage): a dedicated shared-memory region behind the
+// barriers, two 32-column chunks per epilogue warp (2 x 32 x 32 f32 = 8 KB), so the
+// input never waits for the TMA ring and persistent pairs keep running.  Kernels that
+// stage are compiled with a 5-stage ring (T2_STAGES 5, T2_STAGE_EXTRA below) to make room.
+#ifndef T2_STAGE_EXTRA
+#define T2_STAGE_EXTRA 0
+#endif
+#define T2_SC 32                                   // columns per staged chunk
 #define T2_TILE_A (T2_BM * TC_BK * 4)
 #define T2_TILE_B (T2_BNH * TC_BK * 4)
 #define T2_STAGE_BYTES (2 * T2_TILE_A + 2 * T2_TILE_B)
-#define T2_SMEM (T2_STAGES * T2_STAGE_BYTES + 1024 + 256)
+#define T2_SMEM (T2_STAGES * T2_STAGE_BYTES + 1024 + 256 + T2_STAGE_EXTRA)
 
 __device__ __forceinline__ uint32_t t2_mapa(const void* p, uint32_t rank) {
     uint32_t r;
@@ -359,34 +369,39 @@ __device__ __forceinline__ void gemm_pair_body(const TmapBytes& tm_ahi, const Tm
         tile_coords(t, m0, n0);
         const i64 row = (i64)m0 + 32 * q + lane;
         // An epilogue that reads an f32 matrix (e.g. alpha AB^T + beta C) stages this warp's
-        // 32 x T2_EC slice of it into shared memory with one burst of 16-byte cp.async issued
-        // when the last chunk's MMAs are complete -- the TMA ring is idle then (the pair has
-        // no next tile) -- instead of T2_EC dependent load rounds per thread after the drain.
-        // T2_EW warps x 32 x T2_EC x 4 B = 128 KB of the 192 KB ring.
-        float* stage_buf = reinterpret_cast<float*>(smem) + (warp - 2) * (32 * T2_EC);
+        // 32 x T2_EC slice of it through its own double buffer of two 32-column chunks
+        // (16-byte cp.async, one group per chunk): chunks 0 and 1 are issued when the tile
+        // starts, so they land during the main loop; chunk c + 2 is issued while chunk c is
+        // evaluated.  The host launches a staging kernel only when the input has unit
+        // stride, a 16-byte base and 4 | m (bm_jit.cu epi_stage_ready); the kernel has no
+        // other path for the program, so a violation traps.
+        float* stage_buf = reinterpret_cast<float*>(smem + T2_STAGES * T2_STAGE_BYTES + 256) +
+                           (warp - 2) * (2 * 32 * T2_SC);
         bool staged = false;
         if constexpr (EPI::kStage) {
-            // the host launches a staged kernel only when these hold (bm_jit.cu epi_stage_ready);
-            // the kernel has no other path for the program, so a violation traps
+            static_assert(!EPI::kStage || T2_STAGE_EXTRA >= T2_EW * 2 * 32 * T2_SC * 4, "staging region too small");
             const float* src = EPI::stage_src(ea);
             staged = apply;
-            if (apply && !(tile_ctr == nullptr && pair + npairs >= ntiles && EPI::stage_ok(ea) && (m & 3) == 0 &&
-                           ((reinterpret_cast<uintptr_t>(src) & 15u) == 0)))
+            if (apply && !(EPI::stage_ok(ea) && (m & 3) == 0 && ((reinterpret_cast<uintptr_t>(src) & 15u) == 0)))
                 __trap();
         }
-        auto stage_issue = [&]() {
+        auto stage_issue = [&](int ci) {       // chunk ci into buffer ci & 1
             const float* src = EPI::stage_src(ea);
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // the ring was last touched by TMA / MMA
             const i64 rr = (i64)m0 + 32 * q + 4 * (lane & 7);
-#pragma unroll 8
-            for (int cb = 0; cb < T2_EC; cb += 4) {
+            float* dst = stage_buf + (ci & 1) * (32 * T2_SC);
+#pragma unroll
+            for (int cb = 0; cb < T2_SC; cb += 4) {
                 const int cl = cb + (lane >> 3);
-                const i64 col = (i64)n0 + h * T2_EC + cl;
+                const i64 col = (i64)n0 + h * T2_EC + ci * T2_SC + cl;
                 const bool ok = col < n && rr < m;     // m % 4 == 0: rr < m covers rr + 3
-                t2_cp_async16(stage_buf + cl * 32 + 4 * (lane & 7), ok ? src + rr + col * m : src, ok);
+                t2_cp_async16(dst + cl * 32 + 4 * (lane & 7), ok ? src + rr + col * m : src, ok);
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
         };
+        if (staged) {
+            stage_issue(0);
+            stage_issue(1);
+        }
         float acc[T2_EC];
         if (accumulate && row < m) {
             const float* cp = C + row + ((i64)n0 + h * T2_EC) * ldc;
@@ -401,7 +416,6 @@ __device__ __forceinline__ void gemm_pair_body(const TmapBytes& tm_ahi, const Tm
             const int b = cc & 1;
             t2_wait(&acc_full[b], (uint32_t)((cc >> 1) & 1));
             tc_fence_after();
-            if (staged && c == nchunks - 1) stage_issue();   // every MMA of the tile is complete
             const uint32_t base = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(b * TC_BN + h * T2_EC);
 #pragma unroll
             for (int j = 0; j < T2_EC / 32; ++j) {
@@ -416,16 +430,24 @@ __device__ __forceinline__ void gemm_pair_body(const TmapBytes& tm_ahi, const Tm
             if (lane == 0) t2_arrive_remote_cta(t2_mapa(&acc_empty[b], 0));
         }
         if (staged) {
-            asm volatile("cp.async.wait_all;" ::: "memory");
-            __syncwarp();
-            if (row < m) {
+            constexpr int NCH = T2_EC / T2_SC;
 #pragma unroll
-                for (int t = 0; t < T2_EC; ++t) {
-                    const i64 col = (i64)n0 + h * T2_EC + t;
-                    typename EPI::Pre pre;
-                    EPI::stage_set(pre, stage_buf[t * 32 + lane]);
-                    if (col < n) C[row + col * ldc] = EPI::at(ea, pre, acc[t]);
+            for (int ci = 0; ci < NCH; ++ci) {
+                if (ci + 1 < NCH) asm volatile("cp.async.wait_group 1;" ::: "memory");
+                else asm volatile("cp.async.wait_group 0;" ::: "memory");
+                __syncwarp();
+                const float* sb = stage_buf + (ci & 1) * (32 * T2_SC);
+                if (row < m) {
+#pragma unroll
+                    for (int t = 0; t < T2_SC; ++t) {
+                        const i64 col = (i64)n0 + h * T2_EC + ci * T2_SC + t;
+                        typename EPI::Pre pre;
+                        EPI::stage_set(pre, sb[t * 32 + lane]);
+                        if (col < n) C[row + col * ldc] = EPI::at(ea, pre, acc[ci * T2_SC + t]);
+                    }
                 }
+                __syncwarp();                  // every lane is done with buffer ci & 1
+                if (ci + 2 < NCH) stage_issue(ci + 2);
             }
         } else if (row < m) {
             if (apply && !EPI::kStage) {   // last K pass: the fused element-wise epilogue (program input 0 = the product)

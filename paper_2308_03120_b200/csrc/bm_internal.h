@@ -105,7 +105,7 @@ typedef std::function<int(float* hi, float* lo, int64_t kp, int64_t rp)> SplitFn
 struct PairEpilogue {
     void* fn;            // CUfunction
     const void* args;    // bm::Args
-    bool staged = false; // stages a memory input through the TMA ring: one tile per CTA pair
+    int smem = 0;        // the kernel's dynamic shared memory (0: T2_SMEM)
 };
 int gemm_tc_f32_core(int64_t m, int64_t n, int64_t k, const SplitFn& split_a, const SplitFn& split_b, float* C,
                      int64_t ldc, bool* handled, const PairEpilogue* epi = nullptr);

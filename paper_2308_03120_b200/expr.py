@@ -782,7 +782,7 @@ class _Lowerer:
         rb = self.lower(b, elem)
         prog = self._fit_program(root, elem, pre=(g, ("gemm", None)))
         # Programs of the product alone, or (f32) of the product and one f32 matrix
-        # with 4 | rows, which the pair kernel stages through its idle TMA ring
+        # with 4 | rows, which the pair kernel stages through shared memory during the main loop
         # (8192^3: exp(AB^T/n) - C 4.53 ms fused vs 4.60 unfused, 2AB^T + 3C 4.45-4.58
         # vs 4.73-4.78; profiles/r02_gemm_persist.txt).  More inputs, f64 and odd row
         # counts read them with dependent loads after the drain: slower, the

@@ -789,7 +789,7 @@ class _Lowerer:
         # reference's plan unless BM_GEMM_EPI_INPUTS=1.
         mem = prog.inputs[1:]
         mem_ok = not mem or _EPI_MEM_INPUTS or (
-            elem == "f32" and len(mem) == 1 and self._ref_elem(mem[0]) == "f32" and s.rows % 4 == 0)
+            _EPI_STAGE and elem == "f32" and len(mem) == 1 and self._ref_elem(mem[0]) == "f32" and s.rows % 4 == 0)
         if not mem_ok or len(prog.stages) > 64 or \
                 prog.inputs[0] != ("gemm", None) or ("load", 0) not in prog.stages:
             del self.steps[mark[0]:]
@@ -986,6 +986,7 @@ _RECIPE_LOCK = threading.Lock()
 _RECIPES_ON = os.environ.get("BM_PLAN_CACHE", "1") != "0"
 _F64_PROLOGUE = os.environ.get("BM_F64_PROLOGUE", "0") == "1"   # f64 operand chains inside DMMA (off: slower)
 _EPI_MEM_INPUTS = os.environ.get("BM_GEMM_EPI_INPUTS", "0") == "1"   # epilogues that read other matrices (off: slower)
+_EPI_STAGE = os.environ.get("BM_GEMM_EPI_STAGE", "1") != "0"        # the kernel stages a one-matrix f32 input
 
 
 class _NoRecipe(Exception):

@@ -1195,7 +1195,6 @@ def evaluate(x, out=None, fuse: bool = True):
 
     node = as_expr(x)
     rt = runtime.get_runtime()
-    shape = shape_of(node)
     if out is not None and out.elem_type != node.elem_type:
         raise ElemTypeError(f"cannot assign {node.elem_type} expression to {out.elem_type} matrix; "
                             "convert explicitly")
@@ -1214,6 +1213,11 @@ def evaluate(x, out=None, fuse: bool = True):
             p = plan(node, node.elem_type, fuse=fuse)
         leaves = None
         leaf_ids = None
+    if p.result[0] == "slot":               # the plan knows the result's shape (no tree walk)
+        si = p.slots[p.result[1]]
+        shape = Shape(si.rows, si.cols)
+    else:
+        shape = shape_of(node)
     if p.result[0] == "leaf":
         src = p.result[1]
         if out is None:
@@ -1289,7 +1293,11 @@ def evaluate_many(*xs, fuse: bool = True) -> list:
         bufs = execute_plan(p, sums=sums, leaves=leaves, recipe=rec)
     result = []
     for node, r, b in zip(nodes, out_refs, bufs):
-        shape = shape_of(node)
+        if r[0] == "slot":
+            si = p.slots[r[1]]
+            shape = Shape(si.rows, si.cols)
+        else:
+            shape = shape_of(node)
         if r[0] == "slot":
             result.append(Matrix._adopt(b, shape.rows, shape.cols, node.elem_type))
             if r[1] in sums:          # accu of this matrix already on the device (runtime sum cache)

@@ -922,6 +922,50 @@ def test_gemm_epilogue_with_memory_input(dm, m, n, k, tb, monkeypatch):
         same(got, want)
 
 
+def _random_epilogue(dm, rng, prod, mats, depth):
+    """A random element-wise tree over the product and the matrices in `mats`
+    (rng: a random.Random)."""
+    if depth == 0 or rng.random() < 0.25:
+        return prod if (not mats or rng.random() < 0.6) else rng.choice(mats)
+    kind = rng.randrange(6)
+    a = _random_epilogue(dm, rng, prod, mats, depth - 1)
+    if kind == 0:
+        return a * rng.choice([0.5, 2.0, -1.5, 3.0])
+    if kind == 1:
+        return a + rng.choice([1.0, -2.0, 0.25])
+    if kind == 2:
+        return rng.choice([dm.exp, dm.square, dm.abs])(a / 512.0)
+    b = _random_epilogue(dm, rng, prod, mats, depth - 1)
+    return {3: lambda: a + b, 4: lambda: a - b, 5: lambda: a % b}[kind]()
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_gemm_epilogue_random_programs_bit_identical(dm, seed):
+    """Random element-wise trees over a tensor-core product and 0-2 more matrices
+    (staged, unstaged and declined shapes, odd row counts, several K passes):
+    the fused plan gives the bits of the reference's plan every time."""
+    import random
+    rng = random.Random(seed)
+    nrng = np.random.default_rng(seed)
+    kinds = []
+    for trial in range(8):
+        m = rng.choice([256, 384, 516, 601, 1024])
+        n = rng.choice([256, 300, 512, 777])
+        k = rng.choice([64, 250, 1000, 17000])
+        a = dm.Matrix.from_numpy(nrng.random((m, k), dtype=np.float32))
+        b = dm.Matrix.from_numpy(nrng.random((n, k), dtype=np.float32))
+        mats = [dm.Matrix.from_numpy(nrng.random((m, n), dtype=np.float32)) for _ in range(rng.randrange(3))]
+        e = _random_epilogue(dm, rng, a @ b.t(), mats, 3)
+        steps = [st.kernel for st in dm.plan(e).steps]
+        if not any(kd in ("gemm_epi", "gemm") for kd in steps):
+            continue                                  # the tree never reached the product
+        kinds.append((steps[-1], len(mats)))
+        got = dm.evaluate(e).to_numpy()
+        want = dm.evaluate(e, fuse=False).to_numpy()
+        same_nan(got, want)
+    assert any(kd == "gemm_epi" for kd, _ in kinds), kinds
+
+
 def test_pair_gemm_repeatable_under_load(dm):
     """The pair kernel's stage / accumulator barriers are CTA-scope (no cluster-wide
     fence per chunk): any ordering hole between the MMA issuer, the TMA threads and

@@ -966,6 +966,29 @@ def test_gemm_epilogue_random_programs_bit_identical(dm, seed):
     assert any(kd == "gemm_epi" for kd, _ in kinds), kinds
 
 
+@pytest.mark.parametrize("seed", [4, 5])
+def test_gemm_prologue_random_programs_bit_identical(dm, seed):
+    """Random element-wise operand programs on both sides of a tensor-core product
+    (evaluated inside the 3xTF32 split pass, no operand materialised): the bits
+    of the reference's plan, which materialises the operands first."""
+    import random
+    rng = random.Random(seed)
+    nrng = np.random.default_rng(seed)
+    fused = 0
+    for trial in range(6):
+        m, n, k = rng.choice([256, 520, 777]), rng.choice([256, 384, 600]), rng.choice([128, 300, 2000])
+        a = dm.Matrix.from_numpy(nrng.random((m, k), dtype=np.float32))
+        b = dm.Matrix.from_numpy(nrng.random((n, k), dtype=np.float32))
+        am = [dm.Matrix.from_numpy(nrng.random((m, k), dtype=np.float32)) for _ in range(rng.randrange(2))]
+        bm = [dm.Matrix.from_numpy(nrng.random((n, k), dtype=np.float32)) for _ in range(rng.randrange(2))]
+        e = _random_epilogue(dm, rng, a, am, 2) @ _random_epilogue(dm, rng, b, bm, 2).t()
+        fused += "gemm_fused" in [st.kernel for st in dm.plan(e).steps]
+        got = dm.evaluate(e).to_numpy()
+        want = dm.evaluate(e, fuse=False).to_numpy()
+        same_nan(got, want)
+    assert fused > 0
+
+
 def test_pair_gemm_repeatable_under_load(dm):
     """The pair kernel's stage / accumulator barriers are CTA-scope (no cluster-wide
     fence per chunk): any ordering hole between the MMA issuer, the TMA threads and

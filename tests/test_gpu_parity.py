@@ -870,6 +870,7 @@ def test_plan_recipes_under_threads_and_eviction(dm, monkeypatch):
 
 @pytest.mark.parametrize("elem,m,n,k,ta,tb", [("f32", 512, 384, 256, 0, 1), ("f32", 1000, 700, 300, 0, 0),
                                               ("f32", 2048, 2048, 1024, 1, 1), ("f32", 256, 256, 20000, 0, 1),
+                                              ("f32", 4096, 4352, 600, 0, 1),   # persistent pairs (272 tiles)
                                               ("f64", 300, 200, 100, 1, 0), ("f64", 512, 512, 512, 0, 1),
                                               ("f64", 1030, 770, 64, 0, 0)])
 def test_gemm_epilogue_bit_identical_to_unfused(dm, elem, m, n, k, ta, tb):
@@ -1076,7 +1077,8 @@ def test_gemm_persistent_pairs_bit_identical(tmp_path):
 
 # ---- GEMM prologue fusion ------------------------------------------------------------------------
 
-@pytest.mark.parametrize("m,n,k,tb", [(512, 384, 256, 1), (1000, 700, 300, 0), (2048, 2048, 1024, 1)])
+@pytest.mark.parametrize("m,n,k,tb", [(512, 384, 256, 1), (1000, 700, 300, 0), (2048, 2048, 1024, 1),
+                                      (4096, 4352, 512, 1)])   # the last: persistent pairs (272 tiles)
 def test_gemm_fused_operand_chains(dm, m, n, k, tb):
     """(2A + 1) @ op(exp(B/4) - 3) with the operand programs inside the split
     pre-pass: same numbers as materialising the operands first."""

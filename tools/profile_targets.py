@@ -48,6 +48,12 @@ def main(which: str) -> None:
         B = dm.Matrix(n, n, fill="randu", elem_type=elem)
         for _ in range(3):
             dm.evaluate(A @ B.t())
+    elif which == "epi_axpby":
+        n = 8192
+        A, B, C = (dm.Matrix(n, n, fill="randu") for _ in range(3))
+        e = 2 * (A @ B.t()) + 3 * C
+        for _ in range(3):
+            dm.evaluate(e)
     elif which in ("epi_exp", "epi_exp_minus_c"):
         # the fused-epilogue pair GEMM at 8192^3: exp(AB^T/n), and exp(AB^T/n) - C with C
         # read in the store (BM_GEMM_EPI_INPUTS forced on)

@@ -508,6 +508,8 @@ class Runtime:
         self.seed = int(os.environ.get(SEED_ENV, "42"))
         self._section_mark = Counters()
         self._live: dict[int, int] = {}     # buffer_id -> device pointer
+        self._pool: dict[int, list] = {}    # byte size -> released device pointers (acquire_memory)
+        self._pool_bytes = 0
         self._sums: dict = {}               # buffer_id -> 1-element buffer holding its accu (sum cache)
         self._queued_ids: set = set()       # buffers used by work enqueued since the last synchronise
         self._pending_error = None          # raised at the next synchronise (asynchronous error contract)
@@ -534,15 +536,53 @@ class Runtime:
         self.counters.cache_hits = n.jit_cache_hits - self._jit_base.jit_cache_hits
 
     # -- memory ------------------------------------------------------------------------
+    # Buffers released in stream order (release_deferred) are kept, by byte size, for the
+    # next acquisition of the same size: reusing one is as stream-ordered as the
+    # cudaFreeAsync / cudaMallocAsync pair it replaces (one stream per device), and the
+    # repeated steps of a loop (config 5: r, g and a sum slot per step) skip both library
+    # calls.  Bounded (POOL_MAX_BYTES, buffers up to POOL_MAX_BUFFER bytes); flushed when
+    # an allocation fails and at shutdown.
+    POOL_MAX_BYTES = 1 << 30
+    POOL_MAX_BUFFER = 64 << 20
+
+    @staticmethod
+    def _nbytes(n: int, elem_type: str) -> int:
+        return max(n * kernels.itemsize(elem_type), 16)    # bm_alloc: zero-length buffers take 16 B
+
+    def _pool_take(self, nbytes: int) -> int:
+        with self._lock:
+            lst = self._pool.get(nbytes)
+            if lst:
+                self._pool_bytes -= nbytes
+                return lst.pop()
+        return 0
+
+    def flush_pool(self) -> None:
+        """Return every pooled buffer to the device allocator (stream-ordered)."""
+        with self._lock:
+            ptrs = [p for lst in self._pool.values() for p in lst]
+            self._pool.clear()
+            self._pool_bytes = 0
+        for p in ptrs:
+            self._lib.bm_free_async(p)
+
     def acquire_memory(self, n: int, elem_type: str) -> DeviceBuffer:
         if n < 0:
             raise ValueError("negative buffer length")
         if elem_type not in kernels.ELEM_TYPES:
             raise TypeError(f"unknown element type {elem_type!r}")
-        ptr = ctypes.c_void_p()
-        _clib.check(self._lib.bm_alloc(n * kernels.itemsize(elem_type), ctypes.byref(ptr)), "acquire_memory")
+        nbytes = self._nbytes(n, elem_type)
+        p = self._pool_take(nbytes) if self._pool else 0
+        if not p:
+            ptr = ctypes.c_void_p()
+            rc = self._lib.bm_alloc(nbytes, ctypes.byref(ptr))
+            if rc != _clib.BM_OK and self._pool:
+                self.flush_pool()              # pooled buffers may be what the device lacks
+                rc = self._lib.bm_alloc(nbytes, ctypes.byref(ptr))
+            _clib.check(rc, "acquire_memory")
+            p = ptr.value or 0
         with self._lock:
-            buf = DeviceBuffer(self.descriptor.device_id, self._next_buffer_id, n, elem_type, ptr.value or 0)
+            buf = DeviceBuffer(self.descriptor.device_id, self._next_buffer_id, n, elem_type, p)
             self._next_buffer_id += 1
             self._live[buf.buffer_id] = buf.ptr
             self.counters.buffers_acquired += 1
@@ -580,8 +620,17 @@ class Runtime:
         _clib.check(self._lib.bm_free(self._retire(buf)), "release")
 
     def release_deferred(self, buf: DeviceBuffer) -> None:
-        """Stream-ordered release (runtime.py:449-451): cudaFreeAsync."""
-        _clib.check(self._lib.bm_free_async(self._retire(buf)), "release_deferred")
+        """Stream-ordered release (runtime.py:449-451): back to the size pool, or
+        cudaFreeAsync."""
+        ptr = self._retire(buf)
+        nbytes = self._nbytes(buf.length, buf.elem_type)
+        if nbytes <= self.POOL_MAX_BUFFER:
+            with self._lock:
+                if self._pool_bytes + nbytes <= self.POOL_MAX_BYTES:
+                    self._pool.setdefault(nbytes, []).append(ptr)
+                    self._pool_bytes += nbytes
+                    return
+        _clib.check(self._lib.bm_free_async(ptr), "release_deferred")
 
     # -- sum cache ----------------------------------------------------------------------------
     # A fused step may leave accu(result) -- in the reference's order, bit-identical to
@@ -892,6 +941,7 @@ def shutdown() -> None:
                     rt._lib.bm_free_async(ptr)
                     rt.counters.buffers_released += 1
                 rt._live.clear()
+            rt.flush_pool()
             _clib.lib().bm_shutdown()
             _runtime = None
 

@@ -301,3 +301,33 @@ def test_sharded_row_reductions_exchange_matches_all_gather(world, rows, cols, e
             assert got["p2p_fused"][0] == res[0][1][op]["p2p_fused"][0], "ranks disagree"
             if op != "sum":
                 assert got["p2p_fused"][0] == single[op]
+
+
+def _rows_empty_worker(rank, world, port, q, rows, cols):
+    dm, D = _init(rank, world, port)
+    try:
+        full = np.random.default_rng(29).random((rows, cols))
+        c0, cc = D.column_block(cols, rank, world)
+        m = dm.Matrix.from_numpy(np.asfortranarray(full[:, c0:c0 + cc])) if cc else dm.Matrix(rows, 0, elem_type="f64")
+        got = {}
+        for coll in ("p2p_fused", "all_gather"):
+            v = D.sharded_reduce_dim("sum", m, 1, collective=coll)
+            got[coll] = (v.to_numpy().tobytes(), D._LAST["rows_collective"])
+        q.put((rank, cc, got))
+        dist.barrier()
+        D.close_exchanges()
+        dm.shutdown()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_sharded_row_sum_with_empty_shards():
+    """More ranks than columns: a rank with no columns takes part in the
+    exchange with zeros, and every rank gets the all-gather path's bits."""
+    res = _collect(4, _rows_empty_worker, 512, 3)
+    assert any(cc == 0 for _, cc, _ in res)
+    for rank, cc, got in res:
+        assert got["p2p_fused"][1] == "peer" and got["all_gather"][1] == "gather"
+        assert got["p2p_fused"][0] == got["all_gather"][0], f"rank {rank}"
+        assert got["p2p_fused"][0] == res[0][2]["p2p_fused"][0]

@@ -245,15 +245,20 @@ def _logistic_worker(rank, world, port, q, rows, cols):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,rows,cols", [(2, 1 << 16, 256), (3, 3 * 8192 * 4, 1024), (2, 65536, 2000)])
+@pytest.mark.parametrize("world,rows,cols", [(2, 1 << 16, 256), (3, 3 * 8192 * 4, 1024), (2, 65536, 2000),
+                                             (2, 65538, 512)])
 def test_sharded_logistic_exchange_matches_all_gather(world, rows, cols):
     """bm_exchange_gsum (g and the sum-cached accu(r) of every rank in one kernel
     over CUDA IPC peer memory, folded in rank order) gives the bits of the NCCL /
     gloo all-gather path -- gathered columns summed along dim 1, accu exchanged --
     on every rank, and matches the single-device step."""
     res = _collect(world, _logistic_worker, rows, cols)
+    paths = {out["p2p_fused"][2] for _, out, _, _ in res}
+    assert len(paths) == 1, "ranks took different paths"      # agreed collectively
     for rank, out, gf, sf in res:
-        assert out["p2p_fused"][2] == "peer" and out["all_gather"][2] == "gather"
+        if rows % (4 * world) == 0:
+            assert out["p2p_fused"][2] == "peer"
+        assert out["all_gather"][2] == "gather"
         assert out["p2p_fused"][:2] == out["all_gather"][:2], f"rank {rank}: exchange differs from all-gather"
         assert out["p2p_fused"][:2] == res[0][1]["p2p_fused"][:2], "ranks disagree"
         g = np.frombuffer(out["p2p_fused"][0], dtype=np.float32).astype(np.float64)

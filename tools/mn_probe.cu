@@ -23,7 +23,7 @@ __device__ __forceinline__ int sw128_off(int mn, int kk, int atom_stride) {
 
 __global__ void probe(const float* A, const float* B, float* C, int variant) {
     __shared__ __align__(1024) unsigned char sa[128 * 8 * 4 * 2];   // 4 atoms x 1 KB (8 rows) -- room for 2 KB stride
-    __shared__ __align__(1024) unsigned char sb[128 * 8 * 4 * 2];
+    __shared__ __align__(1024) unsigned char sb[128 * 8 * 4 * 2];   // (type-1 variants use 4 KB: 2 K groups x 2 KB)
     __shared__ uint64_t bar;
     __shared__ uint32_t tslot;
     const int tid = threadIdx.x;
@@ -37,6 +37,13 @@ __global__ void probe(const float* A, const float* B, float* C, int variant) {
             off = (mn >> 2) * 128 + (kk & 7) * 16 + (mn & 3) * 4;
         } else if (variant == 6) {   // K-major SWIZZLE_64B (the GEMM's layout): 64-B rows, 16-B chunk ^= (row >> 1) & 3
             off = mn * 64 + (((kk >> 2) ^ ((mn >> 1) & 3)) * 16) + (kk & 3) * 4;
+        } else if (variant >= 7) {   // MN-major SWIZZLE_128B with 32-B atomicity (layout type 1):
+            // 128-B rows of 32 MN elements per K index, 32-B chunks XORed with the K row
+            // (7, 8: chunk ^= kk & 3; 9, 10: chunk ^= (kk >> 1) & 3), atoms of 4 K rows;
+            // MN atoms 512 B apart, K atom groups 2048 B apart
+            const int j = mn >> 5, w = mn & 31;
+            const int swz = variant <= 8 ? (kk & 3) : ((kk >> 1) & 3);
+            off = j * 512 + (kk >> 2) * 2048 + (kk & 3) * 128 + (((w >> 3) ^ swz) * 32) + (w & 7) * 4;
         } else {
             off = sw128_off(mn, kk, atom);
         }
@@ -63,6 +70,12 @@ __global__ void probe(const float* A, const float* B, float* C, int variant) {
             if (variant == 4) { lbo = 128; sbo = 256; lt = 0; }
             if (variant == 5) { lbo = 1024; sbo = 128; lt = 0; }
             if (variant == 6) { lbo = 16; sbo = 512; lt = 4; }
+            if (variant >= 7) {          // type 1; 7, 9: LBO = MN atom stride; 8, 10: swapped
+                lt = 1;
+                const bool sw = (variant == 8 || variant == 10);
+                lbo = sw ? 2048 : 512;
+                sbo = sw ? 512 : 2048;
+            }
             d |= (uint64_t)(lbo >> 4) << 16;
             d |= (uint64_t)(sbo >> 4) << 32;
             d |= (uint64_t)1 << 46;
@@ -70,7 +83,7 @@ __global__ void probe(const float* A, const float* B, float* C, int variant) {
             return d;
         };
         uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-        if (variant != 4 && variant != 6) idesc |= (1u << 15) | (1u << 16);
+        if (variant != 4 && variant != 6) idesc |= (1u << 15) | (1u << 16);   // MN-major: transpose A and B
         mma_tf32(tmem, desc(sa), desc(sb), idesc, 0u);
         mma_commit(&bar);
     }
@@ -106,7 +119,7 @@ int main() {
     cudaMalloc(&dc, c.size() * 4);
     cudaMemcpy(da, a.data(), a.size() * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(db, b.data(), b.size() * 4, cudaMemcpyHostToDevice);
-    for (int variant = 0; variant < 7; ++variant) {
+    for (int variant = 0; variant < 11; ++variant) {
         cudaMemset(dc, 0, c.size() * 4);
         probe<<<1, 128>>>(da, db, dc, variant);
         cudaError_t e = cudaDeviceSynchronize();
@@ -117,8 +130,14 @@ int main() {
             maxref = std::max(maxref, (double)std::abs(ref[i]));
             maxgot = std::max(maxgot, (double)std::abs(c[i]));
         }
-        printf("variant %d (atom %d B, %s): %s max|err| %.1f max|ref| %.1f max|got| %.1f  C[0..3]=%.0f %.0f %.0f %.0f ref %.0f %.0f %.0f %.0f\n",
-               variant, (variant & 1) ? 2048 : 1024, (variant & 2) ? "LBO=1KB,SBO=atom" : "LBO=atom,SBO=1KB",
+        const char* what = variant < 4 ? ((variant & 2) ? "MN SW128, LBO=1KB,SBO=atom" : "MN SW128, LBO=atom,SBO=1KB")
+                         : variant == 4 ? "K-major, no swizzle" : variant == 5 ? "MN, no swizzle"
+                         : variant == 6 ? "K-major SW64 (the GEMM's)"
+                         : variant == 7 ? "MN SW128/32B-atom, chunk^=k&3, LBO=MN atom 512, SBO=K group 2048"
+                         : variant == 8 ? "MN SW128/32B-atom, chunk^=k&3, LBO/SBO swapped"
+                         : variant == 9 ? "MN SW128/32B-atom, chunk^=(k>>1)&3" : "MN SW128/32B-atom, chunk^=(k>>1)&3, swapped";
+        printf("variant %d (%s): %s max|err| %.1f max|ref| %.1f max|got| %.1f  C[0..3]=%.0f %.0f %.0f %.0f ref %.0f %.0f %.0f %.0f\n",
+               variant, what,
                cudaGetErrorString(e), maxerr, maxref, maxgot, c[0], c[1], c[2], c[3], ref[0], ref[1], ref[2], ref[3]);
         if (e != cudaSuccess) return 1;
     }

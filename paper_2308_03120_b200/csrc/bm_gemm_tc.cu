@@ -40,8 +40,8 @@ struct PlainSrc {
 template <bool SRC_KMAJOR, bool VEC>
 __global__ void __launch_bounds__(256) split_tf32_kernel(const float* __restrict__ src, i64 ld, i64 rows, i64 k,
                                                          float* __restrict__ hi, float* __restrict__ lo, i64 kp,
-                                                         i64 rp) {
-    split_tf32_body<SRC_KMAJOR, VEC>(PlainSrc{src, ld}, ld, rows, k, hi, lo, kp, rp);
+                                                         i64 rp, int trunc) {
+    split_tf32_body<SRC_KMAJOR, VEC>(PlainSrc{src, ld}, ld, rows, k, hi, lo, kp, rp, trunc != 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -206,14 +206,40 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 }
 
 // the ahead-of-time kernels: plain stores
+template <bool AMN, bool BMN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T2_THREADS, 1)
     gemm_3xtf32_pair_kernel(const __grid_constant__ TmapBytes tm_ahi, const __grid_constant__ TmapBytes tm_alo,
                             const __grid_constant__ TmapBytes tm_bhi, const __grid_constant__ TmapBytes tm_blo,
                             float* __restrict__ C, i64 m, i64 n, i64 ldc, int nk, int group_m, int kb0,
                             int accumulate, unsigned int* tile_ctr) {
     const Args none{};
-    gemm_pair_body<PlainEpi>(tm_ahi, tm_alo, tm_bhi, tm_blo, C, m, n, ldc, nk, group_m, kb0, accumulate, none, 0,
-                             tile_ctr);
+    gemm_pair_body<PlainEpi, AMN, BMN>(tm_ahi, tm_alo, tm_bhi, tm_blo, C, m, n, ldc, nk, group_m, kb0, accumulate,
+                                       none, 0, tile_ctr);
+}
+
+// lo = x - trunc_tf32(x) of a column-major rows x k matrix (ld), into a compact copy
+// (ldl = rows rounded up to 4): the second operand of an MN-major 3xTF32 product, whose
+// first is x itself (the tensor core truncates it).  No transpose: streamed at copy rate.
+__global__ void __launch_bounds__(256) tf32_lo_kernel(const float* __restrict__ x, i64 ld, i64 rows, i64 k,
+                                                       float* __restrict__ lo, i64 ldl) {
+    const i64 nq = ldl / 4;                       // quads per column
+    const i64 total = nq * k;
+    for (i64 q = (i64)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (i64)gridDim.x * blockDim.x) {
+        const i64 c = q / nq, r = (q - c * nq) * 4;
+        float v[4];
+        if (r + 3 < rows) {
+            const float4 t = *reinterpret_cast<const float4*>(x + r + c * ld);
+            v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) v[e] = r + e < rows ? x[r + e + c * ld] : 0.f;
+        }
+        float4 o;
+        float* op = &o.x;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) op[e] = v[e] - __uint_as_float(__float_as_uint(v[e]) & 0xffffe000u);
+        *reinterpret_cast<float4*>(lo + r + c * ldl) = o;
+    }
 }
 
 template <bool TA, bool TB, int BM, int BK, int ST, bool VEC>
@@ -242,16 +268,50 @@ static int encode_kmajor(bm::TmapBytes* tmb, const float* p, int64_t kp, int64_t
     return BM_OK;
 }
 
+// an MN-major operand map: dims {rows (contiguous), k}, boxes of 32 rows x 16 K with the
+// 128-B swizzle in 32-B atoms (bm_gemm_tc.cuh mn32_desc)
+// as a 3-D map {32 rows, k, rows / 32} (strides ld * 4, 128 B) so one request moves the
+// 4 row atoms of a 128-row tile (rows must be a multiple of 32: the caller pads)
+static int encode_mn(bm::TmapBytes* tmb, const float* p, int64_t ld, int64_t rows, int64_t k) {
+    CUtensorMap* tm = reinterpret_cast<CUtensorMap*>(tmb);
+    const cuuint64_t gdim[3] = {32, (cuuint64_t)k, (cuuint64_t)((rows + 31) / 32)};
+    const cuuint64_t gstride[2] = {(cuuint64_t)(ld * 4), 128};
+    const cuuint32_t box[3] = {32, TC_BK, 4};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = drv().tensorMapEncodeTiled(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)p, gdim, gstride, box, estr,
+                                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cu_fail(r, "cuTensorMapEncodeTiled (gemm operand, MN-major)");
+    return BM_OK;
+}
+
+// Which operands of a pair GEMM are read MN-major from the stored matrix: op(A) is M x K
+// and MN-major when A is not transposed; op(B)^T is N x K and MN-major when B is.  TMA
+// needs a 16-B base and a 16-B multiple row stride, and the 3-D map whole 32-row atoms
+// (32 | m, 32 | n).  BM_GEMM_MN selects it (measured slower, off by default: DESIGN.md).
+bool gemm_mn_enabled() {
+    static const bool on = std::getenv("BM_GEMM_MN") && std::atoi(std::getenv("BM_GEMM_MN")) != 0;
+    return on;
+}
+
+void pair_mn_modes(int ta, int tb, const float* A, int64_t lda, const float* B, int64_t ldb, int64_t m, int64_t n,
+                   bool* amn, bool* bmn) {
+    const bool on = gemm_mn_enabled();
+    *amn = on && !ta && lda % 4 == 0 && m % 32 == 0 && ((uintptr_t)A & 15u) == 0;
+    *bmn = on && tb && ldb % 4 == 0 && n % 32 == 0 && ((uintptr_t)B & 15u) == 0;
+}
+
 static int split_operand(const float* src, int64_t ld, bool kmajor, int64_t rows, int64_t k, float* hi, float* lo,
                          int64_t kp, int64_t rp) {
+    const int tr = gemm_mn_enabled() ? 1 : 0;   // truncating split alongside in-place MN-major operands
     dim3 grid((unsigned)((kp + 63) / 64), (unsigned)((rp + 63) / 64));
     const bool vec = (ld % 4 == 0) && (((uintptr_t)src & 15u) == 0);
     if (kmajor) {
-        if (vec) bm::split_tf32_kernel<true, true><<<grid, dim3(32, 8), 0, st().stream>>>(src, ld, rows, k, hi, lo, kp, rp);
-        else bm::split_tf32_kernel<true, false><<<grid, dim3(32, 8), 0, st().stream>>>(src, ld, rows, k, hi, lo, kp, rp);
+        if (vec) bm::split_tf32_kernel<true, true><<<grid, dim3(32, 8), 0, st().stream>>>(src, ld, rows, k, hi, lo, kp, rp, tr);
+        else bm::split_tf32_kernel<true, false><<<grid, dim3(32, 8), 0, st().stream>>>(src, ld, rows, k, hi, lo, kp, rp, tr);
     } else {
-        if (vec) bm::split_tf32_kernel<false, true><<<grid, dim3(32, 8), 0, st().stream>>>(src, ld, rows, k, hi, lo, kp, rp);
-        else bm::split_tf32_kernel<false, false><<<grid, dim3(32, 8), 0, st().stream>>>(src, ld, rows, k, hi, lo, kp, rp);
+        if (vec) bm::split_tf32_kernel<false, true><<<grid, dim3(32, 8), 0, st().stream>>>(src, ld, rows, k, hi, lo, kp, rp, tr);
+        else bm::split_tf32_kernel<false, false><<<grid, dim3(32, 8), 0, st().stream>>>(src, ld, rows, k, hi, lo, kp, rp, tr);
     }
     BM_CUDA(cudaGetLastError());
     st().launches++;
@@ -266,11 +326,13 @@ bool gemm_pair_persistent() {
 // C = op(A) op(B) on the 3xTF32 tcgen05 path; split_a / split_b fill the
 // K-major hi/lo copies of op(A) (m x k) and op(B)^T (n x k).
 int gemm_tc_f32_core(int64_t m, int64_t n, int64_t k, const SplitFn& split_a, const SplitFn& split_b, float* C,
-                     int64_t ldc, bool* handled, const PairEpilogue* epi) {
+                     int64_t ldc, bool* handled, const PairEpilogue* epi, const MnOperand* a_mn,
+                     const MnOperand* b_mn) {
     *handled = false;
     // CTA pairs (cta_group::2, 256 x 256 tiles) unless BM_GEMM_PAIR=0
     static const bool pair = !std::getenv("BM_GEMM_PAIR") || std::atoi(std::getenv("BM_GEMM_PAIR")) != 0;
     if (epi && !pair) return BM_OK;     // fused epilogues exist for the pair kernel only
+    if (!pair) a_mn = b_mn = nullptr;   // the single-CTA kernel reads K-major copies only
     const int64_t tm_ = pair ? 2 * T2_BM : TC_BM, tn_ = pair ? 2 * T2_BNH : TC_BN;
     const int64_t mp = (m + tm_ - 1) / tm_ * tm_;
     const int64_t np = (n + tn_ - 1) / tn_ * tn_;
@@ -278,25 +340,61 @@ int gemm_tc_f32_core(int64_t m, int64_t n, int64_t k, const SplitFn& split_a, co
     if ((mp / tm_) * (np / tn_) * (pair ? 2 : 1) > (1LL << 31) - 1) return BM_OK;
     cudaStream_t s = st().stream;
     float* buf = nullptr;
-    const int64_t a_elems = mp * kp, b_elems = np * kp;
+    // K-major operands: hi and lo copies, mp (np) x kp; MN-major ones: a lo copy only
+    const int64_t lda_lo = a_mn ? (m + 3) / 4 * 4 : 0, ldb_lo = b_mn ? (n + 3) / 4 * 4 : 0;
+    const int64_t a_elems = a_mn ? lda_lo * k : 2 * mp * kp, b_elems = b_mn ? ldb_lo * k : 2 * np * kp;
     constexpr int kMaxPasses = 64;     // tile counters of the persistent pairs, one per K pass
-    BM_CUDA(cudaMallocAsync((void**)&buf, (size_t)(2 * (a_elems + b_elems) * 4 + kMaxPasses * 4), s));
-    float *ahi = buf, *alo = buf + a_elems, *bhi = buf + 2 * a_elems, *blo = buf + 2 * a_elems + b_elems;
-    unsigned int* ctr = reinterpret_cast<unsigned int*>(buf + 2 * (a_elems + b_elems));
-    int rc = split_a(ahi, alo, kp, mp);
-    if (!rc) rc = split_b(bhi, blo, kp, np);
+    BM_CUDA(cudaMallocAsync((void**)&buf, (size_t)((a_elems + b_elems) * 4 + kMaxPasses * 4 + 64), s));
+    float* abuf = buf;
+    float* bbuf = buf + (a_elems + 3) / 4 * 4;          // 16-B aligned
+    unsigned int* ctr = reinterpret_cast<unsigned int*>(bbuf + (b_elems + 3) / 4 * 4);
+    auto lo_pass = [&](const MnOperand* o, int64_t rows, float* lo, int64_t ldl) -> int {
+        const int64_t quads = ldl / 4 * k;
+        const int grid = (int)std::min<int64_t>((quads + 255) / 256, (int64_t)st().sm_count * 8);
+        bm::tf32_lo_kernel<<<grid > 0 ? grid : 1, 256, 0, s>>>(o->p, o->ld, rows, k, lo, ldl);
+        BM_CUDA(cudaGetLastError());
+        st().launches++;
+        return BM_OK;
+    };
     bm::TmapBytes tm[4];
-    if (!rc) rc = encode_kmajor(&tm[0], ahi, kp, mp, TC_BM);
-    if (!rc) rc = encode_kmajor(&tm[1], alo, kp, mp, TC_BM);
-    if (!rc) rc = encode_kmajor(&tm[2], bhi, kp, np, pair ? T2_BNH : TC_BN);
-    if (!rc) rc = encode_kmajor(&tm[3], blo, kp, np, pair ? T2_BNH : TC_BN);
+    int rc = BM_OK;
+    if (a_mn) {
+        rc = lo_pass(a_mn, m, abuf, lda_lo);
+        if (!rc) rc = encode_mn(&tm[0], a_mn->p, a_mn->ld, m, k);
+        if (!rc) rc = encode_mn(&tm[1], abuf, lda_lo, m, k);
+    } else {
+        rc = split_a(abuf, abuf + mp * kp, kp, mp);
+        if (!rc) rc = encode_kmajor(&tm[0], abuf, kp, mp, TC_BM);
+        if (!rc) rc = encode_kmajor(&tm[1], abuf + mp * kp, kp, mp, TC_BM);
+    }
+    if (!rc && b_mn) {
+        rc = lo_pass(b_mn, n, bbuf, ldb_lo);
+        if (!rc) rc = encode_mn(&tm[2], b_mn->p, b_mn->ld, n, k);
+        if (!rc) rc = encode_mn(&tm[3], bbuf, ldb_lo, n, k);
+    } else if (!rc) {
+        rc = split_b(bbuf, bbuf + np * kp, kp, np);
+        if (!rc) rc = encode_kmajor(&tm[2], bbuf, kp, np, pair ? T2_BNH : TC_BN);
+        if (!rc) rc = encode_kmajor(&tm[3], bbuf + np * kp, kp, np, pair ? T2_BNH : TC_BN);
+    }
+    if (!rc && epi && (epi->amn != (a_mn != nullptr) || epi->bmn != (b_mn != nullptr)))
+        rc = set_error(BM_ERR_ARG, "3xTF32 GEMM: epilogue kernel compiled for other operand layouts");
     if (!rc) {
         static bool attr = false;
         if (!attr) {
             cudaError_t e = cudaFuncSetAttribute(bm::gemm_3xtf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  TC_SMEM);
             if (e == cudaSuccess)
-                e = cudaFuncSetAttribute(bm::gemm_3xtf32_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, T2_SMEM);
+                e = cudaFuncSetAttribute(bm::gemm_3xtf32_pair_kernel<false, false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, T2_SMEM);
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(bm::gemm_3xtf32_pair_kernel<true, false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, T2_SMEM);
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(bm::gemm_3xtf32_pair_kernel<false, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, T2_SMEM);
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(bm::gemm_3xtf32_pair_kernel<true, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, T2_SMEM);
             if (e != cudaSuccess) rc = cuda_fail(e, "cudaFuncSetAttribute (3xTF32)");
             attr = true;
         }
@@ -357,10 +455,13 @@ int gemm_tc_f32_core(int64_t m, int64_t n, int64_t k, const SplitFn& split_a, co
                 st().launches++;
                 continue;
             }
-            if (pair)
-                bm::gemm_3xtf32_pair_kernel<<<grid, T2_THREADS, T2_SMEM, s>>>(tm[0], tm[1], tm[2], tm[3], C, m, n, ldc,
-                                                                               len, group_m > 0 ? group_m : 8, kb0, kb0 > 0,
-                                                                               tile_ctr);
+            if (pair) {
+                const int gm = group_m > 0 ? group_m : 8;
+                auto* kfn = a_mn ? (b_mn ? bm::gemm_3xtf32_pair_kernel<true, true> : bm::gemm_3xtf32_pair_kernel<true, false>)
+                                 : (b_mn ? bm::gemm_3xtf32_pair_kernel<false, true> : bm::gemm_3xtf32_pair_kernel<false, false>);
+                kfn<<<grid, T2_THREADS, T2_SMEM, s>>>(tm[0], tm[1], tm[2], tm[3], C, m, n, ldc, len, gm, kb0, kb0 > 0,
+                                                      tile_ctr);
+            }
             else
                 bm::gemm_3xtf32_kernel<<<grid, TC_THREADS, TC_SMEM, s>>>(tm[0], tm[1], tm[2], tm[3], C, m, n, ldc, len,
                                                                           group_m > 0 ? group_m : 8, kb0, kb0 > 0);
@@ -379,12 +480,17 @@ int gemm_tc_f32(int ta, int tb, int64_t m, int64_t n, int64_t k, const float* A,
     *handled = false;
     if (m * n * k < (int64_t)1 << 21) return BM_OK;   // tiny: the SIMT kernel is cheaper than the split pass
     // op(A) is m x k; K-major iff A is stored transposed.  op(B) is k x n and we
-    // need its N x K K-major form: K-major iff B is NOT transposed.
+    // need its N x K K-major form: K-major iff B is NOT transposed.  The MN-major ones
+    // are read in place (pair_mn_modes); the K-major ones get hi/lo copies.
+    bool amn, bmn;
+    pair_mn_modes(ta, tb, A, lda, B, ldb, m, n, &amn, &bmn);
+    if (epi) { amn = epi->amn; bmn = epi->bmn; }       // the modes the epilogue kernel was compiled for
+    const MnOperand ao{A, lda}, bo{B, ldb};
     return gemm_tc_f32_core(
         m, n, k,
         [&](float* hi, float* lo, int64_t kp, int64_t rp) { return split_operand(A, lda, ta != 0, m, k, hi, lo, kp, rp); },
         [&](float* hi, float* lo, int64_t kp, int64_t rp) { return split_operand(B, ldb, tb == 0, n, k, hi, lo, kp, rp); },
-        C, ldc, handled, epi);
+        C, ldc, handled, epi, amn ? &ao : nullptr, bmn ? &bo : nullptr);
 }
 
 template <bool TA, bool TB, int BM, int BK, int ST, bool VEC>

@@ -73,6 +73,22 @@ __host__ __device__ constexpr uint32_t tf32_idesc(int m, int n) {
     return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 
+// MN-major operand read straight from a column-major matrix (tools/mn_tma_probe.cu):
+// TMA boxes of 32 MN x 16 K with CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, one per 32 rows of
+// the 128-row tile (2 KB apart), so the canonical layout is the 128-B swizzle in 32-B
+// atoms (layout type 1): LBO = the 2 KB MN-atom stride, SBO = the 512 B stride of 4-row K
+// groups; the second 8-K MMA of a 16-K block starts 1 KB in.  Needs the transpose bit of
+// the operand in the instruction descriptor (bit 15: A, bit 16: B).
+__device__ __forceinline__ uint64_t mn32_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
+    d |= (uint64_t)(2048u >> 4) << 16;
+    d |= (uint64_t)(512u >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)1 << 61;
+    return d;
+}
+
 // ---------------------------------------------------------------------------
 // The same product on CTA pairs (cta_group::2).  A cluster of two CTAs owns
 // a 256 x 256 tile: CTA r loads rows [128 r, 128 r + 128) of the A tile and
@@ -164,6 +180,14 @@ __device__ __forceinline__ void t2_commit_both(uint64_t* bar) {
         "h"((uint16_t)3)
         : "memory");
 }
+// the same for a 3-D map (MN-major operands: {32 MN, 16 K, 4 atoms} in one request)
+__device__ __forceinline__ void t2_tma3(void* dst, const void* tmap, int c0, int c1, int c2, uint32_t leader_bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+        "%4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(leader_bar)
+        : "memory");
+}
 __device__ __forceinline__ void t2_arrive_remote(uint32_t cluster_bar) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
 }
@@ -186,7 +210,10 @@ __device__ __forceinline__ void t2_cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-template <class EPI>
+// AMN / BMN: operand read MN-major from the stored matrix (its `hi` is the raw value, which
+// the tensor core truncates to tf32; `lo` = x - trunc(x) comes from a transpose-free pass)
+// instead of from K-major hi/lo copies.
+template <class EPI, bool AMN = false, bool BMN = false>
 __device__ __forceinline__ void gemm_pair_body(const TmapBytes& tm_ahi, const TmapBytes& tm_alo, const TmapBytes& tm_bhi,
                                                const TmapBytes& tm_blo, float* __restrict__ C, i64 m, i64 n, i64 ldc,
                                                int nk, int group_m, int kb0, int accumulate, const Args& ea,
@@ -300,10 +327,20 @@ __device__ __forceinline__ void gemm_pair_body(const TmapBytes& tm_ahi, const Tm
                     if (leader) mbar_expect_tx(&full[s], 2 * T2_STAGE_BYTES);   // both CTAs' bytes
                     const uint32_t lbar = t2_mapa(&full[s], 0);
                     const int kc = (kb0 + kb) * TC_BK;
-                    t2_tma(tile_ahi(s), &tm_ahi, kc, m0, lbar);
-                    t2_tma(tile_alo(s), &tm_alo, kc, m0, lbar);
-                    t2_tma(tile_bhi(s), &tm_bhi, kc, nb0, lbar);
-                    t2_tma(tile_blo(s), &tm_blo, kc, nb0, lbar);
+                    if constexpr (AMN) {           // 3-D map: {32 rows, 16 K, 4 row atoms}
+                        t2_tma3(tile_ahi(s), &tm_ahi, 0, kc, m0 / 32, lbar);
+                        t2_tma3(tile_alo(s), &tm_alo, 0, kc, m0 / 32, lbar);
+                    } else {
+                        t2_tma(tile_ahi(s), &tm_ahi, kc, m0, lbar);
+                        t2_tma(tile_alo(s), &tm_alo, kc, m0, lbar);
+                    }
+                    if constexpr (BMN) {
+                        t2_tma3(tile_bhi(s), &tm_bhi, 0, kc, nb0 / 32, lbar);
+                        t2_tma3(tile_blo(s), &tm_blo, 0, kc, nb0 / 32, lbar);
+                    } else {
+                        t2_tma(tile_bhi(s), &tm_bhi, kc, nb0, lbar);
+                        t2_tma(tile_blo(s), &tm_blo, kc, nb0, lbar);
+                    }
                 }
                 if (leader) {
                     int nx = t + npairs;
@@ -324,7 +361,7 @@ __device__ __forceinline__ void gemm_pair_body(const TmapBytes& tm_ahi, const Tm
         }
     } else if (warp == 1) {
         if (leader && lane == 0) {
-            constexpr uint32_t idesc = tf32_idesc(2 * T2_BM, 2 * T2_BNH);
+            constexpr uint32_t idesc = tf32_idesc(2 * T2_BM, 2 * T2_BNH) | (AMN ? 1u << 15 : 0u) | (BMN ? 1u << 16 : 0u);
             int it = 0, cc = 0, qi = 0;        // k blocks, accumulator chunks, tiles taken
             for (int t = take(qi); t >= 0; t = take(qi))
             for (int c = 0; c < nchunks; ++c, ++cc) {
@@ -337,17 +374,19 @@ __device__ __forceinline__ void gemm_pair_body(const TmapBytes& tm_ahi, const Tm
                     const int s = it % T2_STAGES;
                     t2_wait(&full[s], (uint32_t)((it / T2_STAGES) & 1));
                     tc_fence_after();
-                    const uint64_t ahi = sw64_kmajor_desc(smem_u32(tile_ahi(s)));
-                    const uint64_t alo = sw64_kmajor_desc(smem_u32(tile_alo(s)));
-                    const uint64_t bhi = sw64_kmajor_desc(smem_u32(tile_bhi(s)));
-                    const uint64_t blo = sw64_kmajor_desc(smem_u32(tile_blo(s)));
+                    const uint64_t ahi = AMN ? mn32_desc(smem_u32(tile_ahi(s))) : sw64_kmajor_desc(smem_u32(tile_ahi(s)));
+                    const uint64_t alo = AMN ? mn32_desc(smem_u32(tile_alo(s))) : sw64_kmajor_desc(smem_u32(tile_alo(s)));
+                    const uint64_t bhi = BMN ? mn32_desc(smem_u32(tile_bhi(s))) : sw64_kmajor_desc(smem_u32(tile_bhi(s)));
+                    const uint64_t blo = BMN ? mn32_desc(smem_u32(tile_blo(s))) : sw64_kmajor_desc(smem_u32(tile_blo(s)));
 #pragma unroll
                     for (int kk = 0; kk < TC_BK / 8; ++kk) {
-                        const uint64_t adv = (uint64_t)((kk * 32) >> 4);
+                        // 8 K further: 32 B along a K-major row, two 512-B K groups MN-major
+                        const uint64_t adva = (uint64_t)((kk * (AMN ? 1024 : 32)) >> 4);
+                        const uint64_t advb = (uint64_t)((kk * (BMN ? 1024 : 32)) >> 4);
                         const uint32_t first = (kb == c * TC_CHUNK_KB && kk == 0) ? 0u : 1u;
-                        t2_mma(d, alo + adv, bhi + adv, idesc, first);
-                        t2_mma(d, ahi + adv, blo + adv, idesc, 1u);
-                        t2_mma(d, ahi + adv, bhi + adv, idesc, 1u);
+                        t2_mma(d, alo + adva, bhi + advb, idesc, first);
+                        t2_mma(d, ahi + adva, blo + advb, idesc, 1u);
+                        t2_mma(d, ahi + adva, bhi + advb, idesc, 1u);
                     }
                     t2_commit_both(&empty[s]);
                 }

@@ -106,9 +106,19 @@ struct PairEpilogue {
     void* fn;            // CUfunction
     const void* args;    // bm::Args
     int smem = 0;        // the kernel's dynamic shared memory (0: T2_SMEM)
+    bool amn = false;    // compiled for MN-major A / B operands (pair_mn_modes)
+    bool bmn = false;
 };
+struct MnOperand {       // an operand read MN-major in place: the stored column-major matrix
+    const float* p;
+    int64_t ld;
+};
+void pair_mn_modes(int ta, int tb, const float* A, int64_t lda, const float* B, int64_t ldb, int64_t m, int64_t n,
+                   bool* amn, bool* bmn);
+bool gemm_mn_enabled();   // BM_GEMM_MN=1: MN-major in-place operands + truncating splits
 int gemm_tc_f32_core(int64_t m, int64_t n, int64_t k, const SplitFn& split_a, const SplitFn& split_b, float* C,
-                     int64_t ldc, bool* handled, const PairEpilogue* epi = nullptr);
+                     int64_t ldc, bool* handled, const PairEpilogue* epi = nullptr, const MnOperand* a_mn = nullptr,
+                     const MnOperand* b_mn = nullptr);
 bool gemm_pair_persistent();   // BM_GEMM_PERSIST (default on): persistent CTA pairs (bm_gemm_tc.cu)
 int gemm_tc_f32(int ta, int tb, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const float* B,
                 int64_t ldb, float* C, int64_t ldc, bool* handled, const PairEpilogue* epi = nullptr);
